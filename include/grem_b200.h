@@ -1,0 +1,154 @@
+/*
+ * grem_b200.h — C ABI of libgrem_b200.so, the B200-native GREM partitioner.
+ *
+ * Drop-in boundary for the reference's GREM path (streamcut, pure Python;
+ * paths below are relative to /root/reference/pkg/src/streamcut/).  Plain
+ * pointers and sizes only; no torch types.  A reference-side binding (ctypes)
+ * is shown in INTEGRATION.md; the package's own binding is
+ * paper_2502_17846_b200/_abi.py.
+ *
+ * Conventions
+ *   - return 0 on success; GREM_E_FORMAT mirrors streamcut.errors.FormatError,
+ *     GREM_E_CAPACITY mirrors CapacityError (errors.py:4-13), GREM_E_CUDA is a
+ *     CUDA/NCCL failure.  grem_last_error() returns a thread-local message.
+ *   - edge arrays are (src, dst) u32 pairs in file order (GRPE payload,
+ *     edgefile.py:1-14); `edges_on_device` says whether the pointer is device
+ *     memory of the context's GPU (no copy) or host memory (chunked,
+ *     double-buffered H2D inside the call).
+ *   - node ids must be < num_nodes < 2^31 (larger id spaces are rejected with
+ *     GREM_E_FORMAT; model.py:18 allows 64-bit ids, no benchmark shape needs
+ *     them).
+ *   - the caller owns every buffer it passes; the context owns device state.
+ */
+#ifndef GREM_B200_H
+#define GREM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GREM_OK 0
+#define GREM_E_FORMAT 1
+#define GREM_E_CAPACITY 2
+#define GREM_E_CUDA 3
+#define GREM_E_NOMEM 4
+#define GREM_E_CALLBACK 5
+
+typedef struct grem_ctx grem_ctx;
+
+/* GremConfig + SeedConfig (grem.py:45-75, seed.py:23-33).  chunk_edges > 0
+ * selects an absolute chunk size; otherwise chunk_frac (default 0.1) is used
+ * exactly as ChunkPlan.plan does (edgefile.py:338-349). */
+typedef struct {
+    int64_t chunk_edges;
+    double chunk_frac;
+    double capacity_slack;
+    int32_t refine;
+    int32_t passes;
+    int32_t seed_algo;               /* 0 = bfs_grow, 1 = random (needs hooks.seed) */
+    int32_t seed_refinement_passes;  /* SeedConfig.refinement_passes */
+} grem_config;
+
+/* CutReport (model.py:115-132).  partition_sizes is a caller buffer of
+ * sizes_cap entries; num_parts = max label + 1 (grem.py:243).  The float
+ * fields (cut_fraction, balance_ratio) are derived by the caller from these
+ * integers with the reference's own expressions (grem.py:245-251). */
+typedef struct {
+    int64_t total_edges;
+    int64_t cut_edges;
+    int64_t num_parts;
+    int64_t* partition_sizes;
+    int64_t sizes_cap;
+} grem_report;
+
+/* seed_bisect(..., algorithm="random") labels (seed.py:48-52) are drawn by
+ * numpy's PCG64 on the host: the library asks for them through this hook. */
+typedef int (*grem_seed_fn)(int64_t n_chunk_nodes, int8_t* labels_out, void* user);
+/* bisect(on_chunk=...) (grem.py:219-221): called after every chunk with the
+ * live sizes; grem_state_parts() may be called from inside it. */
+typedef int (*grem_chunk_fn)(const int64_t* sizes, void* user);
+/* ResidencyMeter (edgefile.py:352-368): +n on acquire, -n on release, called
+ * with the reference's stream_chunks timing (edgefile.py:384-391,453-462). */
+typedef void (*grem_meter_fn)(int64_t delta_edges, void* user);
+
+typedef struct {
+    grem_seed_fn seed;
+    grem_chunk_fn on_chunk;
+    grem_meter_fn meter;
+    void* user;
+} grem_hooks;
+
+/* Per-call statistics (diagnostics; zeroed per call). */
+typedef struct {
+    int64_t chunks;          /* chunks processed (all passes, all bisections) */
+    int64_t rounds;          /* fixpoint rounds summed over non-seed chunks */
+    int64_t max_rounds;      /* worst chunk */
+    int64_t visits;          /* chunk-node visits (sum of N_c) */
+    int64_t walk_steps;      /* sequential sizes-chain repairs */
+    int64_t seed_bfs_levels; /* BFS levels on the boundary component */
+    int64_t bisections;
+    int64_t kernels;         /* kernel launches issued */
+    double ms_total;         /* device time of the call (CUDA events) */
+} grem_stats;
+
+/* ------------------------------------------------------------------ life */
+grem_ctx* grem_create(int device);
+void grem_destroy(grem_ctx* ctx);
+const char* grem_last_error(void);
+int grem_get_stats(grem_ctx* ctx, grem_stats* out);
+
+/* --------------------------------------------------------------- the path */
+
+/* bisect (grem.py:192-224).  capacity <= 0 => default_capacity(n, slack)
+ * (grem.py:78-79).  labels_out: n int32 in {0,1}.  rep may be NULL (the
+ * count_cuts pass is then skipped, as partition() discards it). */
+int grem_bisect_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                    int edges_on_device, const grem_config* cfg, int64_t capacity,
+                    const grem_hooks* hooks, int32_t* labels_out, grem_report* rep);
+
+/* partition (grem.py:277-319): p a power of two >= 2; level capacity from the
+ * original node count; recursion over device-resident induced subgraphs;
+ * final count_cuts on the original edges. */
+int grem_partition_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                       int edges_on_device, int64_t p, const grem_config* cfg, const grem_hooks* hooks,
+                       int32_t* labels_out, grem_report* rep);
+
+/* count_cuts (grem.py:227-252).  labels_on_device as for edges. */
+int grem_count_cuts_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                        int edges_on_device, const int32_t* labels, int labels_on_device,
+                        grem_report* rep);
+
+/* File front ends: stream a GRPE u32 file (edgefile.py:107-126,186-219)
+ * through two pinned chunk buffers into HBM (the ingest subsystem), honouring
+ * the meter hook, then run the path.  64-bit-id and text files are parsed by
+ * the Python layer and passed to the pointer entry points above. */
+int grem_bisect_file(grem_ctx* ctx, const char* path, const grem_config* cfg, int64_t capacity,
+                     const grem_hooks* hooks, int32_t* labels_out, grem_report* rep);
+int grem_partition_file(grem_ctx* ctx, const char* path, int64_t p, const grem_config* cfg,
+                        const grem_hooks* hooks, int32_t* labels_out, grem_report* rep);
+
+/* During an on_chunk hook: D2H copy of the live parts (int32, -1 unassigned). */
+int grem_state_parts(grem_ctx* ctx, int32_t* out, int64_t n);
+
+/* ------------------------------------------------- device memory helpers */
+/* Let a caller keep edges resident across calls (bench, multi-call users). */
+int grem_device_alloc(grem_ctx* ctx, uint64_t bytes, void** out);
+int grem_device_free(grem_ctx* ctx, void* ptr);
+int grem_memcpy_h2d(grem_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int grem_memcpy_d2h(grem_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
+/* ------------------------------------------------------------- synthetic */
+/* Deterministic Chung-Lu power-law edges (grem_gen.h): edges [e0, e0+count)
+ * of the graph (n, beta, seed); host and device produce identical bytes. */
+double grem_gen_scale(uint64_t n, uint32_t beta);
+int grem_gen_edges_host(uint64_t n, uint32_t beta, uint64_t seed, uint64_t e0, uint64_t count,
+                        uint32_t* out, int threads);
+int grem_gen_edges_device(grem_ctx* ctx, uint64_t n, uint32_t beta, uint64_t seed, uint64_t e0,
+                          uint64_t count, uint32_t* dev_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GREM_B200_H */

@@ -1,0 +1,1097 @@
+// grem_kernels.cu — hand-written sm_100a kernels of the GREM path.
+//
+// The reference sweep (process_chunk, grem.py:119-155) is sequential: node i
+// sees the *live* labels of lower-id chunk neighbours and one shared `sizes`
+// pair gates every decision.  It is reproduced exactly in parallel by rounds
+// to a fixpoint:
+//   counts   per node, lower neighbours read the tentative labels of the
+//            previous round, higher neighbours the pre-sweep labels
+//            (k_count_init / k_count_delta: edge-parallel, packed u64 REDs);
+//   prefs    fp64 averaging (a + c) * 0.5 exactly as Python (k_prefs);
+//   sizes    every node's effect on x = sizes[0] is a clamp; clamps compose in
+//            O(1), so the exact sequential sizes chain is a parallel scan
+//            (k_scan_*); ties (go to the smaller side) are not clamps, so
+//            they are speculated, verified, and repaired by a sequential walk
+//            only where the speculation was wrong (k_walk);
+//   decide   b = [x - o <= t]; labels that changed feed the next round.
+// A fixpoint equals the sequential result (by induction over the sweep).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "grem_core.cuh"
+#include "grem_gen.h"
+#include "grem_kernels.cuh"
+
+namespace grem {
+
+static int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+static inline unsigned grid_for(int64_t work, int threads, int per_sm = 8) {
+    int64_t blocks = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms() * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (unsigned)blocks;
+}
+
+#define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); \
+                               i += (int64_t)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------------ scan core
+
+__device__ __forceinline__ Clamp shfl_up_clamp(const Clamp& v, int off) {
+    Clamp r;
+    r.d = __shfl_up_sync(0xffffffffu, v.d, off);
+    r.L = __shfl_up_sync(0xffffffffu, v.L, off);
+    r.U = __shfl_up_sync(0xffffffffu, v.U, off);
+    return r;
+}
+__device__ __forceinline__ Clamp shfl_clamp(const Clamp& v, int src) {
+    Clamp r;
+    r.d = __shfl_sync(0xffffffffu, v.d, src);
+    r.L = __shfl_sync(0xffffffffu, v.L, src);
+    r.U = __shfl_sync(0xffffffffu, v.U, src);
+    return r;
+}
+
+__device__ __forceinline__ Clamp warp_incl_scan(Clamp v) {
+    int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        Clamp o = shfl_up_clamp(v, off);
+        if (lane >= off) v = clamp_then(o, v);
+    }
+    return v;
+}
+
+// exclusive, order-respecting block scan of clamps (thread order)
+template <int BT>
+__device__ __forceinline__ Clamp block_excl_scan(Clamp v, Clamp* smem /* >= BT/32 */, Clamp* total) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = BT / 32;
+    Clamp incl = warp_incl_scan(v);
+    Clamp excl = shfl_up_clamp(incl, 1);
+    if (lane == 0) excl = clamp_identity();
+    if (lane == 31) smem[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        Clamp w = lane < NW ? smem[lane] : clamp_identity();
+        Clamp wi = warp_incl_scan(w);
+        Clamp we = shfl_up_clamp(wi, 1);
+        if (lane == 0) we = clamp_identity();
+        if (lane < NW) smem[lane] = we;
+        if (lane == 31 && total) *total = wi;
+    }
+    __syncthreads();
+    Clamp pre = smem[warp];
+    __syncthreads();
+    return clamp_then(pre, excl);
+}
+
+// map sources -----------------------------------------------------------------
+
+struct ChunkMapSrc {
+    const uint8_t* meta;
+    const int32_t* newb;
+    long long s0, cap;
+    __device__ __forceinline__ NodeMap get(int64_t i) const {
+        uint8_t m = meta[i];
+        long long lift = (meta_active(m) && meta_old(m) != -1) ? 1 : 0;
+        return node_map(m, s0 + newb[i] - lift, cap);
+    }
+};
+
+// seed refinement pass (seed.py:96-116): moves are x-independent wishes gated
+// by the receiving side's room; 0->1: x' = max(x-1, s-cap); 1->0: min(x+1, cap)
+struct RefineMapSrc {
+    const uint8_t* want;
+    const int8_t* pre;
+    long long s, cap;
+    __device__ __forceinline__ NodeMap get(int64_t i) const {
+        NodeMap r;
+        r.o = 0;
+        r.t = 0;
+        if (!want[i]) {
+            r.f = clamp_identity();
+        } else if (pre[i] == 0) {
+            r.f = Clamp{-1, s - cap, kInf};
+        } else {
+            r.f = Clamp{1, -kInf, cap};
+        }
+        return r;
+    }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Src src, int64_t N, Clamp* tile_agg) {
+    __shared__ Clamp smem[kScanThreads / 32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    Clamp acc = clamp_identity();
+#pragma unroll 4
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i < N) acc = clamp_then(acc, src.get(i).f);
+    }
+    __shared__ Clamp stotal;
+    block_excl_scan<kScanThreads>(acc, smem, &stotal);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_agg[blockIdx.x] = stotal;
+}
+
+// single block: exclusive scan over tile aggregates, evaluated at x0
+__global__ void __launch_bounds__(1024) k_scan_top(const Clamp* tile_agg, int64_t ntiles, const long long* x0p,
+                                                   long long* tile_x) {
+    __shared__ Clamp smem[32];
+    int64_t per = (ntiles + 1023) / 1024;
+    int64_t lo = (int64_t)threadIdx.x * per;
+    int64_t hi = lo + per < ntiles ? lo + per : ntiles;
+    Clamp acc = clamp_identity();
+    for (int64_t t = lo; t < hi; ++t) acc = clamp_then(acc, tile_agg[t]);
+    Clamp pre = block_excl_scan<1024>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, *x0p);
+    for (int64_t t = lo; t < hi; ++t) {
+        tile_x[t] = x;
+        x = clamp_apply(tile_agg[t], x);
+    }
+}
+
+// chunk downsweep: x before every node, tie verification
+struct ChunkOut {
+    int32_t* x;
+    uint8_t* bad;
+    long long* tile_bad;
+    long long* nbad;
+    const uint8_t* meta;
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down_chunk(Src src, int64_t N, const long long* tile_x,
+                                                                  ChunkOut out) {
+    __shared__ Clamp smem[kScanThreads / 32];
+    __shared__ long long sbad;
+    if (threadIdx.x == 0) sbad = kInf;
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    Clamp acc = clamp_identity();
+#pragma unroll 4
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i < N) acc = clamp_then(acc, src.get(i).f);
+    }
+    Clamp pre = block_excl_scan<kScanThreads>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, tile_x[blockIdx.x]);
+    long long mybad = kInf;
+    int nb = 0;
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i >= N) break;
+        NodeMap nm = src.get(i);
+        out.x[i] = (int32_t)x;
+        uint8_t m = out.meta[i];
+        uint8_t isbad = 0;
+        if (meta_active(m) && meta_pref(m) == 2) {
+            int b = (x - nm.o <= nm.t) ? 0 : 1;
+            int spec = (m & M_SPEC) ? 1 : 0;
+            if (b != spec) {
+                isbad = 1;
+                if (i < mybad) mybad = i;
+                nb++;
+            }
+        }
+        out.bad[i] = isbad;
+        x = clamp_apply(nm.f, x);
+        if (i == N - 1) out.x[N] = (int32_t)x;
+    }
+    if (mybad != kInf) atomicMin(&sbad, mybad);
+    if (nb) atomicAdd((unsigned long long*)out.nbad, (unsigned long long)nb);
+    __syncthreads();
+    if (threadIdx.x == 0) out.tile_bad[blockIdx.x] = sbad;
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down_plain(Src src, int64_t N, const long long* tile_x,
+                                                                  int32_t* xo) {
+    __shared__ Clamp smem[kScanThreads / 32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    Clamp acc = clamp_identity();
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i < N) acc = clamp_then(acc, src.get(i).f);
+    }
+    Clamp pre = block_excl_scan<kScanThreads>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, tile_x[blockIdx.x]);
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i >= N) break;
+        xo[i] = (int32_t)x;
+        x = clamp_apply(src.get(i).f, x);
+        if (i == N - 1) xo[N] = (int32_t)x;
+    }
+}
+
+// ------------------------------------------------------------- counting
+
+// round 1: every chunk neighbour read with its pre-sweep label (cnt_nbrs,
+// grem.py:82-97 / 138-145); nodes whose counts stay zero get a flag so the
+// chunk node set (np.unique, model.py:59) still contains them.
+__global__ void k_count_init(const uint2* __restrict__ e, int64_t m, const int8_t* __restrict__ lab,
+                             unsigned long long* __restrict__ cnt, uint8_t* __restrict__ flag) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        uint32_t u = ed.x, v = ed.y;
+        if (u == v) {   // self-loops never count (model.py:53-55) but make u a chunk node
+            flag[u] = 1;
+            continue;
+        }
+        int lu = lab[u], lv = lab[v];
+        if (lv >= 0) atomicAdd(&cnt[u], lv == 0 ? 1ULL : (1ULL << 32));
+        else flag[u] = 1;
+        if (lu >= 0) atomicAdd(&cnt[v], lu == 0 ? 1ULL : (1ULL << 32));
+        else flag[v] = 1;
+    }
+}
+
+// rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
+// tentative label; apply the change since the previous round.
+__global__ void k_count_delta(const uint2* __restrict__ e, int64_t m, const uint8_t* __restrict__ tl,
+                              unsigned long long* __restrict__ cnt) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        uint32_t u = ed.x, v = ed.y;
+        if (u == v) continue;
+        uint32_t lo = u < v ? u : v, hi = u < v ? v : u;
+        uint8_t t = tl[lo];
+        int cur = t & 0xF, prev = t >> 4;
+        if (cur != prev) atomicAdd(&cnt[hi], enc_label(cur) - enc_label(prev));
+    }
+}
+
+void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
+    k_count_init<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, b.lab, b.cnt, b.flag);
+}
+void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
+    k_count_delta<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, b.tl, b.cnt);
+}
+
+__global__ void k_mark_all(const uint2* __restrict__ e, int64_t m, uint8_t* __restrict__ flag) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        flag[ed.x] = 1;
+        flag[ed.y] = 1;
+    }
+}
+void launch_mark_all(const uint2* e, int64_t m, uint8_t* flag, cudaStream_t s) {
+    k_mark_all<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, flag);
+}
+
+struct PresentPred {
+    const uint8_t* flag;
+    const unsigned long long* cnt;
+    __device__ __forceinline__ bool operator()(const uint32_t& g) const { return flag[g] || cnt[g]; }
+};
+
+size_t select_nodes_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(nullptr, bytes, it, (uint32_t*)nullptr, (long long*)nullptr, (int)n,
+                          PresentPred{nullptr, nullptr});
+    return bytes;
+}
+void launch_select_nodes(const uint8_t* flag, const unsigned long long* cnt, int64_t n, uint32_t* nodes,
+                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s) {
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(temp, temp_bytes, it, nodes, d_count, (int)n, PresentPred{flag, cnt}, s);
+}
+
+// ------------------------------------------------------------ node passes
+
+__global__ void k_node_init(const uint32_t* __restrict__ nodes, int64_t nc, const int8_t* __restrict__ lab,
+                            int refine, uint8_t* __restrict__ meta, uint8_t* __restrict__ tl,
+                            int32_t* __restrict__ newflag, long long* total_new) {
+    int cnt_new = 0;
+    GRID_STRIDE(i, nc) {
+        uint32_t g = nodes[i];
+        int old = lab[g];
+        int code = old + 1;
+        bool isnew = old == -1;
+        bool active = isnew || refine;
+        meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
+        tl[g] = (uint8_t)(code | (code << 4));
+        int nf = (active && isnew) ? 1 : 0;
+        newflag[i] = nf;
+        cnt_new += nf;
+    }
+    for (int off = 16; off; off >>= 1) cnt_new += __shfl_down_sync(0xffffffffu, cnt_new, off);
+    if ((threadIdx.x & 31) == 0 && cnt_new) atomicAdd((unsigned long long*)total_new, (unsigned long long)cnt_new);
+}
+
+void launch_node_init(const ChunkBufs& b, int64_t nc, int refine, cudaStream_t s) {
+    k_node_init<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.lab, refine, b.meta, b.tl, b.x, b.scal + 2);
+}
+
+__device__ __forceinline__ void averaged(uint8_t m, unsigned long long c, double2 nb, double& a0, double& a1) {
+    double c0 = (double)(uint32_t)(c & 0xffffffffULL);
+    double c1 = (double)(uint32_t)(c >> 32);
+    if (meta_old(m) != -1) {   // (nbr + c) * 0.5 in binary64 (grem.py:147-148)
+        a0 = __dmul_rn(__dadd_rn(nb.x, c0), 0.5);
+        a1 = __dmul_rn(__dadd_rn(nb.y, c1), 0.5);
+    } else {
+        a0 = c0;
+        a1 = c1;
+    }
+}
+
+__global__ void k_prefs(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
+                        const int32_t* __restrict__ newb, const unsigned long long* __restrict__ cnt,
+                        const double2* __restrict__ nbr, const long long* __restrict__ sizes, int first_round) {
+    long long x0 = sizes[0];
+    GRID_STRIDE(i, nc) {
+        uint8_t m = meta[i];
+        if (!meta_active(m)) continue;
+        uint32_t g = nodes[i];
+        unsigned long long c = cnt[g];
+        double2 nb = make_double2(0.0, 0.0);
+        if (meta_old(m) != -1) nb = nbr[g];
+        double a0, a1;
+        averaged(m, c, nb, a0, a1);
+        int pref = a0 < a1 ? 1 : (a1 < a0 ? 0 : 2);   // assign(), grem.py:106-110
+        m = (uint8_t)((m & ~M_PREF) | (pref << M_PREF_SHIFT));
+        if (first_round) {
+            // first guess for ties: smaller side at the chunk's starting sizes
+            long long o = meta_old(m) == 0 ? 1 : 0;
+            long long lift = meta_old(m) != -1 ? 1 : 0;
+            long long sl = newb[i] - lift;   // newb holds s0 + new nodes before i
+            bool side0 = (x0 - o) <= (sl >> 1);
+            m = (uint8_t)(side0 ? (m & ~M_SPEC) : (m | M_SPEC));
+        }
+        meta[i] = m;
+    }
+}
+
+void launch_prefs(const ChunkBufs& b, int64_t nc, int first_round, cudaStream_t s) {
+    k_prefs<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.newb, b.cnt, b.nbr, b.sizes, first_round);
+}
+
+template <class Src>
+static void run_scan_chunk(const Src& src, int64_t N, const ChunkBufs& b, cudaStream_t s) {
+    int64_t ntiles = (N + kScanTile - 1) / kScanTile;
+    k_scan_reduce<Src><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, N, b.tile_agg);
+    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x);
+    ChunkOut out{b.x, b.bad, b.tile_bad, b.scal + 4, b.meta};
+    k_scan_down_chunk<Src><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, N, b.tile_x, out);
+}
+
+// The map source needs s_l = s0 + (active new nodes before i) - lift; s0 is
+// folded into newb once per chunk so the source stays a plain value.
+__global__ void k_add_base(int32_t* a, int64_t n, const long long* sizes) {
+    long long s0 = sizes[0] + sizes[1];
+    GRID_STRIDE(i, n) a[i] = (int32_t)(a[i] + s0);
+}
+void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t s) {
+    k_add_base<<<grid_for(n, 256), 256, 0, s>>>(a, n, sizes);
+}
+
+void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
+    // newb already holds s0 + (active new nodes before i)  (see runtime)
+    ChunkMapSrc src{b.meta, b.newb, 0, cap};
+    run_scan_chunk(src, nc, b, s);
+}
+
+// Sequential repair of mis-speculated ties (single warp; all lanes run the
+// chain redundantly, lanes prefetch node parameters in batches of 32).
+__global__ void __launch_bounds__(32) k_walk(const uint8_t* __restrict__ meta, const int32_t* __restrict__ newb,
+                                             int32_t* __restrict__ x, const uint8_t* __restrict__ bad,
+                                             const long long* __restrict__ tile_bad, int64_t nc, long long cap,
+                                             const long long* nbad, long long* steps_out) {
+    if (*nbad == 0) return;
+    const int lane = threadIdx.x;
+    const int64_t ntiles = (nc + kScanTile - 1) / kScanTile;
+    int64_t pos = 0;
+    long long steps = 0;
+    while (true) {
+        // ---- next flagged index >= pos
+        int64_t k = -1;
+        int64_t t = pos / kScanTile;
+        if (t < ntiles && tile_bad[t] != kInf) {
+            int64_t lo = pos, hi = (t + 1) * kScanTile < nc ? (t + 1) * kScanTile : nc;
+            for (int64_t j = lo; j < hi && k < 0; j += 32) {
+                int64_t idx = j + lane;
+                unsigned bal = __ballot_sync(0xffffffffu, idx < hi && bad[idx]);
+                if (bal) k = j + __ffs(bal) - 1;
+            }
+        }
+        for (int64_t tt = t + 1; k < 0 && tt < ntiles; tt += 32) {
+            int64_t mt = tt + lane;
+            unsigned bal = __ballot_sync(0xffffffffu, mt < ntiles && tile_bad[mt] != kInf);
+            if (bal) {
+                int64_t ft = tt + __ffs(bal) - 1;
+                k = tile_bad[ft];
+            }
+        }
+        if (k < 0) break;
+        // ---- walk from k with the exact x until it re-joins the speculative chain
+        long long xe = x[k];
+        int64_t i = k;
+        bool done = false;
+        while (!done) {
+            int64_t idx = i + lane;
+            uint8_t m = idx < nc ? meta[idx] : 0;
+            int32_t nb = idx < nc ? newb[idx] : 0;
+            int32_t xs = idx < nc ? x[idx + 1] : 0;   // speculative x after node idx (read before writes)
+            __syncwarp();
+            for (int j = 0; j < 32; ++j) {
+                int64_t p = i + j;
+                uint8_t mj = __shfl_sync(0xffffffffu, m, j);
+                int32_t nbj = __shfl_sync(0xffffffffu, nb, j);
+                int32_t xsj = __shfl_sync(0xffffffffu, xs, j);
+                if (p >= nc) { done = true; pos = nc; break; }
+                long long lift = (meta_active(mj) && meta_old(mj) != -1) ? 1 : 0;
+                NodeMap nm = node_map(mj, (long long)nbj - lift, cap);
+                if (lane == 0) x[p] = (int32_t)xe;
+                if (meta_active(mj)) xe = xe - nm.o + ((xe - nm.o <= nm.t) ? 1 : 0);
+                steps++;
+                if (p + 1 == nc) {
+                    if (lane == 0) x[nc] = (int32_t)xe;
+                    done = true;
+                    pos = nc;
+                    break;
+                }
+                if (xe == (long long)xsj) {   // re-joined: the speculative chain is exact again
+                    done = true;
+                    pos = p + 1;
+                    break;
+                }
+            }
+            i += 32;
+            __syncwarp();
+        }
+        if (pos >= nc) break;
+    }
+    if (lane == 0) atomicAdd((unsigned long long*)steps_out, (unsigned long long)steps);
+}
+
+void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
+    k_walk<<<1, 32, 0, s>>>(b.meta, b.newb, b.x, b.bad, b.tile_bad, nc, cap, b.scal + 4, b.scal + 3);
+}
+
+__global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
+                         const int32_t* __restrict__ newb, const int32_t* __restrict__ x, long long cap,
+                         uint8_t* __restrict__ tl, long long* changed) {
+    int ch = 0;
+    GRID_STRIDE(i, nc) {
+        uint8_t m = meta[i];
+        if (!meta_active(m)) continue;
+        long long lift = meta_old(m) != -1 ? 1 : 0;
+        NodeMap nm = node_map(m, (long long)newb[i] - lift, cap);
+        int b = ((long long)x[i] - nm.o <= nm.t) ? 0 : 1;
+        uint32_t g = nodes[i];
+        uint8_t t = tl[g];
+        int cur = t & 0xF;
+        int code = b + 1;
+        tl[g] = (uint8_t)(code | (cur << 4));
+        ch += (code != cur);
+        meta[i] = (uint8_t)(b ? (m | M_SPEC) : (m & ~M_SPEC));   // next round's tie guess
+    }
+    for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
+}
+
+void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
+    k_decide<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.newb, b.x, cap, b.tl, b.scal + 1);
+}
+
+__global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const uint8_t* __restrict__ meta,
+                         unsigned long long* __restrict__ cnt, double2* __restrict__ nbr, int8_t* __restrict__ lab,
+                         const uint8_t* __restrict__ tl, uint8_t* __restrict__ flag) {
+    GRID_STRIDE(i, nc) {
+        uint32_t g = nodes[i];
+        uint8_t m = meta[i];
+        if (meta_active(m)) {
+            double2 nb = make_double2(0.0, 0.0);
+            if (meta_old(m) != -1) nb = nbr[g];
+            double a0, a1;
+            averaged(m, cnt[g], nb, a0, a1);
+            nbr[g] = make_double2(a0, a1);
+            lab[g] = (int8_t)((tl[g] & 0xF) - 1);
+        }
+        cnt[g] = 0ULL;
+        flag[g] = 0;
+    }
+}
+
+void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
+    k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cnt, b.nbr, b.lab, b.tl, b.flag);
+}
+
+__global__ void k_sizes_update(long long* sizes, const int32_t* x, int64_t nc, const long long* total_new) {
+    long long s0 = sizes[0] + sizes[1];
+    long long xe = x[nc];
+    sizes[0] = xe;
+    sizes[1] = s0 + *total_new - xe;
+}
+void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
+    k_sizes_update<<<1, 1, 0, s>>>(b.sizes, b.x, nc, b.scal + 2);
+}
+
+// ----------------------------------------------------------------- seed
+
+__global__ void k_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank) {
+    GRID_STRIDE(i, nc) rank[nodes[i]] = (int32_t)i;
+}
+void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStream_t s) {
+    k_set_rank<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, rank);
+}
+
+__global__ void k_degrees(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ rank,
+                          int32_t* __restrict__ deg) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        if (ed.x == ed.y) continue;
+        atomicAdd(&deg[rank[ed.x]], 1);
+        atomicAdd(&deg[rank[ed.y]], 1);
+    }
+}
+void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, cudaStream_t s) {
+    k_degrees<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, deg);
+}
+
+__global__ void k_fill_csr(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ rank,
+                           int32_t* __restrict__ cursor, uint32_t* __restrict__ adj, uint32_t* __restrict__ row_of) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        if (ed.x == ed.y) continue;
+        int32_t a = rank[ed.x], c = rank[ed.y];
+        int32_t pa = atomicAdd(&cursor[a], 1);
+        adj[pa] = (uint32_t)c;
+        row_of[pa] = (uint32_t)a;
+        int32_t pc = atomicAdd(&cursor[c], 1);
+        adj[pc] = (uint32_t)a;
+        row_of[pc] = (uint32_t)c;
+    }
+}
+void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
+                     uint32_t* row_of, cudaStream_t s) {
+    k_fill_csr<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, cursor, adj, row_of);
+}
+
+// union-find connected components (link larger root under smaller root)
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
+    uint32_t p = ((volatile uint32_t*)parent)[x];
+    while (p != x) {
+        uint32_t gp = ((volatile uint32_t*)parent)[p];
+        if (gp != p) ((volatile uint32_t*)parent)[x] = gp;   // path halving
+        x = p;
+        p = gp;
+    }
+    return x;
+}
+
+__global__ void k_iota_u32(uint32_t* a, int64_t n) {
+    GRID_STRIDE(i, n) a[i] = (uint32_t)i;
+}
+
+__global__ void k_cc_link(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ rank, uint32_t* parent) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        if (ed.x == ed.y) continue;
+        uint32_t a = (uint32_t)rank[ed.x], b = (uint32_t)rank[ed.y];
+        while (true) {
+            uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+            if (ra == rb) break;
+            if (ra > rb) { uint32_t t = ra; ra = rb; rb = t; }
+            if (atomicCAS(&parent[rb], rb, ra) == rb) break;
+            a = ra;
+            b = rb;
+        }
+    }
+}
+
+__global__ void k_cc_compress(uint32_t* parent, int64_t nc) {
+    GRID_STRIDE(i, nc) parent[i] = uf_find(parent, (uint32_t)i);
+}
+
+void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, int64_t nc, cudaStream_t s) {
+    k_iota_u32<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
+    k_cc_link<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, parent);
+    k_cc_compress<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
+}
+
+// restart order of _bfs_grow (seed.py:69-75): a component is entered at its
+// highest-degree, lowest-index node; key = (~degree << 32) | index, min wins.
+__global__ void k_comp_keys(const int32_t* __restrict__ start, const uint32_t* __restrict__ parent, int64_t nc,
+                            unsigned long long* ckey, uint32_t* csize) {
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nc; base += stride) {
+        int64_t i = base + (threadIdx.x & 31);
+        bool valid = i < nc;
+        uint32_t r = valid ? parent[i] : 0xFFFFFFFFu;
+        if (valid) {
+            uint32_t d = (uint32_t)(start[i + 1] - start[i]);
+            unsigned long long key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
+            if (key < ((volatile unsigned long long*)ckey)[r]) atomicMin(&ckey[r], key);
+        }
+        unsigned peers = __match_any_sync(0xffffffffu, r);   // aggregate the giant component's size
+        int leader = __ffs(peers) - 1;
+        if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&csize[r], (uint32_t)__popc(peers));
+    }
+}
+void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
+    cudaMemsetAsync(sb.ckey, 0xFF, sizeof(unsigned long long) * nc, s);
+    cudaMemsetAsync(sb.csize, 0, sizeof(uint32_t) * nc, s);
+    k_comp_keys<<<grid_for(nc, 256), 256, 0, s>>>(sb.start, sb.parent, nc, sb.ckey, sb.csize);
+}
+
+struct RootPred {
+    const uint32_t* parent;
+    __device__ __forceinline__ bool operator()(const uint32_t& i) const { return parent[i] == i; }
+};
+void launch_select_roots(const SeedBufs& sb, int64_t nc, void* temp, size_t temp_bytes, cudaStream_t s) {
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(temp, temp_bytes, it, sb.roots, sb.scal + 0, (int)nc, RootPred{sb.parent}, s);
+}
+
+__global__ void k_root_keys(const uint32_t* roots, int64_t nr, const unsigned long long* ckey,
+                            unsigned long long* rkeys, uint32_t* rvals) {
+    GRID_STRIDE(j, nr) {
+        rkeys[j] = ckey[roots[j]];
+        rvals[j] = roots[j];
+    }
+}
+void launch_root_keys(const SeedBufs& sb, int64_t nr, cudaStream_t s) {
+    k_root_keys<<<grid_for(nr, 256), 256, 0, s>>>(sb.roots, nr, sb.ckey, sb.rkeys, sb.rvals);
+}
+
+// cumulative component sizes in restart order -> boundary component
+__global__ void k_csize_sorted(const uint32_t* rvals2, int64_t nr, const uint32_t* csize, int64_t* out) {
+    GRID_STRIDE(j, nr) out[j] = csize[rvals2[j]];
+}
+__global__ void k_find_boundary(const int64_t* cum_excl, const uint32_t* rvals2, const uint32_t* csize,
+                                const unsigned long long* rkeys2, int64_t nr, long long target, uint32_t* cpos,
+                                long long* scal) {
+    GRID_STRIDE(j, nr) {
+        long long before = cum_excl[j];
+        long long after = before + csize[rvals2[j]];
+        cpos[rvals2[j]] = (uint32_t)j;
+        if (before < target && after >= target) {
+            scal[1] = j;                                  // boundary component position
+            scal[2] = target - before;                    // BFS quota inside it
+            scal[3] = (long long)(rkeys2[j] & 0xFFFFFFFFULL);   // its start node
+        }
+    }
+}
+void launch_boundary(const SeedBufs& sb, int64_t nr, long long target, void* temp, size_t temp_bytes,
+                     cudaStream_t s) {
+    k_csize_sorted<<<grid_for(nr, 256), 256, 0, s>>>(sb.rvals2, nr, sb.csize, sb.fdeg);
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, sb.fdeg, sb.cum, (int)nr, s);
+    k_find_boundary<<<grid_for(nr, 256), 256, 0, s>>>(sb.cum, sb.rvals2, sb.csize, sb.rkeys2, nr, target, sb.cpos,
+                                                       sb.scal);
+}
+
+__global__ void k_seed_labels(const uint32_t* parent, const uint32_t* cpos, int64_t nc, const long long* scal,
+                              int8_t* slab, uint32_t* disc) {
+    long long jb = scal[1];
+    long long s0 = scal[3];
+    GRID_STRIDE(i, nc) {
+        long long p = cpos[parent[i]];
+        slab[i] = (int8_t)(p < jb ? 0 : (p > jb ? 1 : 2));
+        disc[i] = 0xFFFFFFFFu;
+        if (i == s0) slab[i] = 0;   // BFS start is picked first (seed.py:70-74)
+    }
+}
+void launch_seed_labels(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
+    k_seed_labels<<<grid_for(nc, 256), 256, 0, s>>>(sb.parent, sb.cpos, nc, sb.scal, sb.slab, sb.disc);
+}
+
+__global__ void k_frontier_deg(const uint32_t* frontier, int64_t fsize, const int32_t* start, int64_t* fdeg) {
+    GRID_STRIDE(j, fsize) {
+        uint32_t v = frontier[j];
+        fdeg[j] = start[v + 1] - start[v];
+    }
+}
+void launch_frontier_degrees(const SeedBufs& sb, int64_t fsize, cudaStream_t s) {
+    k_frontier_deg<<<grid_for(fsize, 256), 256, 0, s>>>(sb.frontier, fsize, sb.start, sb.fdeg);
+}
+
+// level expansion: every (frontier node, neighbour) pair, balanced over
+// entries; a candidate keeps its minimum discoverer rank (FIFO order of
+// _bfs_grow: queue order, then ascending neighbour id).
+__global__ void k_bfs_expand(const uint32_t* __restrict__ frontier, int64_t fsize, long long rbase,
+                             const int64_t* __restrict__ fpre, int64_t total, const int32_t* __restrict__ start,
+                             const uint32_t* __restrict__ adj, const int8_t* __restrict__ slab,
+                             uint32_t* __restrict__ disc, unsigned long long* __restrict__ cand, long long* ncand) {
+    GRID_STRIDE(k, total) {
+        // j = last index with fpre[j] <= k
+        int64_t lo = 0, hi = fsize - 1;
+        while (lo < hi) {
+            int64_t mid = (lo + hi + 1) >> 1;
+            if (fpre[mid] <= k) lo = mid; else hi = mid - 1;
+        }
+        uint32_t v = frontier[lo];
+        uint32_t w = adj[start[v] + (k - fpre[lo])];
+        if (slab[w] != 2) continue;
+        uint32_t r = (uint32_t)(rbase + lo);
+        if (r < ((volatile uint32_t*)disc)[w]) {
+            uint32_t old = atomicMin(&disc[w], r);
+            if (old == 0xFFFFFFFFu) {
+                unsigned long long idx = atomicAdd((unsigned long long*)ncand, 1ULL);
+                cand[idx] = w;
+            }
+        }
+    }
+}
+void launch_bfs_expand(const SeedBufs& sb, int64_t fsize, long long rbase, int64_t total, cudaStream_t s) {
+    k_bfs_expand<<<grid_for(total, 256, 16), 256, 0, s>>>(sb.frontier, fsize, rbase, sb.cum, total, sb.start, sb.adj,
+                                                         sb.slab, sb.disc, sb.cand_keys, sb.scal + 4);
+}
+
+__global__ void k_cand_keys(unsigned long long* cand, int64_t nc, const uint32_t* disc) {
+    GRID_STRIDE(c, nc) {
+        uint32_t w = (uint32_t)cand[c];
+        cand[c] = ((unsigned long long)disc[w] << 32) | w;
+    }
+}
+void launch_cand_keys(const SeedBufs& sb, int64_t ncand, cudaStream_t s) {
+    k_cand_keys<<<grid_for(ncand, 256), 256, 0, s>>>(sb.cand_keys, ncand, sb.disc);
+}
+__global__ void k_bfs_take(const unsigned long long* sorted, int64_t take, int8_t* slab, uint32_t* frontier) {
+    GRID_STRIDE(c, take) {
+        uint32_t w = (uint32_t)(sorted[c] & 0xFFFFFFFFULL);
+        slab[w] = 0;
+        frontier[c] = w;
+    }
+}
+void launch_bfs_take(const SeedBufs& sb, int64_t ncand, int64_t take, cudaStream_t s) {
+    k_bfs_take<<<grid_for(take, 256), 256, 0, s>>>(sb.cand_keys2, take, sb.slab, sb.frontier);
+}
+
+__global__ void k_seed_finalize(int8_t* slab, int64_t nc) {
+    GRID_STRIDE(i, nc) if (slab[i] == 2) slab[i] = 1;
+}
+void launch_seed_finalize(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
+    k_seed_finalize<<<grid_for(nc, 256), 256, 0, s>>>(sb.slab, nc);
+}
+
+// per-row packed counts over the chunk-0 CSR (entries of a row are
+// contiguous): warp-segmented reduction, one atomic per row segment.
+//   mode 0 (refinement pass, seed.py:96-116): (same | other<<32) where a
+//          neighbour's label is `cur` if its index is lower, else `pre`;
+//   mode 1 (estimates, grem.py:166-174): (#label0 | #label1<<32) over `cur`.
+__global__ void k_row_counts(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ row_of, int64_t entries,
+                             const int8_t* __restrict__ cur, const int8_t* __restrict__ pre, int mode,
+                             unsigned long long* __restrict__ pair) {
+    int lane = threadIdx.x & 31;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < entries; base += stride) {
+        int64_t k = base + lane;
+        bool valid = k < entries;
+        uint32_t row = valid ? row_of[k] : 0xFFFFFFFFu;
+        unsigned long long v = 0;
+        if (valid) {
+            uint32_t w = adj[k];
+            if (mode == 0) {
+                int lw = w < row ? cur[w] : pre[w];
+                v = (lw == pre[row]) ? 1ULL : (1ULL << 32);
+            } else {
+                int lw = cur[w];
+                v = lw == 0 ? 1ULL : (lw == 1 ? (1ULL << 32) : 0ULL);
+            }
+        }
+        // segmented inclusive scan over equal rows (rows are non-decreasing in k)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned long long ov = __shfl_up_sync(0xffffffffu, v, off);
+            uint32_t orow = __shfl_up_sync(0xffffffffu, row, off);
+            if (lane >= off && orow == row) v += ov;
+        }
+        uint32_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        bool tail = (lane == 31) || (nrow != row);
+        if (valid && tail && v) atomicAdd(&pair[row], v);
+    }
+}
+void launch_row_counts(const SeedBufs& sb, const int8_t* cur, const int8_t* pre, int mode, int64_t entries,
+                       int64_t nc, cudaStream_t s) {
+    cudaMemsetAsync(sb.pair, 0, sizeof(unsigned long long) * nc, s);
+    if (entries > 0)
+        k_row_counts<<<grid_for(entries, 256, 16), 256, 0, s>>>(sb.adj, sb.row_of, entries, cur, pre, mode, sb.pair);
+}
+
+__global__ void k_want(const unsigned long long* pair, int64_t nc, uint8_t* want) {
+    GRID_STRIDE(i, nc) {
+        unsigned long long p = pair[i];
+        uint32_t same = (uint32_t)(p & 0xFFFFFFFFULL), other = (uint32_t)(p >> 32);
+        want[i] = (other > 0 && other > same) ? 1 : 0;
+    }
+}
+
+// one refinement round's sizes chain: x before every node, starting from the
+// pass-start x in scal[6]
+void launch_refine_scan(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
+    k_want<<<grid_for(nc, 256), 256, 0, s>>>(sb.pair, nc, sb.want);
+    RefineMapSrc src{sb.want, sb.slab, (long long)nc, cap};
+    int64_t ntiles = (nc + kScanTile - 1) / kScanTile;
+    k_scan_reduce<RefineMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_agg);
+    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, sb.scal + 6, b.tile_x);
+    k_scan_down_plain<RefineMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, b.x);
+}
+
+// x at pass start = number of label-0 chunk nodes, passed via scal[6] (host)
+__global__ void k_refine_decide(const uint8_t* want, const int8_t* pre, const int32_t* x, int64_t nc, long long cap,
+                                int8_t* tent, long long* changed) {
+    int ch = 0;
+    GRID_STRIDE(i, nc) {
+        int p = pre[i];
+        int t = p;
+        if (want[i]) {
+            long long xi = x[i];
+            bool room = (p == 0) ? (xi > nc - cap) : (xi < cap);
+            if (room) t = 1 - p;
+        }
+        ch += (t != tent[i]);
+        tent[i] = (int8_t)t;
+    }
+    for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
+}
+
+void launch_refine_decide(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
+    k_refine_decide<<<grid_for(nc, 256), 256, 0, s>>>(sb.want, sb.slab, b.x, nc, cap, sb.slab2, sb.scal + 5);
+}
+
+__global__ void k_seed_commit(const uint32_t* nodes, int64_t nc, const int8_t* slab,
+                              const unsigned long long* pair, int8_t* lab, double2* nbr, uint8_t* flag,
+                              long long* zeros) {
+    int z = 0;
+    GRID_STRIDE(i, nc) {
+        uint32_t g = nodes[i];
+        lab[g] = slab[i];
+        unsigned long long p = pair[i];
+        nbr[g] = make_double2((double)(uint32_t)(p & 0xFFFFFFFFULL), (double)(uint32_t)(p >> 32));
+        flag[g] = 0;
+        z += (slab[i] == 0);
+    }
+    for (int off = 16; off; off >>= 1) z += __shfl_down_sync(0xffffffffu, z, off);
+    if ((threadIdx.x & 31) == 0 && z) atomicAdd((unsigned long long*)zeros, (unsigned long long)z);
+}
+void launch_seed_commit(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* nodes, int64_t nc, cudaStream_t s) {
+    k_seed_commit<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, sb.slab, sb.pair, b.lab, b.nbr, b.flag, sb.scal + 7);
+}
+
+// ------------------------------------------------------------ after stream
+
+// _fill_unassigned (grem.py:177-189): in ascending id every never-seen node
+// goes to the smaller side (ties to 0); capacity can never redirect it when
+// 2*cap >= n.  Closed form: with d = sizes[1]-sizes[0], the first |d| go to
+// the smaller side, then sides alternate starting with 0.
+__global__ void k_unassigned_flags(const int8_t* lab, int64_t n, int32_t* f) {
+    GRID_STRIDE(i, n) f[i] = lab[i] == -1 ? 1 : 0;
+}
+__global__ void k_fill_apply(int8_t* lab, int64_t n, const int32_t* rank, const long long* sizes) {
+    long long d = sizes[1] - sizes[0];
+    long long ad = d < 0 ? -d : d;
+    int first = d > 0 ? 0 : 1;
+    GRID_STRIDE(i, n) {
+        if (lab[i] != -1) continue;
+        long long j = rank[i];
+        lab[i] = (int8_t)(j < ad ? first : ((j - ad) & 1));
+    }
+}
+void launch_fill_unassigned(int8_t* lab, int64_t n, const long long* sizes, int32_t* rank_scratch, void* temp,
+                            size_t temp_bytes, cudaStream_t s) {
+    // rank_scratch must hold 2n int32
+    int32_t* f = rank_scratch + n;
+    k_unassigned_flags<<<grid_for(n, 256), 256, 0, s>>>(lab, n, f);
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, f, rank_scratch, (int)n, s);
+    k_fill_apply<<<grid_for(n, 256), 256, 0, s>>>(lab, n, rank_scratch, sizes);
+}
+
+__global__ void k_labels_to_i32(const int8_t* lab, int64_t n, int32_t* out) {
+    GRID_STRIDE(i, n) out[i] = lab[i];
+}
+void launch_labels_to_i32(const int8_t* lab, int64_t n, int32_t* out, cudaStream_t s) {
+    k_labels_to_i32<<<grid_for(n, 256), 256, 0, s>>>(lab, n, out);
+}
+
+// count_cuts (grem.py:227-252)
+__global__ void k_cut(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ lab,
+                      unsigned long long* cut, int* neg) {
+    unsigned long long c = 0;
+    int ng = 0;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        int a = lab[ed.x], b = lab[ed.y];
+        ng |= (a < 0) | (b < 0);
+        c += (a != b);
+    }
+    for (int off = 16; off; off >>= 1) {
+        c += __shfl_down_sync(0xffffffffu, c, off);
+        ng |= __shfl_down_sync(0xffffffffu, ng, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c) atomicAdd(cut, c);
+        if (ng) atomicOr(neg, 1);
+    }
+}
+__global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long long* sizes, int64_t cap,
+                       int* mx) {
+    extern __shared__ unsigned long long sh[];
+    int64_t nb = cap < 1024 ? cap : 1024;
+    for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) sh[j] = 0;
+    __syncthreads();
+    int lm = -1;
+    GRID_STRIDE(i, n) {
+        int l = lab[i];
+        if (l < 0) continue;
+        lm = l > lm ? l : lm;
+        if (l < nb) atomicAdd(&sh[l], 1ULL);
+        else if (l < cap) atomicAdd(&sizes[l], 1ULL);
+    }
+    for (int off = 16; off; off >>= 1) {
+        int o = __shfl_down_sync(0xffffffffu, lm, off);
+        lm = o > lm ? o : lm;
+    }
+    if ((threadIdx.x & 31) == 0 && lm >= 0) atomicMax(mx, lm);
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < nb; j += blockDim.x)
+        if (sh[j]) atomicAdd(&sizes[j], sh[j]);
+}
+void launch_count_cuts(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* d_cut,
+                       unsigned long long* d_sizes, int64_t sizes_cap, int* d_max, int* d_neg, cudaStream_t s) {
+    if (m > 0) k_cut<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, lab, d_cut, d_neg);
+    int64_t nb = sizes_cap < 1024 ? sizes_cap : 1024;
+    k_hist<<<grid_for(n, 256, 4), 256, nb * sizeof(unsigned long long), s>>>(lab, n, d_sizes, sizes_cap, d_max);
+}
+
+__global__ void k_max_id(const uint2* __restrict__ e, int64_t m, uint32_t* mx) {
+    uint32_t v = 0;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        v = max(v, max(ed.x, ed.y));
+    }
+    for (int off = 16; off; off >>= 1) v = max(v, __shfl_down_sync(0xffffffffu, v, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, v);
+}
+void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_t s) {
+    if (m > 0) k_max_id<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, d_max_id);
+}
+
+// --------------------------------------------------------------- recursion
+
+__global__ void k_side_flags(const int8_t* lab, int64_t n, int side, int32_t* f) {
+    GRID_STRIDE(i, n) f[i] = lab[i] == side ? 1 : 0;
+}
+void launch_side_flags(const int8_t* lab, int64_t n, int side, int32_t* flags, cudaStream_t s) {
+    k_side_flags<<<grid_for(n, 256), 256, 0, s>>>(lab, n, side, flags);
+}
+
+struct SidePred {
+    const int8_t* lab;
+    int side;
+    __device__ __forceinline__ bool operator()(const uint2& ed) const {
+        return lab[ed.x] == side && lab[ed.y] == side;
+    }
+};
+size_t extract_temp_bytes(int64_t m) {
+    size_t bytes = 0;
+    cub::DeviceSelect::If(nullptr, bytes, (const uint2*)nullptr, (uint2*)nullptr, (long long*)nullptr, (int)m,
+                          SidePred{nullptr, 0});
+    return bytes;
+}
+__global__ void k_remap(uint2* e, const long long* cnt, const int32_t* newid) {
+    int64_t m = *cnt;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        e[i] = make_uint2((uint32_t)newid[ed.x], (uint32_t)newid[ed.y]);
+    }
+}
+void launch_extract(const uint2* e, int64_t m, const int8_t* lab, int side, const int32_t* newid, uint2* out,
+                    long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s) {
+    // kept edges in file order (stable selection), dense ids = rank among members
+    cub::DeviceSelect::If(temp, temp_bytes, e, out, d_count, (int)m, SidePred{lab, side}, s);
+    k_remap<<<grid_for(m, 256, 8), 256, 0, s>>>(out, d_count, newid);
+}
+
+__global__ void k_sub_orig(const int8_t* lab, int64_t n, int side, const int32_t* newid, const int32_t* orig,
+                           int32_t* sub) {
+    GRID_STRIDE(i, n) if (lab[i] == side) sub[newid[i]] = orig[i];
+}
+void launch_sub_orig(const int8_t* lab, int64_t n, int side, const int32_t* newid, const int32_t* orig,
+                     int32_t* sub_orig, cudaStream_t s) {
+    k_sub_orig<<<grid_for(n, 256), 256, 0, s>>>(lab, n, side, newid, orig, sub_orig);
+}
+
+__global__ void k_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_t base, int32_t* fin) {
+    GRID_STRIDE(i, n) fin[orig[i]] = base + lab[i];
+}
+void launch_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_t leaf_base, int32_t* final_lab,
+                       cudaStream_t s) {
+    k_leaf_write<<<grid_for(n, 256), 256, 0, s>>>(lab, n, orig, leaf_base, final_lab);
+}
+
+__global__ void k_iota(int32_t* a, int64_t n) {
+    GRID_STRIDE(i, n) a[i] = (int32_t)i;
+}
+void launch_iota(int32_t* a, int64_t n, cudaStream_t s) { k_iota<<<grid_for(n, 256), 256, 0, s>>>(a, n); }
+
+// ------------------------------------------------------------- CUB helpers
+
+size_t scan_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    return a > b ? a : b;
+}
+void exclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+}
+void exclusive_sum_i64(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+}
+size_t sort_temp_bytes(int64_t n) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    cub::DeviceRadixSort::SortKeys(nullptr, b, (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+    return a > b ? a : b;
+}
+void sort_pairs_u64_u32(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin, uint32_t* vout,
+                        int64_t n, void* temp, size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, (int)n, 0, 64, s);
+}
+void sort_keys_u64(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp, size_t temp_bytes,
+                   cudaStream_t s) {
+    cub::DeviceRadixSort::SortKeys(temp, temp_bytes, kin, kout, (int)n, 0, 64, s);
+}
+
+// ------------------------------------------------------------- generator
+__global__ void k_gen(gg_params p, uint64_t e0, uint64_t count, uint32_t* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t j = 2 * (e0 + i);
+        uint2 ed = make_uint2(gg_endpoint(&p, j), gg_endpoint(&p, j + 1));
+        reinterpret_cast<uint2*>(out)[i] = ed;
+    }
+}
+void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, uint64_t perm_mask, uint32_t perm_bits,
+                      uint64_t e0, uint64_t count, uint32_t* out, cudaStream_t s) {
+    gg_params p;
+    p.n = n;
+    p.seed = seed;
+    p.beta = beta;
+    p.scale = scale;
+    p.perm_mask = perm_mask;
+    p.perm_bits = perm_bits;
+    k_gen<<<grid_for((int64_t)count, 256, 32), 256, 0, s>>>(p, e0, count, out);
+}
+
+}  // namespace grem

@@ -1,0 +1,147 @@
+// grem_kernels.cuh — launch wrappers of the sm_100a kernels (grem_kernels.cu).
+// Every wrapper enqueues on `s` and never synchronises; counts that the host
+// needs (N_c, changed, ...) are left in device scalars.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "grem_core.cuh"
+
+namespace grem {
+
+struct ChunkBufs {
+    // global per-node state (n)
+    int8_t* lab;
+    uint8_t* tl;
+    unsigned long long* cnt;
+    uint8_t* flag;
+    double2* nbr;
+    // per chunk node (cap = chunk node capacity)
+    uint32_t* nodes;
+    uint8_t* meta;
+    int32_t* newb;      // exclusive count of active new nodes before i
+    int32_t* x;         // sizes[0] before node i; x[N_c] = after the chunk
+    uint8_t* bad;       // tie speculation inconsistent at i
+    // per scan tile
+    Clamp* tile_agg;
+    long long* tile_x;
+    long long* tile_bad;
+    // device scalars
+    long long* sizes;   // [2] live sizes (read-only during a chunk)
+    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 walk steps, 4 nbad
+};
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+int num_sms();
+
+// --- non-seed chunk (process_chunk, grem.py:119-155) ---
+void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
+void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
+void launch_node_init(const ChunkBufs& b, int64_t nc, int refine, cudaStream_t s);
+void launch_prefs(const ChunkBufs& b, int64_t nc, int first_round, cudaStream_t s);
+void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t s);
+void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
+void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);
+
+// --- chunk membership ---
+void launch_mark_all(const uint2* e, int64_t m, uint8_t* flag, cudaStream_t s);
+// nodes = ascending ids with flag or cnt nonzero; count -> *d_count (device)
+size_t select_nodes_temp_bytes(int64_t n);
+void launch_select_nodes(const uint8_t* flag, const unsigned long long* cnt, int64_t n, uint32_t* nodes,
+                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s);
+
+// --- seed chunk (seed.py:36-118, grem.py:158-174) ---
+struct SeedBufs {
+    int32_t* rank;        // n: local index of a chunk node
+    int32_t* start;       // nc+1 CSR row starts
+    int32_t* cursor;      // nc
+    uint32_t* adj;        // entries: local neighbour ids (rows unsorted)
+    uint32_t* row_of;     // entries: owning row
+    uint32_t* parent;     // nc: union-find
+    unsigned long long* ckey;  // nc: component (-degree, index) min key
+    uint32_t* csize;      // nc
+    uint32_t* roots;      // nc
+    unsigned long long* rkeys;   // nc
+    unsigned long long* rkeys2;  // nc
+    uint32_t* rvals;      // nc
+    uint32_t* rvals2;     // nc
+    uint32_t* cpos;       // nc: sorted position of a component root
+    int8_t* slab;         // nc: seed labels (0/1; 2 = boundary component, undecided)
+    int8_t* slab2;        // nc
+    uint32_t* disc;       // nc: BFS min discoverer rank
+    uint32_t* frontier;   // nc
+    unsigned long long* cand_keys;   // nc
+    unsigned long long* cand_keys2;  // nc
+    int64_t* fdeg;        // nc+1 frontier row lengths / sorted component sizes
+    int64_t* cum;         // nc+1 exclusive prefix of fdeg
+    unsigned long long* pair;        // nc: per-row packed counts
+    uint8_t* want;        // nc
+    long long* scal;      // [16]
+};
+
+void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStream_t s);
+void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, cudaStream_t s);
+void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
+                     uint32_t* row_of, cudaStream_t s);
+void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, int64_t nc, cudaStream_t s);
+void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s);
+void launch_select_roots(const SeedBufs& sb, int64_t nc, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_root_keys(const SeedBufs& sb, int64_t nroots, cudaStream_t s);
+void launch_boundary(const SeedBufs& sb, int64_t nroots, long long target, void* temp, size_t temp_bytes,
+                     cudaStream_t s);
+void launch_seed_labels(const SeedBufs& sb, int64_t nc, cudaStream_t s);
+// expansion reads frontier row-length prefix from sb.cum
+void launch_bfs_expand(const SeedBufs& sb, int64_t fsize, long long rbase, int64_t total, cudaStream_t s);
+void launch_cand_keys(const SeedBufs& sb, int64_t ncand, cudaStream_t s);
+void launch_frontier_degrees(const SeedBufs& sb, int64_t fsize, cudaStream_t s);
+void launch_bfs_take(const SeedBufs& sb, int64_t ncand, int64_t take, cudaStream_t s);
+void launch_seed_finalize(const SeedBufs& sb, int64_t nc, cudaStream_t s);
+void launch_row_counts(const SeedBufs& sb, const int8_t* cur, const int8_t* pre, int mode, int64_t entries,
+                       int64_t nc, cudaStream_t s);
+void launch_refine_scan(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+void launch_refine_decide(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+void launch_seed_commit(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* nodes, int64_t nc,
+                        cudaStream_t s);
+
+// --- after the stream ---
+void launch_fill_unassigned(int8_t* lab, int64_t n, const long long* sizes, int32_t* rank_scratch,
+                            void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_labels_to_i32(const int8_t* lab, int64_t n, int32_t* out, cudaStream_t s);
+// count_cuts (grem.py:227-252): cut, per-part sizes (int32 labels), max label
+void launch_count_cuts(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* d_cut,
+                       unsigned long long* d_sizes, int64_t sizes_cap, int* d_max, int* d_neg, cudaStream_t s);
+void launch_count_cuts_i8(const uint2* e, int64_t m, const int8_t* lab, unsigned long long* d_cut, cudaStream_t s);
+void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_t s);
+
+// --- recursion (_extract_induced, grem.py:255-274) ---
+void launch_side_flags(const int8_t* lab, int64_t n, int side, int32_t* flags, cudaStream_t s);
+void launch_extract(const uint2* e, int64_t m, const int8_t* lab, int side, const int32_t* newid,
+                    uint2* out, long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s);
+size_t extract_temp_bytes(int64_t m);
+void launch_sub_orig(const int8_t* lab, int64_t n, int side, const int32_t* newid, const int32_t* orig,
+                     int32_t* sub_orig, cudaStream_t s);
+void launch_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_t leaf_base, int32_t* final_lab,
+                       cudaStream_t s);
+void launch_iota(int32_t* a, int64_t n, cudaStream_t s);
+
+// generic CUB helpers
+size_t scan_temp_bytes(int64_t n);
+void exclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
+void exclusive_sum_i64(const int64_t* in, int64_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
+size_t sort_temp_bytes(int64_t n);
+void sort_pairs_u64_u32(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin,
+                        uint32_t* vout, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);
+void sort_keys_u64(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp,
+                   size_t temp_bytes, cudaStream_t s);
+
+// synthetic generator (grem_gen.h)
+void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, uint64_t perm_mask,
+                      uint32_t perm_bits, uint64_t e0, uint64_t count, uint32_t* out, cudaStream_t s);
+
+}  // namespace grem

@@ -1,0 +1,986 @@
+// grem_runtime.cu — host orchestration and the C ABI of libgrem_b200.so.
+//
+// Mirrors the reference drivers (paths relative to pkg/src/streamcut/):
+//   bisect        grem.py:192-224   chunk loop, seed on pass 0 chunk 0, fill
+//   partition     grem.py:277-319   recursive bisection over induced subgraphs
+//   count_cuts    grem.py:227-252
+//   ingest        edgefile.py:107-126,186-219,371-465 (GRPE u32 -> HBM through
+//                 two pinned chunk buffers; ResidencyMeter schedule)
+// All edge data stays resident in HBM for the whole call; per-node state is
+// O(n) device arrays (grem_core.cuh).  The host only reads a handful of
+// scalars per chunk round (N_c, labels changed).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/grem_b200.h"
+#include "grem_core.cuh"
+#include "grem_gen.h"
+#include "grem_kernels.cuh"
+
+using namespace grem;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct GremError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw GremError{code, msg}; }
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            fail(GREM_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));        \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;   // elements
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        size_t c = n + n / 8 + 64;
+        CK(cudaMalloc(&p, c * sizeof(T)));
+        cap = c;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct grem_ctx {
+    int device = 0;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // per node
+    DBuf<int8_t> lab;
+    DBuf<uint8_t> tl, flag;
+    DBuf<unsigned long long> cnt;
+    DBuf<double2> nbr;
+    DBuf<int32_t> rank, scratch, newid;
+    // per chunk node
+    DBuf<uint32_t> nodes;
+    DBuf<uint8_t> meta, bad, want;
+    DBuf<int32_t> newb, x;
+    DBuf<Clamp> tile_agg;
+    DBuf<long long> tile_x, tile_bad;
+    // seed
+    DBuf<int32_t> start, cursor;
+    DBuf<uint32_t> adj, row_of, parent, csize, roots, rvals, rvals2, cpos, disc, frontier;
+    DBuf<unsigned long long> ckey, rkeys, rkeys2, cand, cand2, pair;
+    DBuf<int8_t> slab, slab2;
+    DBuf<int64_t> fdeg, cum;
+    // scalars
+    long long* d_sizes = nullptr;   // [2]
+    long long* d_scal = nullptr;    // [8]
+    long long* d_sscal = nullptr;   // [16] seed scalars
+    long long* h_pin = nullptr;     // [32] pinned mirror
+    // cub temp
+    DBuf<unsigned char> temp;
+    // ingest
+    void* pin_buf[2] = {nullptr, nullptr};
+    size_t pin_bytes = 0;
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    DBuf<uint2> edges_owned;
+    // count_cuts
+    DBuf<unsigned long long> cc_sizes;
+    DBuf<int32_t> lab32;
+    // live state for hooks
+    int64_t live_n = 0;
+    grem_stats stats{};
+    long long kernels = 0;
+};
+
+namespace {
+
+void scal_read(grem_ctx* c, const long long* dsrc, int count) {
+    CK(cudaMemcpyAsync(c->h_pin, dsrc, sizeof(long long) * count, cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+}
+
+void scal_write(grem_ctx* c, long long* ddst, const long long* vals, int count) {
+    // stage through a private pinned slot so the async copy never races the host
+    for (int i = 0; i < count; ++i) c->h_pin[16 + i] = vals[i];
+    CK(cudaMemcpyAsync(ddst, c->h_pin + 16, sizeof(long long) * count, cudaMemcpyHostToDevice, c->s));
+    CK(cudaStreamSynchronize(c->s));
+}
+
+void ensure_temp(grem_ctx* c, size_t bytes) { c->temp.ensure(bytes); }
+
+void ensure_nodes(grem_ctx* c, int64_t n) {
+    c->lab.ensure(n);
+    c->tl.ensure(n);
+    c->flag.ensure(n);
+    c->cnt.ensure(n);
+    c->nbr.ensure(n);
+    c->rank.ensure(n);
+    c->scratch.ensure(2 * n + 2);
+    c->newid.ensure(n + 1);
+    ensure_temp(c, select_nodes_temp_bytes(n));
+    ensure_temp(c, scan_temp_bytes(n + 1));
+}
+
+void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
+    c->nodes.ensure(nc_cap);
+    c->meta.ensure(nc_cap);
+    c->bad.ensure(nc_cap);
+    c->want.ensure(nc_cap);
+    c->newb.ensure(nc_cap + 1);
+    c->x.ensure(nc_cap + 1);
+    int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
+    c->tile_agg.ensure(tiles);
+    c->tile_x.ensure(tiles);
+    c->tile_bad.ensure(tiles);
+    ensure_temp(c, scan_temp_bytes(nc_cap + 1));
+    ensure_temp(c, sort_temp_bytes(nc_cap));
+}
+
+void ensure_seed(grem_ctx* c, int64_t nc, int64_t entries) {
+    c->start.ensure(nc + 1);
+    c->cursor.ensure(nc + 1);
+    c->adj.ensure(entries + 1);
+    c->row_of.ensure(entries + 1);
+    c->parent.ensure(nc);
+    c->csize.ensure(nc);
+    c->roots.ensure(nc);
+    c->rvals.ensure(nc);
+    c->rvals2.ensure(nc);
+    c->cpos.ensure(nc);
+    c->disc.ensure(nc);
+    c->frontier.ensure(nc);
+    c->ckey.ensure(nc);
+    c->rkeys.ensure(nc);
+    c->rkeys2.ensure(nc);
+    c->cand.ensure(nc);
+    c->cand2.ensure(nc);
+    c->pair.ensure(nc);
+    c->slab.ensure(nc);
+    c->slab2.ensure(nc);
+    c->fdeg.ensure(nc + 1);
+    c->cum.ensure(nc + 1);
+    ensure_temp(c, sort_temp_bytes(nc));
+    ensure_temp(c, scan_temp_bytes(nc + 1));
+}
+
+ChunkBufs chunk_bufs(grem_ctx* c) {
+    ChunkBufs b;
+    b.lab = c->lab.p;
+    b.tl = c->tl.p;
+    b.cnt = c->cnt.p;
+    b.flag = c->flag.p;
+    b.nbr = c->nbr.p;
+    b.nodes = c->nodes.p;
+    b.meta = c->meta.p;
+    b.newb = c->newb.p;
+    b.x = c->x.p;
+    b.bad = c->bad.p;
+    b.tile_agg = c->tile_agg.p;
+    b.tile_x = c->tile_x.p;
+    b.tile_bad = c->tile_bad.p;
+    b.sizes = c->d_sizes;
+    b.scal = c->d_scal;
+    return b;
+}
+
+SeedBufs seed_bufs(grem_ctx* c) {
+    SeedBufs sb;
+    sb.rank = c->rank.p;
+    sb.start = c->start.p;
+    sb.cursor = c->cursor.p;
+    sb.adj = c->adj.p;
+    sb.row_of = c->row_of.p;
+    sb.parent = c->parent.p;
+    sb.ckey = c->ckey.p;
+    sb.csize = c->csize.p;
+    sb.roots = c->roots.p;
+    sb.rkeys = c->rkeys.p;
+    sb.rkeys2 = c->rkeys2.p;
+    sb.rvals = c->rvals.p;
+    sb.rvals2 = c->rvals2.p;
+    sb.cpos = c->cpos.p;
+    sb.slab = c->slab.p;
+    sb.slab2 = c->slab2.p;
+    sb.disc = c->disc.p;
+    sb.frontier = c->frontier.p;
+    sb.cand_keys = c->cand.p;
+    sb.cand_keys2 = c->cand2.p;
+    sb.fdeg = c->fdeg.p;
+    sb.cum = c->cum.p;
+    sb.pair = c->pair.p;
+    sb.want = c->want.p;
+    sb.scal = c->d_sscal;
+    return sb;
+}
+
+struct BisectArgs {
+    const uint2* e;
+    int64_t m, n;
+    int64_t chunk;
+    long long cap;
+    int refine, passes, seed_algo, seed_passes;
+    const grem_hooks* hooks;
+};
+
+// ------------------------------------------------------------ seed chunk
+__global__ void k_count_diff(const int8_t* a, const int8_t* b, int64_t n, long long* out) {
+    int d = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d += a[i] != b[i];
+    for (int off = 16; off; off >>= 1) d += __shfl_down_sync(0xffffffffu, d, off);
+    if ((threadIdx.x & 31) == 0 && d) atomicAdd((unsigned long long*)out, (unsigned long long)d);
+}
+
+void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
+    cudaStream_t s = c->s;
+    ChunkBufs b = chunk_bufs(c);
+    launch_mark_all(e, mc, c->flag.p, s);
+    launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
+    c->kernels += 2;
+    scal_read(c, c->d_scal, 1);
+    int64_t nc = c->h_pin[0];
+    if (nc == 0) fail(GREM_E_FORMAT, "cannot seed an empty chunk");
+    if (2 * a.cap < nc)
+        fail(GREM_E_CAPACITY, "capacity " + std::to_string(a.cap) + " infeasible for " + std::to_string(nc) +
+                                  " chunk nodes");
+    c->stats.visits += nc;
+    launch_set_rank(c->nodes.p, nc, c->rank.p, s);
+    ensure_seed(c, nc, 0);
+    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));
+    launch_degrees(e, mc, c->rank.p, c->cursor.p, s);
+    exclusive_sum_i32(c->cursor.p, c->start.p, nc + 1, c->temp.p, c->temp.cap, s);
+    c->kernels += 3;
+    int32_t entries32 = 0;
+    CK(cudaMemcpyAsync(&c->h_pin[0], c->start.p + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(&entries32, &c->h_pin[0], sizeof(int32_t));
+    int64_t entries = entries32;
+    ensure_seed(c, nc, entries);
+    SeedBufs sb = seed_bufs(c);
+    CK(cudaMemcpyAsync(c->cursor.p, c->start.p, sizeof(int32_t) * nc, cudaMemcpyDeviceToDevice, s));
+    launch_fill_csr(e, mc, c->rank.p, c->cursor.p, c->adj.p, c->row_of.p, s);
+    c->kernels += 1;
+    long long target = (nc + 1) / 2;   // ceil(n / 2), seed.py:57
+
+    if (a.seed_algo == 1) {
+        // SeedConfig(algorithm="random"): numpy PCG64 permutation on the host (seed.py:48-52)
+        if (!a.hooks || !a.hooks->seed) fail(GREM_E_FORMAT, "random seed needs a seed hook");
+        std::vector<int8_t> hl(nc);
+        if (a.hooks->seed(nc, hl.data(), a.hooks->user)) fail(GREM_E_CALLBACK, "seed hook failed");
+        CK(cudaMemcpyAsync(c->slab.p, hl.data(), nc, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    } else {
+        // ---- _bfs_grow (seed.py:56-94): components in restart order, BFS only
+        // inside the component where the pick count crosses `target`.
+        launch_cc(e, mc, c->rank.p, c->parent.p, nc, s);
+        launch_comp_keys(sb, nc, s);
+        ensure_temp(c, select_nodes_temp_bytes(nc));
+        launch_select_roots(sb, nc, c->temp.p, c->temp.cap, s);
+        c->kernels += 5;
+        scal_read(c, c->d_sscal, 1);
+        int64_t nr = c->h_pin[0];
+        launch_root_keys(sb, nr, s);
+        sort_pairs_u64_u32(c->rkeys.p, c->rkeys2.p, c->rvals.p, c->rvals2.p, nr, c->temp.p, c->temp.cap, s);
+        launch_boundary(sb, nr, target, c->temp.p, c->temp.cap, s);
+        c->kernels += 6;
+        scal_read(c, c->d_sscal, 4);
+        long long quota = c->h_pin[2];
+        long long sstar = c->h_pin[3];
+        launch_seed_labels(sb, nc, s);
+        c->kernels += 1;
+        long long count = 1;
+        if (count < quota) {
+            long long h = sstar;
+            uint32_t s32 = (uint32_t)h;
+            c->h_pin[20] = 0;
+            memcpy(&c->h_pin[20], &s32, sizeof(uint32_t));
+            CK(cudaMemcpyAsync(c->frontier.p, &c->h_pin[20], sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            int64_t fsize = 1;
+            long long rbase = 0;
+            while (count < quota) {
+                launch_frontier_degrees(sb, fsize, s);
+                CK(cudaMemsetAsync(c->fdeg.p + fsize, 0, sizeof(int64_t), s));
+                exclusive_sum_i64(c->fdeg.p, c->cum.p, fsize + 1, c->temp.p, c->temp.cap, s);
+                CK(cudaMemsetAsync(c->d_sscal + 4, 0, sizeof(long long), s));
+                CK(cudaMemcpyAsync(&c->h_pin[0], c->cum.p + fsize, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                int64_t total = c->h_pin[0];
+                if (total > 0) launch_bfs_expand(sb, fsize, rbase, total, s);
+                c->kernels += 3;
+                scal_read(c, c->d_sscal + 4, 1);
+                int64_t ncand = c->h_pin[0];
+                if (ncand == 0) fail(GREM_E_FORMAT, "internal: BFS frontier exhausted before quota");
+                launch_cand_keys(sb, ncand, s);
+                sort_keys_u64(c->cand.p, c->cand2.p, ncand, c->temp.p, c->temp.cap, s);
+                int64_t take = ncand < quota - count ? ncand : quota - count;
+                launch_bfs_take(sb, ncand, take, s);
+                c->kernels += 3;
+                c->stats.seed_bfs_levels++;
+                count += take;
+                rbase += fsize;
+                fsize = take;
+            }
+        }
+        launch_seed_finalize(sb, nc, s);
+        c->kernels += 1;
+        // ---- boundary refinement passes (seed.py:96-116): rounds to a
+        // fixpoint with the exact sizes scan (moves are clamps, no ties)
+        long long xstart = target;
+        SeedBufs cur = sb;   // cur.slab = pre-pass labels P, cur.slab2 = tentative T
+        for (int pass = 0; pass < a.seed_passes; ++pass) {
+            CK(cudaMemcpyAsync(cur.slab2, cur.slab, nc, cudaMemcpyDeviceToDevice, s));
+            scal_write(c, c->d_sscal + 6, &xstart, 1);
+            for (int round = 0;; ++round) {
+                launch_row_counts(cur, cur.slab2, cur.slab, 0, entries, nc, s);
+                launch_refine_scan(cur, b, nc, a.cap, s);
+                CK(cudaMemsetAsync(c->d_sscal + 5, 0, sizeof(long long), s));
+                launch_refine_decide(cur, b, nc, a.cap, s);
+                c->kernels += 6;
+                scal_read(c, c->d_sscal + 5, 1);
+                if (c->h_pin[0] == 0) break;
+                if (round > nc + 2) fail(GREM_E_FORMAT, "internal: refinement rounds did not converge");
+            }
+            CK(cudaMemsetAsync(c->d_sscal + 7, 0, sizeof(long long), s));
+            k_count_diff<<<148 * 4, 256, 0, s>>>(cur.slab, cur.slab2, nc, c->d_sscal + 7);
+            c->kernels += 1;
+            scal_read(c, c->d_sscal + 7, 1);
+            if (c->h_pin[0] == 0) break;   // "if not moved: break"
+            CK(cudaMemcpyAsync(&c->h_pin[0], c->x.p + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            int32_t xe32;
+            memcpy(&xe32, &c->h_pin[0], sizeof(int32_t));
+            xstart = xe32;
+            int8_t* t = cur.slab;
+            cur.slab = cur.slab2;
+            cur.slab2 = t;
+        }
+        sb = cur;
+    }
+    // ---- _seed_chunk (grem.py:158-174): labels, sizes recount, estimates
+    launch_row_counts(sb, sb.slab, sb.slab, 1, entries, nc, s);
+    CK(cudaMemsetAsync(c->d_sscal + 7, 0, sizeof(long long), s));
+    launch_seed_commit(sb, b, c->nodes.p, nc, s);
+    c->kernels += 2;
+    scal_read(c, c->d_sscal + 7, 1);
+    long long zeros = c->h_pin[0];
+    long long sz[2] = {zeros, nc - zeros};
+    scal_write(c, c->d_sizes, sz, 2);
+}
+
+// ------------------------------------------------------------ process_chunk
+void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
+    cudaStream_t s = c->s;
+    ChunkBufs b = chunk_bufs(c);
+    CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, s));
+    launch_count_init(e, mc, b, s);
+    launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
+    c->kernels += 2;
+    scal_read(c, c->d_scal, 1);
+    int64_t nc = c->h_pin[0];
+    c->stats.visits += nc;
+    launch_node_init(b, nc, a.refine, s);
+    exclusive_sum_i32(c->x.p, c->newb.p, nc, c->temp.p, c->temp.cap, s);
+    launch_add_base(c->newb.p, nc, c->d_sizes, s);
+    c->kernels += 3;
+    int64_t rounds = 0;
+    for (int r = 1;; ++r) {
+        rounds++;
+        if (r > 1) {
+            launch_count_delta(e, mc, b, s);
+            c->kernels++;
+        }
+        launch_prefs(b, nc, r == 1, s);
+        CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
+        CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
+        launch_chunk_scan(b, nc, a.cap, s);
+        launch_walk(b, nc, a.cap, s);
+        launch_decide(b, nc, a.cap, s);
+        c->kernels += 6;
+        scal_read(c, c->d_scal + 1, 1);
+        if (c->h_pin[0] == 0) break;
+        if (r > nc + 2) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
+    }
+    launch_commit(b, nc, s);
+    launch_sizes_update(b, nc, s);
+    c->kernels += 2;
+    scal_read(c, c->d_scal + 3, 1);
+    c->stats.walk_steps += c->h_pin[0];
+    c->stats.rounds += rounds;
+    if (rounds > c->stats.max_rounds) c->stats.max_rounds = rounds;
+}
+
+// meter schedule of stream_chunks/_raw_chunks (edgefile.py:384-391,453-462)
+struct Meter {
+    const grem_hooks* h;
+    int64_t prev = -1;
+    void acquire(int64_t n) {
+        if (h && h->meter) h->meter(n, h->user);
+    }
+    void on_chunk(int64_t n) {
+        acquire(n);
+        if (prev >= 0 && h && h->meter) h->meter(-prev, h->user);
+        prev = n;
+    }
+    void end() {
+        if (prev >= 0 && h && h->meter) h->meter(-prev, h->user);
+        prev = -1;
+    }
+};
+
+// bisect (grem.py:192-224) on device-resident edges; leaves labels in c->lab
+void bisect_core(grem_ctx* c, const BisectArgs& a) {
+    cudaStream_t s = c->s;
+    if (a.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+    if (2 * a.cap < a.n)
+        fail(GREM_E_CAPACITY, "capacity " + std::to_string(a.cap) + " cannot hold " + std::to_string(a.n) +
+                                  " nodes across two parts");
+    if (a.chunk < 1) fail(GREM_E_FORMAT, "chunk_size must be >= 1");
+    c->stats.bisections++;
+    ensure_nodes(c, a.n);
+    int64_t nc_cap = a.n < 2 * a.chunk ? a.n : 2 * a.chunk;
+    ensure_chunk(c, nc_cap, 0);
+    CK(cudaMemsetAsync(c->lab.p, 0xFF, a.n, s));
+    CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
+    CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
+    CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
+    CK(cudaMemsetAsync(c->d_sizes, 0, sizeof(long long) * 2, s));
+    c->live_n = a.n;
+    int64_t num_chunks = a.m ? (a.m + a.chunk - 1) / a.chunk : 0;
+    for (int pass = 0; pass < a.passes; ++pass) {
+        Meter meter{a.hooks};
+        for (int64_t ci = 0; ci < num_chunks; ++ci) {
+            int64_t lo = ci * a.chunk;
+            int64_t mc = a.m - lo < a.chunk ? a.m - lo : a.chunk;
+            meter.on_chunk(mc);
+            const uint2* e = a.e + lo;
+            if (pass == 0 && ci == 0) seed_chunk(c, a, e, mc);
+            else process_chunk(c, a, e, mc);
+            c->stats.chunks++;
+            if (a.hooks && a.hooks->on_chunk) {
+                scal_read(c, c->d_sizes, 2);
+                long long sz[2] = {c->h_pin[0], c->h_pin[1]};
+                int64_t sz64[2] = {sz[0], sz[1]};
+                if (a.hooks->on_chunk(sz64, a.hooks->user)) {
+                    meter.end();
+                    fail(GREM_E_CALLBACK, "on_chunk hook raised");
+                }
+            }
+        }
+        meter.end();
+    }
+    // _fill_unassigned (grem.py:177-189)
+    launch_fill_unassigned(c->lab.p, a.n, c->d_sizes, c->scratch.p, c->temp.p, c->temp.cap, s);
+    c->kernels += 3;
+}
+
+int64_t plan_chunk(const grem_config* cfg, int64_t m) {
+    // ChunkPlan.plan (edgefile.py:338-349); GremConfig.plan_for default 0.1
+    if (cfg->chunk_edges > 0) return cfg->chunk_edges;
+    double frac = cfg->chunk_frac > 0 ? cfg->chunk_frac : 0.1;
+    if (!(frac > 0 && frac <= 1)) fail(GREM_E_FORMAT, "chunk_frac must be in (0, 1]");
+    double t = frac * (double)m;
+    int64_t ce = (int64_t)std::ceil(t);
+    return ce < 1 ? 1 : ce;
+}
+
+void validate_cfg(const grem_config* cfg) {
+    if (cfg->capacity_slack < 0) fail(GREM_E_FORMAT, "capacity_slack must be >= 0");
+    if (cfg->passes < 1) fail(GREM_E_FORMAT, "passes must be >= 1");
+    if (cfg->seed_refinement_passes < 0) fail(GREM_E_FORMAT, "refinement_passes must be >= 0");
+    if (cfg->seed_algo != 0 && cfg->seed_algo != 1) fail(GREM_E_FORMAT, "unknown seed algorithm");
+}
+
+// count_cuts on device edges / int32 device labels
+void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, int64_t n, grem_report* rep) {
+    cudaStream_t s = c->s;
+    int64_t cap = rep && rep->sizes_cap > 0 ? rep->sizes_cap : 2;
+    if (cap < 2) cap = 2;
+    c->cc_sizes.ensure(cap + 4);
+    unsigned long long* d = c->cc_sizes.p;   // [0] cut, [1] max|neg, [2..] sizes
+    CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (cap + 4), s));
+    int* d_max = (int*)(d + 1);
+    int* d_neg = d_max + 1;
+    CK(cudaMemsetAsync(d_max, 0xFF, sizeof(int), s));   // -1
+    launch_count_cuts(e, m, lab, n, d, d + 2, cap, d_max, d_neg, s);
+    c->kernels += 2;
+    std::vector<unsigned long long> h(cap + 2);
+    CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * (cap + 2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int mx, neg;
+    memcpy(&mx, &h[1], sizeof(int));
+    memcpy(&neg, ((char*)&h[1]) + sizeof(int), sizeof(int));
+    if (neg) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+    int64_t np = mx >= 0 ? (int64_t)mx + 1 : 1;
+    if (rep) {
+        rep->total_edges = m;
+        rep->cut_edges = (int64_t)h[0];
+        rep->num_parts = np;
+        if (rep->partition_sizes) {
+            if (np > rep->sizes_cap) fail(GREM_E_FORMAT, "partition_sizes buffer too small");
+            for (int64_t k = 0; k < np; ++k) rep->partition_sizes[k] = (int64_t)h[2 + k];
+        }
+    }
+}
+
+// ------------------------------------------------------------ ingest
+// host (pageable) edges -> HBM through two pinned staging buffers, so the
+// copy engine overlaps the host-side copy of the next block.
+void ensure_pinned(grem_ctx* c, size_t bytes) {
+    if (c->pin_bytes >= bytes) return;
+    for (int i = 0; i < 2; ++i) {
+        if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
+        c->pin_buf[i] = nullptr;
+        CK(cudaHostAlloc(&c->pin_buf[i], bytes, cudaHostAllocDefault));
+        if (!c->pin_ev[i]) CK(cudaEventCreateWithFlags(&c->pin_ev[i], cudaEventDisableTiming));
+    }
+    c->pin_bytes = bytes;
+}
+
+template <class Fill>
+void staged_upload(grem_ctx* c, void* dst, uint64_t total, Fill fill) {
+    const size_t block = 64ull << 20;
+    ensure_pinned(c, block);
+    uint64_t off = 0;
+    int k = 0;
+    bool used[2] = {false, false};
+    while (off < total) {
+        size_t len = total - off < block ? (size_t)(total - off) : block;
+        int i = k & 1;
+        if (used[i]) CK(cudaEventSynchronize(c->pin_ev[i]));
+        fill(c->pin_buf[i], off, len);
+        CK(cudaMemcpyAsync((char*)dst + off, c->pin_buf[i], len, cudaMemcpyHostToDevice, c->s));
+        CK(cudaEventRecord(c->pin_ev[i], c->s));
+        used[i] = true;
+        off += len;
+        k++;
+    }
+    CK(cudaStreamSynchronize(c->s));
+}
+
+const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device) {
+    if (n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+    if (n >= (1LL << 31)) fail(GREM_E_FORMAT, "num_nodes >= 2^31 is not supported by the GPU path");
+    const uint2* d;
+    if (on_device || m == 0) {
+        d = reinterpret_cast<const uint2*>(edges);
+    } else {
+        c->edges_owned.ensure(m);
+        staged_upload(c, c->edges_owned.p, (uint64_t)m * 8,
+                      [&](void* buf, uint64_t off, size_t len) { memcpy(buf, (const char*)edges + off, len); });
+        d = c->edges_owned.p;
+    }
+    if (m > 0) {
+        // _check_ids (edgefile.py:63-65)
+        unsigned long long* tmp;
+        c->cc_sizes.ensure(4);
+        tmp = c->cc_sizes.p;
+        CK(cudaMemsetAsync(tmp, 0, sizeof(unsigned long long), c->s));
+        launch_check_ids(d, m, (uint32_t*)tmp, c->s);
+        CK(cudaMemcpyAsync(&c->h_pin[0], tmp, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        uint32_t mx;
+        memcpy(&mx, &c->h_pin[0], sizeof(uint32_t));
+        if ((int64_t)mx >= n)
+            fail(GREM_E_FORMAT, "edge endpoint " + std::to_string(mx) + " >= num_nodes " + std::to_string(n));
+    }
+    return d;
+}
+
+struct GrpeHeader {
+    int64_t n, m;
+};
+
+GrpeHeader read_grpe_header(const char* path) {
+    FILE* f = fopen(path, "rb");
+    if (!f) fail(GREM_E_FORMAT, std::string(path) + ": cannot open");
+    unsigned char h[28];
+    size_t got = fread(h, 1, 28, f);
+    fseek(f, 0, SEEK_END);
+    long long size = ftell(f);
+    fclose(f);
+    if (got < 28) fail(GREM_E_FORMAT, std::string(path) + ": too short for a binary edge header");
+    if (memcmp(h, "GRPE", 4) != 0) fail(GREM_E_FORMAT, std::string(path) + ": bad magic");
+    uint32_t version, flags;
+    uint64_t n, m;
+    memcpy(&version, h + 4, 4);
+    memcpy(&flags, h + 8, 4);
+    memcpy(&n, h + 12, 8);
+    memcpy(&m, h + 20, 8);
+    if (version != 1) fail(GREM_E_FORMAT, std::string(path) + ": unsupported version");
+    if (flags & 1) fail(GREM_E_FORMAT, std::string(path) + ": 64-bit ids are parsed by the Python layer");
+    if ((uint64_t)size != 28 + m * 8)
+        fail(GREM_E_FORMAT, std::string(path) + ": payload length does not match header num_edges");
+    return GrpeHeader{(int64_t)n, (int64_t)m};
+}
+
+const uint2* load_grpe(grem_ctx* c, const char* path, GrpeHeader* hd) {
+    *hd = read_grpe_header(path);
+    int64_t m = hd->m;
+    if (m == 0) return nullptr;
+    c->edges_owned.ensure(m);
+    FILE* f = fopen(path, "rb");
+    if (!f) fail(GREM_E_FORMAT, std::string(path) + ": cannot open");
+    fseek(f, 28, SEEK_SET);
+    bool ok = true;
+    staged_upload(c, c->edges_owned.p, (uint64_t)m * 8, [&](void* buf, uint64_t, size_t len) {
+        if (fread(buf, 1, len, f) != len) ok = false;
+    });
+    fclose(f);
+    if (!ok) fail(GREM_E_FORMAT, std::string(path) + ": truncated payload");
+    return stage_edges(c, reinterpret_cast<const uint32_t*>(c->edges_owned.p), m, hd->n, 1);
+}
+
+void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_config* cfg, int64_t capacity,
+                  const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+    validate_cfg(cfg);
+    BisectArgs a;
+    a.e = d;
+    a.m = m;
+    a.n = n;
+    a.chunk = plan_chunk(cfg, m);
+    a.cap = capacity > 0 ? capacity : (long long)std::ceil((1.0 + cfg->capacity_slack) * (double)n / 2);
+    a.refine = cfg->refine;
+    a.passes = cfg->passes;
+    a.seed_algo = cfg->seed_algo;
+    a.seed_passes = cfg->seed_refinement_passes;
+    a.hooks = hooks;
+    bisect_core(c, a);
+    c->lab32.ensure(n);
+    launch_labels_to_i32(c->lab.p, n, c->lab32.p, c->s);
+    c->kernels++;
+    if (rep) count_cuts_dev(c, d, m, c->lab32.p, n, rep);
+    if (labels_out) CK(cudaMemcpyAsync(labels_out, c->lab32.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+}
+
+// partition (grem.py:277-319): depth-first like the reference; both sides
+// are extracted (device-resident, file order kept) before recursing, so the
+// parent's labels can be overwritten by the child bisections.
+struct PartCtx {
+    int64_t total_nodes;
+    const grem_config* cfg;
+    const grem_hooks* hooks;
+    int32_t* final_lab;
+};
+
+void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, const int32_t* orig, int64_t p_level,
+             int level, int64_t leaf_base) {
+    cudaStream_t s = c->s;
+    double capd = std::ceil((1.0 + pc.cfg->capacity_slack) * (double)pc.total_nodes / (double)(1LL << (level + 1)));
+    BisectArgs a;
+    a.e = e;
+    a.m = m;
+    a.n = n;
+    a.chunk = plan_chunk(pc.cfg, m);
+    a.cap = (long long)capd;
+    a.refine = pc.cfg->refine;
+    a.passes = pc.cfg->passes;
+    a.seed_algo = pc.cfg->seed_algo;
+    a.seed_passes = pc.cfg->seed_refinement_passes;
+    a.hooks = pc.hooks ? pc.hooks : nullptr;
+    grem_hooks sub = pc.hooks ? *pc.hooks : grem_hooks{nullptr, nullptr, nullptr, nullptr};
+    sub.on_chunk = nullptr;   // partition() passes only the meter down (grem.py:300)
+    a.hooks = &sub;
+    bisect_core(c, a);
+    if (p_level == 2) {
+        launch_leaf_write(c->lab.p, n, orig, (int32_t)leaf_base, pc.final_lab, s);
+        c->kernels++;
+        return;
+    }
+    // extract both sides
+    uint2* sub_e = nullptr;
+    int32_t* sub_o = nullptr;
+    CK(cudaMallocAsync(&sub_e, sizeof(uint2) * (m > 0 ? m : 1), s));
+    CK(cudaMallocAsync(&sub_o, sizeof(int32_t) * n, s));
+    int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
+    ensure_temp(c, extract_temp_bytes(m > 0 ? m : 1));
+    for (int side = 0; side < 2; ++side) {
+        int32_t* flags = c->scratch.p;
+        launch_side_flags(c->lab.p, n, side, flags, s);
+        exclusive_sum_i32(flags, c->newid.p, n, c->temp.p, c->temp.cap, s);
+        CK(cudaMemcpyAsync(&c->h_pin[0], c->newid.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(((int32_t*)&c->h_pin[0]) + 1, flags + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int32_t v[2];
+        memcpy(v, &c->h_pin[0], sizeof(v));
+        int64_t k = (int64_t)v[0] + v[1];
+        launch_sub_orig(c->lab.p, n, side, c->newid.p, orig, sub_o + n_off[side], s);
+        int64_t kept = 0;
+        if (m > 0) {
+            launch_extract(e, m, c->lab.p, side, c->newid.p, sub_e + e_off[side], c->d_scal + 7, c->temp.p,
+                           c->temp.cap, s);
+            scal_read(c, c->d_scal + 7, 1);
+            kept = c->h_pin[0];
+        }
+        c->kernels += 5;
+        e_off[side + 1] = e_off[side] + kept;
+        n_off[side + 1] = n_off[side] + k;
+    }
+    for (int side = 0; side < 2; ++side) {
+        int64_t k = n_off[side + 1] - n_off[side];
+        if (k == 0) continue;   // grem.py:308-309
+        int64_t base = leaf_base + side * (p_level / 2);
+        recurse(c, pc, sub_e + e_off[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
+                level + 1, base);
+    }
+    CK(cudaFreeAsync(sub_e, s));
+    CK(cudaFreeAsync(sub_o, s));
+}
+
+void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t p, const grem_config* cfg,
+                     const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+    if (p < 2 || (p & (p - 1)) != 0)
+        fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
+    validate_cfg(cfg);
+    cudaStream_t s = c->s;
+    int32_t* fin = nullptr;
+    int32_t* orig = nullptr;
+    CK(cudaMallocAsync(&fin, sizeof(int32_t) * n, s));
+    CK(cudaMallocAsync(&orig, sizeof(int32_t) * n, s));
+    CK(cudaMemsetAsync(fin, 0xFF, sizeof(int32_t) * n, s));
+    launch_iota(orig, n, s);
+    PartCtx pc{n, cfg, hooks, fin};
+    try {
+        recurse(c, pc, d, m, n, orig, p, 0, 0);
+        count_cuts_dev(c, d, m, fin, n, rep);
+        if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaFreeAsync(fin, s);
+        cudaFreeAsync(orig, s);
+        cudaStreamSynchronize(s);
+        throw;
+    }
+    CK(cudaFreeAsync(fin, s));
+    CK(cudaFreeAsync(orig, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+template <class F>
+int guarded(grem_ctx* c, F f) {
+    g_err.clear();
+    try {
+        if (c) {
+            CK(cudaSetDevice(c->device));
+            memset(&c->stats, 0, sizeof(c->stats));
+            c->kernels = 0;
+            CK(cudaEventRecord(c->ev0, c->s));
+        }
+        f();
+        if (c) {
+            CK(cudaEventRecord(c->ev1, c->s));
+            CK(cudaEventSynchronize(c->ev1));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            c->stats.ms_total = ms;
+            c->stats.kernels = c->kernels;
+        }
+        return GREM_OK;
+    } catch (const GremError& e) {
+        g_err = e.msg;
+        if (c) cudaStreamSynchronize(c->s);
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GREM_E_NOMEM;
+    }
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+
+extern "C" {
+
+const char* grem_last_error(void) { return g_err.c_str(); }
+
+grem_ctx* grem_create(int device) {
+    g_err.clear();
+    grem_ctx* c = new grem_ctx();
+    c->device = device;
+    try {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&c->ev0));
+        CK(cudaEventCreate(&c->ev1));
+        CK(cudaMalloc(&c->d_sizes, sizeof(long long) * 2));
+        CK(cudaMalloc(&c->d_scal, sizeof(long long) * 8));
+        CK(cudaMalloc(&c->d_sscal, sizeof(long long) * 16));
+        CK(cudaHostAlloc(&c->h_pin, sizeof(long long) * 32, cudaHostAllocDefault));
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        ensure_temp(c, 1 << 20);
+    } catch (const GremError& e) {
+        g_err = e.msg;
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+void grem_destroy(grem_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->s);
+    c->lab.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
+    c->rank.release(); c->scratch.release(); c->newid.release();
+    c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
+    c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
+    c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release(); c->parent.release();
+    c->csize.release(); c->roots.release(); c->rvals.release(); c->rvals2.release(); c->cpos.release();
+    c->disc.release(); c->frontier.release(); c->ckey.release(); c->rkeys.release(); c->rkeys2.release();
+    c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
+    c->fdeg.release(); c->cum.release(); c->temp.release(); c->edges_owned.release(); c->cc_sizes.release();
+    c->lab32.release();
+    for (int i = 0; i < 2; ++i) {
+        if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
+        if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
+    }
+    if (c->d_sizes) cudaFree(c->d_sizes);
+    if (c->d_scal) cudaFree(c->d_scal);
+    if (c->d_sscal) cudaFree(c->d_sscal);
+    if (c->h_pin) cudaFreeHost(c->h_pin);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->s) cudaStreamDestroy(c->s);
+    delete c;
+}
+
+int grem_get_stats(grem_ctx* c, grem_stats* out) {
+    if (!c || !out) return GREM_E_FORMAT;
+    *out = c->stats;
+    return GREM_OK;
+}
+
+int grem_bisect_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device, const grem_config* cfg,
+                    int64_t capacity, const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+    if (!c || !cfg) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        bisect_entry(c, d, m, n, cfg, capacity, hooks, labels_out, rep);
+    });
+}
+
+int grem_partition_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device, int64_t p,
+                       const grem_config* cfg, const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+    if (!c || !cfg) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        if (p < 2 || (p & (p - 1)) != 0)
+            fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
+        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        partition_entry(c, d, m, n, p, cfg, hooks, labels_out, rep);
+    });
+}
+
+int grem_count_cuts_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device,
+                        const int32_t* labels, int labels_on_device, grem_report* rep) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        const int32_t* dl = labels;
+        if (!labels_on_device) {
+            c->lab32.ensure(n);
+            CK(cudaMemcpyAsync(c->lab32.p, labels, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->s));
+            dl = c->lab32.p;
+        }
+        count_cuts_dev(c, d, m, dl, n, rep);
+    });
+}
+
+int grem_bisect_file(grem_ctx* c, const char* path, const grem_config* cfg, int64_t capacity,
+                     const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+    if (!c || !cfg || !path) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        GrpeHeader hd;
+        const uint2* d = load_grpe(c, path, &hd);
+        if (hd.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+        bisect_entry(c, d, hd.m, hd.n, cfg, capacity, hooks, labels_out, rep);
+    });
+}
+
+int grem_partition_file(grem_ctx* c, const char* path, int64_t p, const grem_config* cfg, const grem_hooks* hooks,
+                        int32_t* labels_out, grem_report* rep) {
+    if (!c || !cfg || !path) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        if (p < 2 || (p & (p - 1)) != 0)
+            fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
+        GrpeHeader hd;
+        const uint2* d = load_grpe(c, path, &hd);
+        if (hd.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+        partition_entry(c, d, hd.m, hd.n, p, cfg, hooks, labels_out, rep);
+    });
+}
+
+int grem_state_parts(grem_ctx* c, int32_t* out, int64_t n) {
+    if (!c || !out) return GREM_E_FORMAT;
+    g_err.clear();
+    try {
+        if (n != c->live_n) fail(GREM_E_FORMAT, "state size mismatch");
+        std::vector<int8_t> h(n);
+        CK(cudaMemcpyAsync(h.data(), c->lab.p, n, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        for (int64_t i = 0; i < n; ++i) out[i] = h[i];
+    } catch (const GremError& e) {
+        g_err = e.msg;
+        return e.code;
+    }
+    return GREM_OK;
+}
+
+int grem_device_alloc(grem_ctx* c, uint64_t bytes, void** out) {
+    if (!c || !out) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaMalloc(out, bytes ? bytes : 1));
+    });
+}
+int grem_device_free(grem_ctx* c, void* p) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] { CK(cudaFree(p)); });
+}
+int grem_memcpy_h2d(grem_ctx* c, void* dst, const void* src, uint64_t bytes) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+int grem_memcpy_d2h(grem_ctx* c, void* dst, const void* src, uint64_t bytes) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int grem_gen_edges_device(grem_ctx* c, uint64_t n, uint32_t beta, uint64_t seed, uint64_t e0, uint64_t count,
+                          uint32_t* dev_out) {
+    if (!c || n < 1 || beta < 1) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(c->device));
+        gg_params p;
+        gg_init(&p, n, beta, seed);
+        launch_gen_edges(p.n, p.beta, p.seed, p.scale, p.perm_mask, p.perm_bits, e0, count, dev_out, c->s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+}  // extern "C"
