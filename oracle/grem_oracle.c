@@ -319,7 +319,7 @@ static int fill_unassigned(state_t* st) {
     return OR_OK;
 }
 
-typedef void (*oracle_chunk_cb)(const int64_t* sizes, void* user);
+typedef void (*oracle_chunk_cb)(const int64_t* sizes, const int8_t* parts, void* user);
 
 /* bisect, grem.py:192-224 (count_cuts is done by the caller) */
 int oracle_bisect(const uint32_t* edges, int64_t m, int64_t n, int64_t chunk_edges, int64_t cap,
@@ -359,7 +359,7 @@ int oracle_bisect(const uint32_t* edges, int64_t m, int64_t n, int64_t chunk_edg
                 if (stats) stats->chunks++;
             }
             chunk_free(&c);
-            if (rc == OR_OK && chunk_cb) chunk_cb(st.sizes, chunk_user);
+            if (rc == OR_OK && chunk_cb) chunk_cb(st.sizes, st.parts, chunk_user);
         }
     }
     if (rc == OR_OK) rc = fill_unassigned(&st);

@@ -27,7 +27,7 @@ _LIB_PATH = os.path.join(_HERE, "build", "libgrem_oracle.so")
 _lib = None
 
 SEED_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_int8), ctypes.c_void_p)
-CHUNK_CB = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
+CHUNK_CB = ctypes.CFUNCTYPE(None, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int8), ctypes.c_void_p)
 
 
 class OracleStats(ctypes.Structure):
@@ -106,7 +106,12 @@ def bisect(edges, n: int, chunk_edges: int, cap: int, refine=True, passes=1, see
     sizes = np.zeros(2, dtype=np.int64)
     seed_cb = _random_seed_cb(rng_seed) if seed_algo == "random" else SEED_CB(0)
     if on_chunk is not None:
-        chunk_cb = CHUNK_CB(lambda s, u: on_chunk((s[0], s[1])))
+        def _cb(s, parts, u):
+            try:
+                on_chunk((s[0], s[1]), np.ctypeslib.as_array(parts, shape=(n,)).astype(np.int32))
+            except TypeError:
+                on_chunk((s[0], s[1]))
+        chunk_cb = CHUNK_CB(_cb)
     else:
         chunk_cb = CHUNK_CB(0)
     st = stats if stats is not None else OracleStats()

@@ -501,7 +501,10 @@ __global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t
         int code = b + 1;
         tl[g] = (uint8_t)(code | (cur << 4));
         ch += (code != cur);
-        meta[i] = (uint8_t)(b ? (m | M_SPEC) : (m & ~M_SPEC));   // next round's tie guess
+        // next round's tie guess: the tie rule evaluated at this round's exact x
+        long long o = meta_old(m) == 0 ? 1 : 0;
+        bool tie0 = ((long long)x[i] - o) <= (((long long)newb[i] - lift) >> 1);
+        meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
     }
     for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
@@ -617,14 +620,26 @@ __global__ void k_cc_link(const uint2* __restrict__ e, int64_t m, const int32_t*
     }
 }
 
-__global__ void k_cc_compress(uint32_t* parent, int64_t nc) {
-    GRID_STRIDE(i, nc) parent[i] = uf_find(parent, (uint32_t)i);
+// After linking the forest is frozen: a read-only walk to the root, written to
+// a separate array (writing parent[] in place would race with other threads'
+// walks through the same node and can leave a non-root parent behind).
+__global__ void k_cc_roots(const uint32_t* __restrict__ parent, int64_t nc, uint32_t* __restrict__ root) {
+    GRID_STRIDE(i, nc) {
+        uint32_t r = (uint32_t)i, p = parent[r];
+        while (p != r) {
+            r = p;
+            p = parent[r];
+        }
+        root[i] = r;
+    }
 }
 
-void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, int64_t nc, cudaStream_t s) {
+void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, uint32_t* scratch, int64_t nc,
+               cudaStream_t s) {
     k_iota_u32<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
     k_cc_link<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, parent);
-    k_cc_compress<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
+    k_cc_roots<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc, scratch);
+    cudaMemcpyAsync(parent, scratch, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, s);
 }
 
 // restart order of _bfs_grow (seed.py:69-75): a component is entered at its

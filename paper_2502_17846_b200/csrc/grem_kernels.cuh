@@ -89,7 +89,8 @@ void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStrea
 void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, cudaStream_t s);
 void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
                      uint32_t* row_of, cudaStream_t s);
-void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, int64_t nc, cudaStream_t s);
+void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, uint32_t* scratch, int64_t nc,
+               cudaStream_t s);
 void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s);
 void launch_select_roots(const SeedBufs& sb, int64_t nc, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_root_keys(const SeedBufs& sb, int64_t nroots, cudaStream_t s);

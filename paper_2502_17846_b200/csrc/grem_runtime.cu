@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,8 +45,11 @@ struct GremError {
 
 template <class T>
 struct DBuf {
+    const char* name = "";
     T* p = nullptr;
     size_t cap = 0;   // elements
+    DBuf() = default;
+    explicit DBuf(const char* nm) : name(nm) {}
     void ensure(size_t n) {
         if (n <= cap) return;
         if (p) cudaFree(p);
@@ -53,6 +57,11 @@ struct DBuf {
         size_t c = n + n / 8 + 64;
         CK(cudaMalloc(&p, c * sizeof(T)));
         cap = c;
+        // debug: GREM_DEBUG_POISON=all|name,name fills new buffers with 0xA5 to
+        // expose reads of memory that was never written in this call
+        static const char* poison = getenv("GREM_DEBUG_POISON");
+        if (poison && (strcmp(poison, "all") == 0 || strstr(poison, (std::string(",") + name + ",").c_str())))
+            CK(cudaMemset(p, 0xA5, c * sizeof(T)));
     }
     void release() {
         if (p) cudaFree(p);
@@ -68,30 +77,30 @@ struct grem_ctx {
     cudaStream_t s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // per node
-    DBuf<int8_t> lab;
-    DBuf<uint8_t> tl, flag;
-    DBuf<unsigned long long> cnt;
-    DBuf<double2> nbr;
-    DBuf<int32_t> rank, scratch, newid;
+    DBuf<int8_t> lab{"lab"};
+    DBuf<uint8_t> tl{"tl"}, flag{"flag"};
+    DBuf<unsigned long long> cnt{"cnt"};
+    DBuf<double2> nbr{"nbr"};
+    DBuf<int32_t> rank{"rank"}, scratch{"scratch"}, newid{"newid"};
     // per chunk node
-    DBuf<uint32_t> nodes;
-    DBuf<uint8_t> meta, bad, want;
-    DBuf<int32_t> newb, x;
-    DBuf<Clamp> tile_agg;
-    DBuf<long long> tile_x, tile_bad;
+    DBuf<uint32_t> nodes{"nodes"};
+    DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
+    DBuf<int32_t> newb{"newb"}, x{"x"};
+    DBuf<Clamp> tile_agg{"tile_agg"};
+    DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
     // seed
-    DBuf<int32_t> start, cursor;
-    DBuf<uint32_t> adj, row_of, parent, csize, roots, rvals, rvals2, cpos, disc, frontier;
-    DBuf<unsigned long long> ckey, rkeys, rkeys2, cand, cand2, pair;
-    DBuf<int8_t> slab, slab2;
-    DBuf<int64_t> fdeg, cum;
+    DBuf<int32_t> start{"start"}, cursor{"cursor"};
+    DBuf<uint32_t> adj{"adj"}, row_of{"row_of"}, parent{"parent"}, csize{"csize"}, roots{"roots"}, rvals{"rvals"}, rvals2{"rvals2"}, cpos{"cpos"}, disc{"disc"}, frontier{"frontier"};
+    DBuf<unsigned long long> ckey{"ckey"}, rkeys{"rkeys"}, rkeys2{"rkeys2"}, cand{"cand"}, cand2{"cand2"}, pair{"pair"};
+    DBuf<int8_t> slab{"slab"}, slab2{"slab2"};
+    DBuf<int64_t> fdeg{"fdeg"}, cum{"cum"};
     // scalars
     long long* d_sizes = nullptr;   // [2]
     long long* d_scal = nullptr;    // [8]
     long long* d_sscal = nullptr;   // [16] seed scalars
     long long* h_pin = nullptr;     // [32] pinned mirror
     // cub temp
-    DBuf<unsigned char> temp;
+    DBuf<unsigned char> temp{"temp"};
     // ingest
     void* pin_buf[2] = {nullptr, nullptr};
     size_t pin_bytes = 0;
@@ -286,7 +295,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     } else {
         // ---- _bfs_grow (seed.py:56-94): components in restart order, BFS only
         // inside the component where the pick count crosses `target`.
-        launch_cc(e, mc, c->rank.p, c->parent.p, nc, s);
+        launch_cc(e, mc, c->rank.p, c->parent.p, c->roots.p, nc, s);
         launch_comp_keys(sb, nc, s);
         ensure_temp(c, select_nodes_temp_bytes(nc));
         launch_select_roots(sb, nc, c->temp.p, c->temp.cap, s);
@@ -984,3 +993,27 @@ int grem_gen_edges_device(grem_ctx* c, uint64_t n, uint32_t beta, uint64_t seed,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- debug
+// Runs the chunk sizes scan (+ tie verification and walk) on caller-provided
+// node maps; used by the GPU unit tests of the scan kernels.
+extern "C" int grem_debug_chunk_scan(grem_ctx* c, const uint8_t* meta, const int32_t* newb, int64_t nc, int64_t x0,
+                                     int64_t cap, int do_walk, int32_t* x_out, uint8_t* bad_out, int64_t* nbad_out) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        ensure_chunk(c, nc + 1, 0);
+        CK(cudaMemcpyAsync(c->meta.p, meta, nc, cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(c->newb.p, newb, sizeof(int32_t) * nc, cudaMemcpyHostToDevice, c->s));
+        long long sz[2] = {x0, 0};
+        scal_write(c, c->d_sizes, sz, 2);
+        CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, c->s));
+        ChunkBufs b = chunk_bufs(c);
+        launch_chunk_scan(b, nc, cap, c->s);
+        if (do_walk) launch_walk(b, nc, cap, c->s);
+        CK(cudaMemcpyAsync(x_out, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost, c->s));
+        CK(cudaMemcpyAsync(bad_out, c->bad.p, nc, cudaMemcpyDeviceToHost, c->s));
+        scal_read(c, c->d_scal + 3, 2);
+        nbad_out[0] = c->h_pin[1];   // flagged ties
+        nbad_out[1] = c->h_pin[0];   // walk steps
+    });
+}

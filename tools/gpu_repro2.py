@@ -1,0 +1,15 @@
+import sys, os
+sys.path.insert(0, ".")
+import numpy as np
+from oracle import oracle
+from paper_2502_17846_b200 import GremConfig, grem, synth, _abi
+s = synth.SHAPES["arxiv"]
+e = synth.shape_edges(s); N = s.num_nodes
+ref = oracle.partition(e, N, 4, chunk_frac=0.1)
+mode = sys.argv[1]
+for rep in range(3):
+    if mode == "fresh" and rep > 0:
+        for d, c in list(grem._ctx.items()):
+            _abi.lib().grem_destroy(c); del grem._ctx[d]
+    lab, _ = grem.partition_edges(e, N, 4, GremConfig(chunk_frac=0.1))
+    print(mode, "rep", rep, "mismatches", int((lab != ref).sum()), flush=True)
