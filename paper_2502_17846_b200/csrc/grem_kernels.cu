@@ -485,6 +485,212 @@ void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) 
     k_walk<<<1, 32, 0, s>>>(b.meta, b.newb, b.x, b.bad, b.tile_bad, nc, cap, b.scal + 4, b.scal + 3);
 }
 
+// ------------------------------------------------------- trajectory bundles
+// Exact repair when tie speculation failed.  Ties pull the
+// sizes chain toward balance, so trajectories started near the true value
+// merge quickly.  Per segment of L nodes a CTA simulates kBundle trajectories
+// from two windows of starting values (around this round's speculative x and
+// around a second predictor); a single warp then chains the segments exactly
+// (a lookup when the exact input falls in a window, a sequential simulation
+// otherwise) and every segment replays its exact trajectory.
+
+struct HalfMapSrc {   // half-step predictor: ties count +1/2 (doubled coordinates)
+    const uint8_t* meta;
+    const int32_t* newb;
+    long long cap;
+    __device__ __forceinline__ NodeMap get(int64_t i) const {
+        NodeMap r;
+        r.o = 0;
+        r.t = 0;
+        uint8_t m = meta[i];
+        if (!meta_active(m)) {
+            r.f = clamp_identity();
+            return r;
+        }
+        long long o = meta_old(m) == 0 ? 1 : 0;
+        long long lift = meta_old(m) != -1 ? 1 : 0;
+        long long sl = (long long)newb[i] - lift;
+        int pref = meta_pref(m);
+        if (pref == 0) r.f = Clamp{2 - 2 * o, -kInf, 2 * cap};
+        else if (pref == 1) r.f = Clamp{-2 * o, 2 * (sl - cap + 1), kInf};
+        else r.f = Clamp{1 - 2 * o, 2 * (sl + 1 - cap), 2 * cap};
+        return r;
+    }
+};
+
+__global__ void k_double_x0(const long long* sizes, long long* out) { *out = 2 * sizes[0]; }
+
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan_down_half(Src src, int64_t N, const long long* tile_x,
+                                                                 int32_t* xo) {
+    __shared__ Clamp smem[kScanThreads / 32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    Clamp acc = clamp_identity();
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i < N) acc = clamp_then(acc, src.get(i).f);
+    }
+    Clamp pre = block_excl_scan<kScanThreads>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, tile_x[blockIdx.x]);
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i >= N) break;
+        xo[i] = (int32_t)(x >> 1);
+        x = clamp_apply(src.get(i).f, x);
+    }
+}
+
+void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_t* xalt, cudaStream_t s) {
+    HalfMapSrc src{b.meta, b.newb, cap};
+    int64_t ntiles = (nc + kScanTile - 1) / kScanTile;
+    k_double_x0<<<1, 1, 0, s>>>(b.sizes, b.scal + 5);
+    k_scan_reduce<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_agg);
+    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.scal + 5, b.tile_x);
+    k_scan_down_half<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, xalt);
+}
+
+// per node: threshold t and lift o packed for the bundle loops (o = 2: inactive)
+__device__ __forceinline__ void bundle_params(uint8_t m, int32_t nb, long long cap, int32_t& t, int8_t& o) {
+    if (!meta_active(m)) {
+        t = 0;
+        o = 2;
+        return;
+    }
+    long long lift = meta_old(m) != -1 ? 1 : 0;
+    NodeMap nm = node_map(m, (long long)nb - lift, cap);
+    t = (int32_t)nm.t;
+    o = (int8_t)nm.o;
+}
+
+constexpr int kBundle = 128;        // trajectories per segment (2 windows x 64)
+constexpr int kBundleHalf = 64;
+constexpr int kBundleBatch = 2048;  // nodes staged in shared memory at a time
+
+__global__ void __launch_bounds__(kBundle) k_bundle_sim(const uint8_t* __restrict__ meta,
+                                                        const int32_t* __restrict__ newb,
+                                                        const int32_t* __restrict__ xspec,
+                                                        const int32_t* __restrict__ xalt, int64_t nc, int64_t L,
+                                                        long long cap, int32_t* __restrict__ ends,
+                                                        const long long* nbad) {
+    if (*nbad == 0) return;
+    __shared__ int32_t st[kBundleBatch];
+    __shared__ int8_t so[kBundleBatch];
+    int64_t lo = (int64_t)blockIdx.x * L;
+    int64_t hi = lo + L < nc ? lo + L : nc;
+    int tid = threadIdx.x;
+    long long c = tid < kBundleHalf ? xspec[lo] : xalt[lo];
+    long long x = c + (tid & (kBundleHalf - 1)) - kBundleHalf / 2;
+    for (int64_t b = lo; b < hi; b += kBundleBatch) {
+        int cnt = (int)(hi - b < kBundleBatch ? hi - b : kBundleBatch);
+        __syncthreads();
+        for (int k = tid; k < cnt; k += kBundle) bundle_params(meta[b + k], newb[b + k], cap, st[k], so[k]);
+        __syncthreads();
+        for (int k = 0; k < cnt; ++k) {
+            int o = so[k];
+            if (o != 2) {
+                long long xl = x - o;
+                x = xl + (xl <= st[k] ? 1 : 0);
+            }
+        }
+    }
+    ends[blockIdx.x * (int64_t)kBundle + tid] = (int32_t)x;
+}
+
+// single warp: exact chain over segments
+__global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__ meta,
+                                                     const int32_t* __restrict__ newb,
+                                                     const int32_t* __restrict__ xspec,
+                                                     const int32_t* __restrict__ xalt, const int32_t* __restrict__ ends,
+                                                     int64_t nseg, int64_t nc, int64_t L, long long cap,
+                                                     const long long* sizes, int32_t* __restrict__ xin,
+                                                     const long long* nbad, long long* misses) {
+    if (*nbad == 0) return;
+    const int lane = threadIdx.x;
+    constexpr int SB = 16;   // segments staged per batch
+    __shared__ int32_t tab[SB][kBundle];
+    __shared__ int32_t cen[SB][2];
+    long long cur = sizes[0];
+    long long nmiss = 0;
+    for (int64_t s0 = 0; s0 < nseg; s0 += SB) {
+        int cnt = (int)(nseg - s0 < SB ? nseg - s0 : SB);
+        __syncwarp();
+        for (int k = lane; k < cnt * kBundle; k += 32) tab[k / kBundle][k % kBundle] = ends[s0 * kBundle + k];
+        if (lane < cnt) {
+            cen[lane][0] = xspec[(s0 + lane) * L];
+            cen[lane][1] = xalt[(s0 + lane) * L];
+        }
+        __syncwarp();
+        for (int j = 0; j < cnt; ++j) {
+            int64_t seg = s0 + j;
+            if (lane == 0) xin[seg] = (int32_t)cur;
+            long long d1 = cur - cen[j][0] + kBundleHalf / 2;
+            long long d2 = cur - cen[j][1] + kBundleHalf / 2;
+            if (d1 >= 0 && d1 < kBundleHalf) {
+                cur = tab[j][d1];
+            } else if (d2 >= 0 && d2 < kBundleHalf) {
+                cur = tab[j][kBundleHalf + d2];
+            } else {   // window miss: simulate the segment (lanes prefetch 32 nodes)
+                nmiss++;
+                int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
+                for (int64_t b = lo; b < hi; b += 32) {
+                    int64_t idx = b + lane;
+                    int32_t t = 0;
+                    int8_t o = 2;
+                    if (idx < hi) bundle_params(meta[idx], newb[idx], cap, t, o);
+                    int lim = (int)(hi - b < 32 ? hi - b : 32);
+                    for (int k = 0; k < lim; ++k) {
+                        int ok = __shfl_sync(0xffffffffu, (int)o, k);
+                        int tk = __shfl_sync(0xffffffffu, t, k);
+                        if (ok != 2) {
+                            long long xl = cur - ok;
+                            cur = xl + (xl <= tk ? 1 : 0);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (lane == 0) atomicAdd((unsigned long long*)misses, (unsigned long long)nmiss);
+}
+
+// every segment replays its exact trajectory: x before each node
+__global__ void k_bundle_final(const uint8_t* __restrict__ meta, const int32_t* __restrict__ newb,
+                               const int32_t* __restrict__ xin, int64_t nseg, int64_t nc, int64_t L, long long cap,
+                               int32_t* __restrict__ x, const long long* nbad) {
+    if (*nbad == 0) return;
+    int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (seg >= nseg) return;
+    int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
+    long long cur = xin[seg];
+    for (int64_t i = lo; i < hi; ++i) {
+        x[i] = (int32_t)cur;
+        int32_t t;
+        int8_t o;
+        bundle_params(meta[i], newb[i], cap, t, o);
+        if (o != 2) {
+            long long xl = cur - o;
+            cur = xl + (xl <= t ? 1 : 0);
+        }
+    }
+    if (hi == nc) x[nc] = (int32_t)cur;
+}
+
+int64_t bundle_segment_len(int64_t nc) {
+    int64_t L = (nc + 4095) / 4096;
+    return L < 64 ? 64 : L;
+}
+
+void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, int32_t* ends, int32_t* xin,
+                   cudaStream_t s) {
+    int64_t L = bundle_segment_len(nc);
+    int64_t nseg = (nc + L - 1) / L;
+    k_bundle_sim<<<(unsigned)nseg, kBundle, 0, s>>>(b.meta, b.newb, b.x, xalt, nc, L, cap, ends, b.scal + 4);
+    k_bundle_chain<<<1, 32, 0, s>>>(b.meta, b.newb, b.x, xalt, ends, nseg, nc, L, cap, b.sizes, xin, b.scal + 4,
+                                    b.scal + 3);
+    k_bundle_final<<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(b.meta, b.newb, xin, nseg, nc, L, cap, b.x,
+                                                                 b.scal + 4);
+}
+
 __global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
                          const int32_t* __restrict__ newb, const int32_t* __restrict__ x, long long cap,
                          uint8_t* __restrict__ tl, long long* changed) {

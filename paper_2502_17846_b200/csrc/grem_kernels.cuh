@@ -28,7 +28,7 @@ struct ChunkBufs {
     long long* tile_bad;
     // device scalars
     long long* sizes;   // [2] live sizes (read-only during a chunk)
-    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 walk steps, 4 nbad
+    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0
 };
 
 constexpr int kScanThreads = 256;
@@ -45,6 +45,11 @@ void launch_prefs(const ChunkBufs& b, int64_t nc, int first_round, cudaStream_t 
 void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t s);
 void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+// exact repair of mis-speculated ties by trajectory bundles (replaces the walk)
+int64_t bundle_segment_len(int64_t nc);
+void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_t* xalt, cudaStream_t s);
+void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, int32_t* ends, int32_t* xin,
+                   cudaStream_t s);
 void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);

@@ -85,7 +85,7 @@ struct grem_ctx {
     // per chunk node
     DBuf<uint32_t> nodes{"nodes"};
     DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
-    DBuf<int32_t> newb{"newb"}, x{"x"};
+    DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, bends{"bends"}, bxin{"bxin"};
     DBuf<Clamp> tile_agg{"tile_agg"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
     // seed
@@ -151,6 +151,10 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->want.ensure(nc_cap);
     c->newb.ensure(nc_cap + 1);
     c->x.ensure(nc_cap + 1);
+    c->xalt.ensure(nc_cap + 1);
+    int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
+    c->bends.ensure(nseg * 128);
+    c->bxin.ensure(nseg);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
     c->tile_agg.ensure(tiles);
     c->tile_x.ensure(tiles);
@@ -416,9 +420,23 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
         launch_chunk_scan(b, nc, a.cap, s);
-        launch_walk(b, nc, a.cap, s);
+        c->kernels += 4;
+        scal_read(c, c->d_scal + 4, 1);
+        if (c->h_pin[0] > 0) {
+            // speculation failed somewhere: exact repair by trajectory bundles;
+            // second window centre = previous round's exact x (round 1: the
+            // half-step predictor)
+            if (r == 1) {
+                launch_half_predictor(b, nc, a.cap, c->xalt.p, s);
+                c->kernels += 4;
+            }
+            launch_bundle(b, nc, a.cap, c->xalt.p, c->bends.p, c->bxin.p, s);
+            c->kernels += 3;
+            c->stats.walk_steps += nc;
+        }
         launch_decide(b, nc, a.cap, s);
-        c->kernels += 6;
+        CK(cudaMemcpyAsync(c->xalt.p, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, s));
+        c->kernels += 1;
         scal_read(c, c->d_scal + 1, 1);
         if (c->h_pin[0] == 0) break;
         if (r > nc + 2) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
@@ -426,8 +444,6 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     launch_commit(b, nc, s);
     launch_sizes_update(b, nc, s);
     c->kernels += 2;
-    scal_read(c, c->d_scal + 3, 1);
-    c->stats.walk_steps += c->h_pin[0];
     c->stats.rounds += rounds;
     if (rounds > c->stats.max_rounds) c->stats.max_rounds = rounds;
 }

@@ -13,6 +13,7 @@ sys.path.insert(0, ".")
 from oracle import oracle  # noqa: E402
 
 INF = 1 << 40
+JACOBI = int(__import__('os').environ.get('JACOBI', '0'))
 
 
 def seed_reference(nodes, adj_lists, cap, passes=2):
@@ -96,30 +97,74 @@ def process_chunk_rounds(parts, nbr0, nbr1, sizes, cap, e, refine, stats, spec_m
         thr = np.where(pref == 0, cap - 1, np.where(pref == 1, s_l - cap, s_l // 2))
         # speculation for ties
         if xprev is None:
-            if spec_mode == "start":
-                spec = np.where(x0 - o <= s_l // 2, 0, 1)
+            if __import__('os').environ.get('HALF', '1') == '1':
+                # half-step predictor: ties count +1/2 (clamp scan in doubled coords)
+                X = np.empty(nn, np.int64); cur = 2 * x0
+                for i in range(nn):
+                    X[i] = cur; p = pref[i]
+                    if p == 3: continue
+                    if p == 0: cur = min(cur + 2 - 2 * o[i], 2 * cap)
+                    elif p == 1: cur = max(cur - 2 * o[i], 2 * (s_l[i] - cap + 1))
+                    else: cur = cur + 1 - 2 * o[i]
+                spec = np.where(X - 2 * o <= 2 * (s_l // 2), 0, 1)
             else:
                 spec = np.where(x0 - o <= s_l // 2, 0, 1)
         else:
             spec = np.where(xprev - o <= s_l // 2, 0, 1)
-        # clamp scan (sequential eval here; associative on the GPU)
-        x = np.empty(nn + 1, dtype=np.int64)
-        cur = x0
-        for i in range(nn):
-            x[i] = cur
-            p = pref[i]
-            if p == 3:
-                continue
-            if p == 0:
-                cur = min(cur - o[i] + 1, cap)
-            elif p == 1:
-                cur = max(cur - o[i], s_l[i] - cap + 1)
-            else:
-                cur = cur - o[i] + (1 if spec[i] == 0 else 0)
-        x[nn] = cur
-        # verify ties
-        bad = np.flatnonzero((pref == 2) & (((x[:nn] - o) <= thr).astype(int) != (1 - spec)))
+        for jac in range(JACOBI + 1):
+            # clamp scan (sequential eval here; associative on the GPU)
+            x = np.empty(nn + 1, dtype=np.int64)
+            cur = x0
+            for i in range(nn):
+                x[i] = cur
+                p = pref[i]
+                if p == 3:
+                    continue
+                if p == 0:
+                    cur = min(cur - o[i] + 1, cap)
+                elif p == 1:
+                    cur = max(cur - o[i], s_l[i] - cap + 1)
+                else:
+                    cur = cur - o[i] + (1 if spec[i] == 0 else 0)
+            x[nn] = cur
+            # verify ties
+            bad = np.flatnonzero((pref == 2) & (((x[:nn] - o) <= thr).astype(int) != (1 - spec)))
+            if not bad.size or jac == JACOBI:
+                break
+            stats["jacobi"] += 1
+            # segment relaxation: exact local simulation from the scanned x at
+            # each segment start -> locally consistent tie guesses
+            SEG = int(__import__('os').environ.get('SEG', '256'))
+            spec = spec.copy()
+            for st in range(0, nn, SEG):
+                xe = x[st]
+                for i in range(st, min(st + SEG, nn)):
+                    p = pref[i]
+                    if p == 3:
+                        continue
+                    b0 = (xe - o[i]) <= thr[i]
+                    if p == 2:
+                        spec[i] = 0 if b0 else 1
+                    xe = xe - o[i] + (1 if b0 else 0)
         walk = 0
+        if bad.size and __import__('os').environ.get('BUNDLE') == '1':
+            import tools.proto_bundle as pb
+            # candidate centers: this round's speculative scan, and the previous
+            # round's exact x (round 1: the half-step predictor)
+            if xprev is not None:
+                c2 = xprev
+            else:
+                Xh = np.empty(nn, np.int64); cur = 2 * x0
+                for i in range(nn):
+                    Xh[i] = cur; p = pref[i]
+                    if p == 3: continue
+                    if p == 0: cur = min(cur + 2 - 2 * o[i], 2 * cap)
+                    elif p == 1: cur = max(cur - 2 * o[i], 2 * (s_l[i] - cap + 1))
+                    else: cur = min(max(cur + 1 - 2 * o[i], 2 * (s_l[i] + 1 - cap)), 2 * cap)
+                c2 = Xh // 2
+            L = max(64, -(-nn // 4096))
+            x = pb.bundle_exact(x0, pref, o, thr, s_l, cap, x[:nn], c2, L)
+            bad = bad[:0]
         if bad.size:
             cursor = -1
             for k in bad:
@@ -200,7 +245,7 @@ if __name__ == "__main__":
     edges = synth.powerlaw_edges(n, m, beta=beta, seed=0)
     chunk = max(1, ceil(frac * m))
     cap = ceil((1.0 + slack) * n / 2)
-    stats = dict(rounds=0, max_rounds=0, visits=0, walk=0, flagged=0)
+    stats = dict(rounds=0, max_rounds=0, visits=0, walk=0, flagged=0, jacobi=0)
     t = time.time()
     mine = bisect_proto(edges, n, chunk, cap, stats=stats)
     t1 = time.time()
