@@ -98,6 +98,10 @@ grem_ctx* grem_create(int device);
 void grem_destroy(grem_ctx* ctx);
 const char* grem_last_error(void);
 int grem_get_stats(grem_ctx* ctx, grem_stats* out);
+/* Per-phase device time (CUDA events on the context stream) of the last call,
+ * when profiling is on.  Returns the number of phases; fills up to `cap`. */
+int grem_set_profiling(grem_ctx* ctx, int on);
+int grem_get_phase_times(grem_ctx* ctx, double* ms_out, int64_t* count_out, int cap, const char** names_out);
 
 /* --------------------------------------------------------------- the path */
 

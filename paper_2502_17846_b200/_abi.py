@@ -51,7 +51,8 @@ class GremStatsC(ctypes.Structure):
 
 # every exported symbol of include/grem_b200.h (tests check they all resolve)
 EXPORTS = [
-    "grem_create", "grem_destroy", "grem_last_error", "grem_get_stats",
+    "grem_create", "grem_destroy", "grem_last_error", "grem_get_stats", "grem_set_profiling",
+    "grem_get_phase_times",
     "grem_bisect_u32", "grem_partition_u32", "grem_count_cuts_u32",
     "grem_bisect_file", "grem_partition_file", "grem_state_parts",
     "grem_device_alloc", "grem_device_free", "grem_memcpy_h2d", "grem_memcpy_d2h",
@@ -89,6 +90,8 @@ def _declare(L):
     L.grem_last_error.argtypes = []
     L.grem_last_error.restype = ctypes.c_char_p
     L.grem_get_stats.argtypes = [c_vp, P(GremStatsC)]
+    L.grem_set_profiling.argtypes = [c_vp, c_int]
+    L.grem_get_phase_times.argtypes = [c_vp, c_vp, c_vp, c_int, c_vp]
     L.grem_bisect_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, P(GremConfigC), c_i64,
                                   P(GremHooksC), c_vp, P(GremReportC)]
     L.grem_partition_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, c_i64, P(GremConfigC),

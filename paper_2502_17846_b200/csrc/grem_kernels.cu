@@ -520,9 +520,44 @@ struct HalfMapSrc {   // half-step predictor: ties count +1/2 (doubled coordinat
 
 __global__ void k_double_x0(const long long* sizes, long long* out) { *out = 2 * sizes[0]; }
 
+// gated variants: skip all work when the speculative scan was already exact
+template <class Src>
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce_gated(Src src, int64_t N, Clamp* tile_agg,
+                                                                     const long long* gate) {
+    if (*gate == 0) return;
+    __shared__ Clamp smem[kScanThreads / 32];
+    int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    Clamp acc = clamp_identity();
+    for (int j = 0; j < kScanItems; ++j) {
+        int64_t i = base + j;
+        if (i < N) acc = clamp_then(acc, src.get(i).f);
+    }
+    __shared__ Clamp stotal;
+    block_excl_scan<kScanThreads>(acc, smem, &stotal);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_agg[blockIdx.x] = stotal;
+}
+__global__ void __launch_bounds__(1024) k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p,
+                                                         long long* tile_x, const long long* gate) {
+    if (*gate == 0) return;
+    __shared__ Clamp smem[32];
+    int64_t per = (ntiles + 1023) / 1024;
+    int64_t lo = (int64_t)threadIdx.x * per;
+    int64_t hi = lo + per < ntiles ? lo + per : ntiles;
+    Clamp acc = clamp_identity();
+    for (int64_t t = lo; t < hi; ++t) acc = clamp_then(acc, tile_agg[t]);
+    Clamp pre = block_excl_scan<1024>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, *x0p);
+    for (int64_t t = lo; t < hi; ++t) {
+        tile_x[t] = x;
+        x = clamp_apply(tile_agg[t], x);
+    }
+}
+
 template <class Src>
 __global__ void __launch_bounds__(kScanThreads) k_scan_down_half(Src src, int64_t N, const long long* tile_x,
-                                                                 int32_t* xo) {
+                                                                 int32_t* xo, const long long* gate) {
+    if (*gate == 0) return;
     __shared__ Clamp smem[kScanThreads / 32];
     int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
     Clamp acc = clamp_identity();
@@ -544,9 +579,9 @@ void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_
     HalfMapSrc src{b.meta, b.newb, cap};
     int64_t ntiles = (nc + kScanTile - 1) / kScanTile;
     k_double_x0<<<1, 1, 0, s>>>(b.sizes, b.scal + 5);
-    k_scan_reduce<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_agg);
-    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.scal + 5, b.tile_x);
-    k_scan_down_half<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, xalt);
+    k_scan_reduce_gated<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_agg, b.scal + 4);
+    k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.scal + 5, b.tile_x, b.scal + 4);
+    k_scan_down_half<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, xalt, b.scal + 4);
 }
 
 // per node: threshold t and lift o packed for the bundle loops (o = 2: inactive)
@@ -562,8 +597,9 @@ __device__ __forceinline__ void bundle_params(uint8_t m, int32_t nb, long long c
     o = (int8_t)nm.o;
 }
 
-constexpr int kBundle = 128;        // trajectories per segment (2 windows x 64)
-constexpr int kBundleHalf = 64;
+constexpr int kBundleWin = 64;      // trajectories per window
+constexpr int kBundleNWin = 3;      // windows: speculative x, second predictor, balance point
+constexpr int kBundle = kBundleWin * kBundleNWin;
 constexpr int kBundleBatch = 2048;  // nodes staged in shared memory at a time
 
 __global__ void __launch_bounds__(kBundle) k_bundle_sim(const uint8_t* __restrict__ meta,
@@ -578,8 +614,9 @@ __global__ void __launch_bounds__(kBundle) k_bundle_sim(const uint8_t* __restric
     int64_t lo = (int64_t)blockIdx.x * L;
     int64_t hi = lo + L < nc ? lo + L : nc;
     int tid = threadIdx.x;
-    long long c = tid < kBundleHalf ? xspec[lo] : xalt[lo];
-    long long x = c + (tid & (kBundleHalf - 1)) - kBundleHalf / 2;
+    int win = tid / kBundleWin;
+    long long c = win == 0 ? xspec[lo] : (win == 1 ? xalt[lo] : ((long long)newb[lo] + 1) / 2);
+    long long x = c + (tid % kBundleWin) - kBundleWin / 2;
     for (int64_t b = lo; b < hi; b += kBundleBatch) {
         int cnt = (int)(hi - b < kBundleBatch ? hi - b : kBundleBatch);
         __syncthreads();
@@ -596,7 +633,19 @@ __global__ void __launch_bounds__(kBundle) k_bundle_sim(const uint8_t* __restric
     ends[blockIdx.x * (int64_t)kBundle + tid] = (int32_t)x;
 }
 
-// single warp: exact chain over segments
+// single warp: exact chain over segments.  Segment tables are staged into
+// shared memory with cp.async, double buffered, so the dependent lookups of
+// the chain overlap the loads of the next batch.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+constexpr int kChainSB = 16;   // segments per staged batch
+
 __global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__ meta,
                                                      const int32_t* __restrict__ newb,
                                                      const int32_t* __restrict__ xspec,
@@ -606,29 +655,45 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__
                                                      const long long* nbad, long long* misses) {
     if (*nbad == 0) return;
     const int lane = threadIdx.x;
-    constexpr int SB = 16;   // segments staged per batch
-    __shared__ int32_t tab[SB][kBundle];
-    __shared__ int32_t cen[SB][2];
+    __shared__ __align__(16) int32_t tab[2][kChainSB * kBundle];
+    __shared__ int32_t cen[2][kChainSB][kBundleNWin];
+    auto stage = [&](int buf, int64_t s0) {
+        int cnt = (int)(nseg - s0 < kChainSB ? nseg - s0 : kChainSB);
+        const int32_t* src = ends + s0 * kBundle;
+        int n16 = cnt * kBundle / 4;   // kBundle is a multiple of 4
+        for (int k = lane; k < n16; k += 32) cp_async16(&tab[buf][k * 4], src + k * 4);
+        if (lane < cnt) {
+            int64_t lo = (s0 + lane) * L;
+            cen[buf][lane][0] = xspec[lo];
+            cen[buf][lane][1] = xalt[lo];
+            cen[buf][lane][2] = (int32_t)(((long long)newb[lo] + 1) / 2);
+        }
+        cp_async_commit();
+    };
     long long cur = sizes[0];
     long long nmiss = 0;
-    for (int64_t s0 = 0; s0 < nseg; s0 += SB) {
-        int cnt = (int)(nseg - s0 < SB ? nseg - s0 : SB);
-        __syncwarp();
-        for (int k = lane; k < cnt * kBundle; k += 32) tab[k / kBundle][k % kBundle] = ends[s0 * kBundle + k];
-        if (lane < cnt) {
-            cen[lane][0] = xspec[(s0 + lane) * L];
-            cen[lane][1] = xalt[(s0 + lane) * L];
+    stage(0, 0);
+    int buf = 0;
+    for (int64_t s0 = 0; s0 < nseg; s0 += kChainSB, buf ^= 1) {
+        int cnt = (int)(nseg - s0 < kChainSB ? nseg - s0 : kChainSB);
+        if (s0 + kChainSB < nseg) {
+            stage(buf ^ 1, s0 + kChainSB);
+            cp_async_wait1();
+        } else {
+            cp_async_wait0();
         }
         __syncwarp();
         for (int j = 0; j < cnt; ++j) {
             int64_t seg = s0 + j;
             if (lane == 0) xin[seg] = (int32_t)cur;
-            long long d1 = cur - cen[j][0] + kBundleHalf / 2;
-            long long d2 = cur - cen[j][1] + kBundleHalf / 2;
-            if (d1 >= 0 && d1 < kBundleHalf) {
-                cur = tab[j][d1];
-            } else if (d2 >= 0 && d2 < kBundleHalf) {
-                cur = tab[j][kBundleHalf + d2];
+            int hit = -1;
+#pragma unroll
+            for (int w = 0; w < kBundleNWin; ++w) {
+                long long d = cur - cen[buf][j][w] + kBundleWin / 2;
+                if (hit < 0 && d >= 0 && d < kBundleWin) hit = w * kBundleWin + (int)d;
+            }
+            if (hit >= 0) {
+                cur = tab[buf][j * kBundle + hit];
             } else {   // window miss: simulate the segment (lanes prefetch 32 nodes)
                 nmiss++;
                 int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
@@ -649,6 +714,7 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__
                 }
             }
         }
+        __syncwarp();
     }
     if (lane == 0) atomicAdd((unsigned long long*)misses, (unsigned long long)nmiss);
 }
@@ -676,7 +742,7 @@ __global__ void k_bundle_final(const uint8_t* __restrict__ meta, const int32_t* 
 }
 
 int64_t bundle_segment_len(int64_t nc) {
-    int64_t L = (nc + 4095) / 4096;
+    int64_t L = (nc + 1023) / 1024;   // <= 1024 segments: the exact chain stays short
     return L < 64 ? 64 : L;
 }
 

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -72,8 +73,24 @@ struct DBuf {
 
 }  // namespace
 
+// Phase profiler: CUDA events around launch groups on the context stream
+// (enabled per call by grem_set_profiling); elapsed times are folded in after
+// the call's final synchronisation.
+enum Phase {
+    PH_COUNT = 0, PH_SELECT, PH_NODE, PH_PREFS, PH_SCAN, PH_BUNDLE, PH_DECIDE, PH_COMMIT,
+    PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_N
+};
+static const char* kPhaseNames[PH_N] = {"count", "select", "node_init", "prefs", "scan", "bundle", "decide",
+                                        "commit", "seed", "fill", "extract", "count_cuts", "ingest"};
+
 struct grem_ctx {
     int device = 0;
+    int profiling = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_open;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    double phase_ms[PH_N] = {0};
+    long long phase_n[PH_N] = {0};
     cudaStream_t s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // per node
@@ -131,6 +148,46 @@ void scal_write(grem_ctx* c, long long* ddst, const long long* vals, int count) 
 
 void ensure_temp(grem_ctx* c, size_t bytes) { c->temp.ensure(bytes); }
 
+cudaEvent_t prof_event(grem_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+struct PhaseScope {
+    grem_ctx* c;
+    int ph;
+    cudaEvent_t a = nullptr, b = nullptr;
+    PhaseScope(grem_ctx* c_, int ph_) : c(c_), ph(ph_) {
+        if (c->profiling) {
+            a = prof_event(c);
+            b = prof_event(c);
+            cudaEventRecord(a, c->s);
+        }
+    }
+    ~PhaseScope() {
+        if (c->profiling) {
+            cudaEventRecord(b, c->s);
+            c->prof_open.push_back({ph, {a, b}});
+        }
+    }
+};
+
+void prof_collect(grem_ctx* c) {
+    for (auto& p : c->prof_open) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+            c->phase_ms[p.first] += ms;
+            c->phase_n[p.first] += 1;
+        }
+    }
+    c->prof_open.clear();
+    c->ev_used = 0;
+}
+
 void ensure_nodes(grem_ctx* c, int64_t n) {
     c->lab.ensure(n);
     c->tl.ensure(n);
@@ -153,7 +210,7 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->x.ensure(nc_cap + 1);
     c->xalt.ensure(nc_cap + 1);
     int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
-    c->bends.ensure(nseg * 128);
+    c->bends.ensure(nseg * 192);
     c->bxin.ensure(nseg);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
     c->tile_agg.ensure(tiles);
@@ -399,51 +456,66 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     cudaStream_t s = c->s;
     ChunkBufs b = chunk_bufs(c);
     CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, s));
-    launch_count_init(e, mc, b, s);
-    launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
+    { PhaseScope ps(c, PH_COUNT); launch_count_init(e, mc, b, s); }
+    { PhaseScope ps(c, PH_SELECT); launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s); }
     c->kernels += 2;
     scal_read(c, c->d_scal, 1);
     int64_t nc = c->h_pin[0];
     c->stats.visits += nc;
-    launch_node_init(b, nc, a.refine, s);
-    exclusive_sum_i32(c->x.p, c->newb.p, nc, c->temp.p, c->temp.cap, s);
-    launch_add_base(c->newb.p, nc, c->d_sizes, s);
+    {
+        PhaseScope ps(c, PH_NODE);
+        launch_node_init(b, nc, a.refine, s);
+        exclusive_sum_i32(c->x.p, c->newb.p, nc, c->temp.p, c->temp.cap, s);
+        launch_add_base(c->newb.p, nc, c->d_sizes, s);
+    }
     c->kernels += 3;
     int64_t rounds = 0;
     for (int r = 1;; ++r) {
         rounds++;
         if (r > 1) {
+            PhaseScope ps(c, PH_COUNT);
             launch_count_delta(e, mc, b, s);
             c->kernels++;
         }
-        launch_prefs(b, nc, r == 1, s);
+        { PhaseScope ps(c, PH_PREFS); launch_prefs(b, nc, r == 1, s); }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
-        launch_chunk_scan(b, nc, a.cap, s);
-        c->kernels += 4;
-        scal_read(c, c->d_scal + 4, 1);
-        if (c->h_pin[0] > 0) {
-            // speculation failed somewhere: exact repair by trajectory bundles;
-            // second window centre = previous round's exact x (round 1: the
-            // half-step predictor)
+        { PhaseScope ps(c, PH_SCAN); launch_chunk_scan(b, nc, a.cap, s); }
+        {
+            // exact repair by trajectory bundles, gated on the device by the
+            // number of mis-speculated ties (no host round trip); second window
+            // centre = previous round's exact x (round 1: the half-step predictor)
+            PhaseScope ps(c, PH_BUNDLE);
             if (r == 1) {
                 launch_half_predictor(b, nc, a.cap, c->xalt.p, s);
                 c->kernels += 4;
             }
             launch_bundle(b, nc, a.cap, c->xalt.p, c->bends.p, c->bxin.p, s);
-            c->kernels += 3;
-            c->stats.walk_steps += nc;
+            c->kernels += 7;
         }
-        launch_decide(b, nc, a.cap, s);
-        CK(cudaMemcpyAsync(c->xalt.p, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, s));
+        if (getenv("GREM_DEBUG_BUNDLE")) {
+            scal_read(c, c->d_scal + 3, 2);
+            fprintf(stderr, "[bundle] round %d nc %lld nbad %lld misses(cum) %lld\n", r, (long long)nc, c->h_pin[1],
+                    c->h_pin[0]);
+        }
+        {
+            PhaseScope ps(c, PH_DECIDE);
+            launch_decide(b, nc, a.cap, s);
+            CK(cudaMemcpyAsync(c->xalt.p, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, s));
+        }
         c->kernels += 1;
         scal_read(c, c->d_scal + 1, 1);
         if (c->h_pin[0] == 0) break;
         if (r > nc + 2) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
     }
-    launch_commit(b, nc, s);
-    launch_sizes_update(b, nc, s);
+    {
+        PhaseScope ps(c, PH_COMMIT);
+        launch_commit(b, nc, s);
+        launch_sizes_update(b, nc, s);
+    }
     c->kernels += 2;
+    scal_read(c, c->d_scal + 3, 1);
+    c->stats.walk_steps += c->h_pin[0];   // bundle window misses (sequential segment replays)
     c->stats.rounds += rounds;
     if (rounds > c->stats.max_rounds) c->stats.max_rounds = rounds;
 }
@@ -469,6 +541,30 @@ struct Meter {
 // bisect (grem.py:192-224) on device-resident edges; leaves labels in c->lab
 void bisect_core(grem_ctx* c, const BisectArgs& a) {
     cudaStream_t s = c->s;
+    static const char* dbg_levels = getenv("GREM_DEBUG_LEVELS");
+    cudaEvent_t lv0 = nullptr, lv1 = nullptr;
+    int64_t r0 = c->stats.rounds, v0 = c->stats.visits, b0 = c->stats.walk_steps;
+    if (dbg_levels) {
+        cudaEventCreate(&lv0);
+        cudaEventCreate(&lv1);
+        cudaEventRecord(lv0, s);
+    }
+    struct LevelLog {
+        grem_ctx* c; cudaEvent_t a, b; const BisectArgs& args; int64_t r0, v0, b0;
+        ~LevelLog() {
+            if (!a) return;
+            cudaEventRecord(b, c->s);
+            cudaEventSynchronize(b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            fprintf(stderr, "[level] n %lld m %lld cap %lld chunk %lld: %.2f ms rounds %lld visits %lld misses %lld\n",
+                    (long long)args.n, (long long)args.m, args.cap, (long long)args.chunk, ms,
+                    (long long)(c->stats.rounds - r0), (long long)(c->stats.visits - v0),
+                    (long long)(c->stats.walk_steps - b0));
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } level_log{c, lv0, lv1, a, r0, v0, b0};
     if (a.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
     if (2 * a.cap < a.n)
         fail(GREM_E_CAPACITY, "capacity " + std::to_string(a.cap) + " cannot hold " + std::to_string(a.n) +
@@ -492,8 +588,12 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
             int64_t mc = a.m - lo < a.chunk ? a.m - lo : a.chunk;
             meter.on_chunk(mc);
             const uint2* e = a.e + lo;
-            if (pass == 0 && ci == 0) seed_chunk(c, a, e, mc);
-            else process_chunk(c, a, e, mc);
+            if (pass == 0 && ci == 0) {
+                PhaseScope ps(c, PH_SEED);
+                seed_chunk(c, a, e, mc);
+            } else {
+                process_chunk(c, a, e, mc);
+            }
             c->stats.chunks++;
             if (a.hooks && a.hooks->on_chunk) {
                 scal_read(c, c->d_sizes, 2);
@@ -508,6 +608,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
         meter.end();
     }
     // _fill_unassigned (grem.py:177-189)
+    PhaseScope ps(c, PH_FILL);
     launch_fill_unassigned(c->lab.p, a.n, c->d_sizes, c->scratch.p, c->temp.p, c->temp.cap, s);
     c->kernels += 3;
 }
@@ -540,7 +641,7 @@ void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, 
     int* d_max = (int*)(d + 1);
     int* d_neg = d_max + 1;
     CK(cudaMemsetAsync(d_max, 0xFF, sizeof(int), s));   // -1
-    launch_count_cuts(e, m, lab, n, d, d + 2, cap, d_max, d_neg, s);
+    { PhaseScope ps(c, PH_CUTS); launch_count_cuts(e, m, lab, n, d, d + 2, cap, d_max, d_neg, s); }
     c->kernels += 2;
     std::vector<unsigned long long> h(cap + 2);
     CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * (cap + 2), cudaMemcpyDeviceToHost, s));
@@ -734,6 +835,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
     ensure_temp(c, extract_temp_bytes(m > 0 ? m : 1));
     for (int side = 0; side < 2; ++side) {
+        PhaseScope ps(c, PH_EXTRACT);
         int32_t* flags = c->scratch.p;
         launch_side_flags(c->lab.p, n, side, flags, s);
         exclusive_sum_i32(flags, c->newid.p, n, c->temp.p, c->temp.cap, s);
@@ -803,6 +905,12 @@ int guarded(grem_ctx* c, F f) {
             CK(cudaSetDevice(c->device));
             memset(&c->stats, 0, sizeof(c->stats));
             c->kernels = 0;
+            for (int k = 0; k < PH_N; ++k) {
+                c->phase_ms[k] = 0;
+                c->phase_n[k] = 0;
+            }
+            c->prof_open.clear();
+            c->ev_used = 0;
             CK(cudaEventRecord(c->ev0, c->s));
         }
         f();
@@ -813,6 +921,7 @@ int guarded(grem_ctx* c, F f) {
             cudaEventElapsedTime(&ms, c->ev0, c->ev1);
             c->stats.ms_total = ms;
             c->stats.kernels = c->kernels;
+            prof_collect(c);
         }
         return GREM_OK;
     } catch (const GremError& e) {
@@ -882,10 +991,28 @@ void grem_destroy(grem_ctx* c) {
     if (c->d_scal) cudaFree(c->d_scal);
     if (c->d_sscal) cudaFree(c->d_sscal);
     if (c->h_pin) cudaFreeHost(c->h_pin);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->s) cudaStreamDestroy(c->s);
     delete c;
+}
+
+int grem_set_profiling(grem_ctx* c, int on) {
+    if (!c) return GREM_E_FORMAT;
+    c->profiling = on ? 1 : 0;
+    return GREM_OK;
+}
+
+int grem_get_phase_times(grem_ctx* c, double* ms_out, int64_t* count_out, int cap, const char** names_out) {
+    if (!c) return GREM_E_FORMAT;
+    int n = cap < PH_N ? cap : PH_N;
+    for (int k = 0; k < n; ++k) {
+        if (ms_out) ms_out[k] = c->phase_ms[k];
+        if (count_out) count_out[k] = c->phase_n[k];
+        if (names_out) names_out[k] = kPhaseNames[k];
+    }
+    return PH_N;
 }
 
 int grem_get_stats(grem_ctx* c, grem_stats* out) {
@@ -1025,7 +1152,11 @@ extern "C" int grem_debug_chunk_scan(grem_ctx* c, const uint8_t* meta, const int
         CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, c->s));
         ChunkBufs b = chunk_bufs(c);
         launch_chunk_scan(b, nc, cap, c->s);
-        if (do_walk) launch_walk(b, nc, cap, c->s);
+        if (do_walk == 1) launch_walk(b, nc, cap, c->s);
+        if (do_walk == 2) {   // production repair: half-step predictor + trajectory bundles
+            launch_half_predictor(b, nc, cap, c->xalt.p, c->s);
+            launch_bundle(b, nc, cap, c->xalt.p, c->bends.p, c->bxin.p, c->s);
+        }
         CK(cudaMemcpyAsync(x_out, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost, c->s));
         CK(cudaMemcpyAsync(bad_out, c->bad.p, nc, cudaMemcpyDeviceToHost, c->s));
         scal_read(c, c->d_scal + 3, 2);

@@ -290,6 +290,36 @@ def partition_edges(edges, num_nodes: int, p: int, config, on_device_ptr: int | 
     return labels, _report(n, rep, sizes)
 
 
+def set_profiling(on: bool = True) -> None:
+    """Per-phase CUDA-event timing of subsequent calls (see phase_times())."""
+    _abi.lib().grem_set_profiling(context(), 1 if on else 0)
+
+
+def phase_times() -> dict:
+    """{phase: (ms, launch groups)} of the last call (profiling on)."""
+    L = _abi.lib()
+    ms = (ctypes.c_double * 32)()
+    cnt = (ctypes.c_int64 * 32)()
+    names = (ctypes.c_char_p * 32)()
+    n = L.grem_get_phase_times(context(), ms, cnt, 32, names)
+    return {names[k].decode(): (ms[k], cnt[k]) for k in range(n)}
+
+
+def count_cuts_edges(edges, num_nodes: int, labels):
+    """count_cuts on an in-memory edge array (grem.py:227-252)."""
+    n = int(num_nodes)
+    lab = np.ascontiguousarray(np.asarray(labels).astype(np.int32))
+    if lab.shape[0] != n:
+        raise FormatError(f"labels cover {lab.shape[0]} nodes, file has {n}")
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+    cap = max(2, int(lab.max()) + 1 if lab.size else 2)
+    rep, sizes = _report_struct(cap)
+    rc = _abi.lib().grem_count_cuts_u32(context(), e.ctypes.data, e.shape[0], n, 0, lab.ctypes.data, 0,
+                                        ctypes.byref(rep))
+    _raise(rc)
+    return _report(n, rep, sizes)
+
+
 def last_stats() -> dict:
     st = _abi.GremStatsC()
     _abi.lib().grem_get_stats(context(), ctypes.byref(st))

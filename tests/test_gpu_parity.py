@@ -1,0 +1,211 @@
+"""GPU parity: the CUDA path (through the C ABI, libgrem_b200.so) against the
+golden fixtures made by the real reference and against the C oracle, plus
+the reference's error behaviour, hooks and file formats.  Bar: bit-exact
+labels (integer/label work)."""
+import json
+import os
+from math import ceil
+
+import numpy as np
+import pytest
+
+from helpers import brute_force_cut, labels_sha, random_multigraph, write_grpe
+from oracle import oracle
+from paper_2502_17846_b200 import (CapacityError, FormatError, GremConfig, SeedConfig, bisect, count_cuts, grem,
+                                   partition, synth)
+from paper_2502_17846_b200.edgefile import open_edge_file
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_random_cases(golden_dir):
+    """40 multigraphs whose labels were produced by streamcut itself."""
+    g = np.load(os.path.join(golden_dir, "golden_random.npz"))
+    for c in sorted({k.split("_")[0] for k in g.files}):
+        e = g[f"{c}_edges"]
+        n, ce, refine, passes, p, rp, t, rnd = (int(v) for v in g[f"{c}_params"])
+        slack, frac = (float(v) for v in g[f"{c}_floats"])
+        seed = SeedConfig(algorithm="random" if rnd else "bfs_grow", refinement_passes=rp, rng_seed=t)
+        cfg = GremConfig(chunk_edges=ce, refine=bool(refine), passes=passes, capacity_slack=slack, seed=seed)
+        lab, rep = grem.bisect_edges(e, n, cfg)
+        assert np.array_equal(lab, g[f"{c}_bisect"]), c
+        assert rep.cut_edges == int(g[f"{c}_rep"][0])
+        cfg2 = GremConfig(chunk_frac=frac, refine=bool(refine), passes=passes, capacity_slack=slack, seed=seed)
+        lab2, rep2 = grem.partition_edges(e, n, p, cfg2)
+        assert np.array_equal(lab2, g[f"{c}_partition"]), c
+        assert rep2.cut_edges == int(g[f"{c}_rep"][1])
+
+
+@pytest.mark.parametrize("key", ["tiny_k4", "arxiv_k8"])
+def test_golden_shapes(golden_dir, key):
+    """Benchmark shapes partitioned by streamcut (labels sha256 + report)."""
+    gs = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))[key]
+    s = synth.SHAPES[gs["shape"]]
+    e = synth.shape_edges(s)
+    lab, rep = grem.partition_edges(e, s.num_nodes, gs["k"], GremConfig(chunk_frac=gs["chunk_frac"]))
+    assert labels_sha(lab) == gs["labels_sha256"]
+    assert rep.cut_edges == gs["cut_edges"] and list(rep.partition_sizes) == gs["partition_sizes"]
+    assert rep.cut_fraction == gs["cut_fraction"] and rep.balance_ratio == gs["balance_ratio"]
+    if key == "tiny_k4":
+        assert np.array_equal(lab, np.load(os.path.join(golden_dir, "golden_tiny_k4.npy")))
+
+
+def test_random_multigraphs_vs_oracle():
+    """c01-style fidelity sweep (tests/test_acceptance.py:72-96) on fresh seeds."""
+    rng = np.random.default_rng(77)
+    for trial in range(120):
+        edges, n = random_multigraph(rng, max_nodes=60, max_edges=1000)
+        ce = int(rng.integers(1, len(edges) + 1))
+        refine = bool(rng.integers(0, 2)) or trial < 60
+        passes = int(rng.integers(1, 3))
+        slack = float(rng.choice([0.0, 0.1, 0.25]))
+        cfg = GremConfig(chunk_edges=ce, refine=refine, passes=passes, capacity_slack=slack)
+        lab, rep = grem.bisect_edges(edges, n, cfg)
+        ref = oracle.bisect(edges, n, ce, ceil((1.0 + slack) * n / 2), refine, passes)
+        assert np.array_equal(lab, ref), (trial, ce, refine, passes, slack)
+        assert rep.cut_edges == brute_force_cut(edges, lab)
+
+
+@pytest.mark.parametrize("frac,slack,refine,passes,algo", [
+    (0.1, 0.0, True, 1, "bfs_grow"),
+    (0.01, 0.1, True, 1, "bfs_grow"),      # secondary sweep, unsaturated regime
+    (0.05, 0.0, False, 1, "bfs_grow"),     # fixed greedy (refine off)
+    (0.2, 0.05, True, 2, "bfs_grow"),      # re-streaming passes
+    (0.1, 0.0, True, 1, "random"),         # random seed (numpy PCG64 on the host)
+])
+def test_arxiv_variants_vs_oracle(frac, slack, refine, passes, algo):
+    s = synth.SHAPES["arxiv"]
+    e = synth.shape_edges(s)
+    seed = SeedConfig(algorithm=algo, rng_seed=11)
+    cfg = GremConfig(chunk_frac=frac, capacity_slack=slack, refine=refine, passes=passes, seed=seed)
+    lab, rep = grem.partition_edges(e, s.num_nodes, 8, cfg)
+    ref = oracle.partition(e, s.num_nodes, 8, slack=slack, chunk_frac=frac, refine=refine, passes=passes,
+                           seed_algo=algo, rng_seed=11)
+    assert np.array_equal(lab, ref)
+    cut, sizes = oracle.count_cuts(e, s.num_nodes, ref)
+    assert rep.cut_edges == cut and tuple(rep.partition_sizes) == sizes
+
+
+def test_deterministic_across_calls():
+    s = synth.SHAPES["arxiv"]
+    e = synth.shape_edges(s)
+    a, _ = grem.partition_edges(e, s.num_nodes, 4, GremConfig(chunk_frac=0.1))
+    b, _ = grem.partition_edges(e, s.num_nodes, 4, GremConfig(chunk_frac=0.1))
+    c, _ = grem.bisect_edges(e, s.num_nodes, GremConfig(chunk_frac=0.1))
+    d, _ = grem.partition_edges(e, s.num_nodes, 2, GremConfig(chunk_frac=0.1))
+    assert np.array_equal(a, b)
+    assert np.array_equal(c, d)   # p=2 == bisect (test_grem.py:329-337)
+
+
+def test_file_formats_and_dropin_api(tmp_path):
+    """GRPE u32 (native ingest), GRPE u64 and text files give identical labels
+    through the reference-shaped API; reports match count_cuts."""
+    rng = np.random.default_rng(3)
+    edges, n = random_multigraph(rng, max_nodes=300, max_edges=5000)
+    f32 = open_edge_file(write_grpe(tmp_path / "a.grpe", edges, n))
+    f64 = open_edge_file(write_grpe(tmp_path / "b.grpe", edges, n, wide=True))
+    txt = tmp_path / "c.txt"
+    txt.write_text("# comment\n" + "".join(f"{u} {v}\n" for u, v in edges.tolist()))
+    ftx = open_edge_file(str(txt), num_nodes=n)
+    cfg = GremConfig(chunk_frac=0.2)
+    outs = [bisect(f, cfg) for f in (f32, f64, ftx)]
+    for lab, rep in outs[1:]:
+        assert np.array_equal(lab, outs[0][0]) and rep == outs[0][1]
+    ref = oracle.bisect(edges, n, ceil(0.2 * len(edges)), ceil(n / 2))
+    assert np.array_equal(outs[0][0], ref)
+    labs, rep = partition(f32, 4, cfg, str(tmp_path / "work"))
+    assert rep == count_cuts(f32, labs)
+    assert os.path.isdir(tmp_path / "work")
+
+
+def test_errors_match_reference(tmp_path):
+    f = open_edge_file(write_grpe(tmp_path / "g.grpe", [[0, 1], [1, 2]], 3))
+    for bad in (0, 1, 3, 6):
+        with pytest.raises(FormatError):
+            partition(f, bad, GremConfig(chunk_frac=1.0), str(tmp_path / "w"))
+    with pytest.raises(CapacityError):
+        bisect(f, GremConfig(chunk_frac=1.0), capacity=1)
+    with pytest.raises(FormatError):
+        count_cuts(f, np.array([0, 1]))                 # length mismatch (grem.py:230-233)
+    with pytest.raises(FormatError):
+        count_cuts(f, np.array([0, -1, 1]))             # unlabeled endpoint (grem.py:238-239)
+    bad_ids = tmp_path / "bad.grpe"
+    write_grpe(bad_ids, [[0, 5]], 3)
+    with pytest.raises(FormatError):
+        bisect(open_edge_file(str(bad_ids)), GremConfig(chunk_frac=1.0))
+
+
+def test_hooks_sizes_and_meter(tmp_path):
+    """on_chunk sees sizes == recount and <= cap after every chunk (test_grem.py:161-177,
+    c11); the meter keeps <= 2 chunks resident and ends at 0 (c06)."""
+    from streamcut import ResidencyMeter
+    s = synth.SHAPES["tiny"]
+    e = synth.shape_edges(s)
+    f = open_edge_file(write_grpe(tmp_path / "t.grpe", e, s.num_nodes))
+    cap = ceil(1.05 * s.num_nodes / 2)
+    seen = []
+
+    def hook(state):
+        assert state.sizes == state.recount_sizes()
+        assert max(state.sizes) <= cap
+        seen.append(state.num_nodes)
+
+    meter = ResidencyMeter()
+    lab, _ = bisect(f, GremConfig(chunk_frac=0.01, capacity_slack=0.05), meter=meter, on_chunk=hook)
+    assert len(seen) == 100 and set(seen) == {s.num_nodes}
+    assert meter.peak <= 2 * ceil(0.01 * len(e)) and meter.current == 0
+    ref = oracle.bisect(e, s.num_nodes, ceil(0.01 * len(e)), cap)
+    assert np.array_equal(lab, ref)
+
+    def boom(state):
+        raise KeyError("hook failure propagates")
+    with pytest.raises(KeyError):
+        bisect(f, GremConfig(chunk_frac=0.1), on_chunk=boom)
+
+
+def test_edge_cases(tmp_path):
+    # empty edge file -> fill only (test_grem.py:231-237)
+    f = open_edge_file(write_grpe(tmp_path / "e.grpe", np.empty((0, 2)), 5))
+    lab, rep = bisect(f, GremConfig(chunk_frac=0.5))
+    assert sorted(np.bincount(lab, minlength=2).tolist()) == [2, 3] and rep.cut_edges == 0
+    # isolated nodes filled 5/5 (test_grem.py:224-230)
+    f = open_edge_file(write_grpe(tmp_path / "i.grpe", [[0, 1], [2, 3]], 10))
+    lab, rep = bisect(f, GremConfig(chunk_frac=1.0))
+    assert np.bincount(lab, minlength=2).tolist() == [5, 5]
+    # self-loop-only chunks, duplicates, single edge
+    for edges, n in (([[0, 0], [1, 1], [0, 0]], 3), ([[0, 1]] * 7, 2), ([[1, 0]], 2)):
+        e = np.asarray(edges)
+        for ce in (1, 2, len(e)):
+            lab, _ = grem.bisect_edges(e, n, GremConfig(chunk_edges=ce))
+            assert np.array_equal(lab, oracle.bisect(e, n, ce, ceil(n / 2)))
+    # two 16-cliques + bridge: cut 1 (test_grem.py:151-158)
+    cl = [(a, b) for base in (0, 16) for a in range(base, base + 16) for b in range(a + 1, base + 16)] + [(0, 16)]
+    perm = np.random.default_rng(5).permutation(len(cl))
+    e = np.asarray(cl)[perm]
+    lab, rep = grem.bisect_edges(e, 32, GremConfig(chunk_frac=1.0))
+    assert rep.cut_edges == 1 and sorted(rep.partition_sizes) == [16, 16]
+
+
+def test_count_cuts_vs_oracle():
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        edges, n = random_multigraph(rng, max_nodes=300, max_edges=3000)
+        lab = rng.integers(0, int(rng.integers(1, 300)), size=n)
+        from paper_2502_17846_b200.grem import count_cuts_edges
+        rep = count_cuts_edges(edges, n, lab)
+        cut, sizes = oracle.count_cuts(edges, n, lab)
+        assert rep.cut_edges == cut and tuple(rep.partition_sizes) == sizes
+
+
+def test_products_k16_golden(golden_dir):
+    """products-shaped 2.45M/61.9M, k=16: labels sha256 pinned by the reference
+    (streamcut, ~20 min on CPU) where available, else by the C oracle."""
+    shapes = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))
+    gs = shapes.get("products_k16")
+    if gs is None:
+        pytest.skip("products golden not generated")
+    s = synth.SHAPES["products"]
+    e = synth.shape_edges(s)
+    lab, rep = grem.partition_edges(e, s.num_nodes, 16, GremConfig(chunk_frac=0.1))
+    assert labels_sha(lab) == gs["labels_sha256"]
+    assert rep.cut_edges == gs["cut_edges"] and list(rep.partition_sizes) == gs["partition_sizes"]

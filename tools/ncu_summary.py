@@ -1,0 +1,23 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV: time per kernel name."""
+import csv, sys, collections
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = None
+agg = collections.defaultdict(lambda: [0, 0.0])
+for r in rows:
+    if "Kernel Name" in r:
+        hdr = r; continue
+    if hdr is None or len(r) != len(hdr):
+        continue
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    name = d["Kernel Name"].split("(")[0].split("<")[0]
+    v = float(d["Metric Value"].replace(",", ""))
+    unit = d.get("Metric Unit", "nsecond")
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1e-3)
+    agg[name][0] += 1
+    agg[name][1] += v * scale
+tot = sum(v[1] for v in agg.values())
+print(f"total kernel time {tot/1e3:.2f} ms over {sum(v[0] for v in agg.values())} launches")
+for name, (n, us) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
+    print(f"{us/1e3:9.3f} ms {100*us/tot:5.1f}% {n:6d}x  {name}")
