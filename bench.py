@@ -1,0 +1,329 @@
+"""bench.py — GREM edges/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json north_star target, fits one B200): papers100M-shaped
+synthetic power-law graph, 111,059,956 nodes / 1,615,685,872 edges
+(Chung-Lu gamma=2.1, paper_2502_17846_b200/synth.py), partitioned into k=16 by
+recursive GREM bisection with the reference defaults (chunk_frac 0.1,
+slack 0, refine, 1 pass, bfs_grow seed with 2 refinement passes).
+
+A step = one full partition(k=16) of the whole graph.  `value` is whole-job
+edges/s (original E / step time) with the edges resident in HBM; `e2e` is the
+same metric through the public API from pinned host memory (H2D of the edge
+list and D2H of the labels inside every timed step).  Device times are CUDA
+events on the library's stream (grem_stats.ms_total); max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload papers100m|friendster|products|arxiv|tiny] [--k K]
+
+N > 1: one process per GPU (torchrun); every rank partitions its own replica
+("scaling": "weak", replicas — see DESIGN.md §7 for the sharded design).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="papers100m")
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+
+    from paper_2502_17846_b200 import GremConfig, _abi, grem, synth
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_
+        dist = dist_
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    grem.set_device(local)
+    shape = synth.SHAPES[args.workload]
+    k = args.k or shape.k
+    E, n = shape.num_edges, shape.num_nodes
+    L = _abi.lib()
+    ctx = grem.context()
+    cfg = GremConfig(chunk_frac=0.1)
+
+    # edges resident in HBM (device generator == host generator, bit for bit)
+    dptr = ctypes.c_void_p()
+    assert L.grem_device_alloc(ctx, E * 8, ctypes.byref(dptr)) == 0, _abi.last_error()
+    assert L.grem_gen_edges_device(ctx, n, shape.beta, shape.seed, 0, E, dptr) == 0, _abi.last_error()
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step_device():
+        lab, rep = grem.partition_edges(None, n, k, cfg, on_device_ptr=dptr.value, num_edges=E)
+        return lab, rep, grem.last_stats()
+
+    for _ in range(args.warmup):
+        lab, rep, st = step_device()
+    ref_sha = None
+
+    grem.set_profiling(True)
+    barrier()
+    dev_ms, kernels, phases = [], 0, {}
+    sampler = ClockSampler(local)
+    t0 = time.perf_counter()
+    with sampler:
+        for _ in range(args.steps):
+            lab, rep, st = step_device()
+            dev_ms.append(st["ms_total"])
+            kernels += st["kernels"]
+            for name, (ms, cnt) in grem.phase_times().items():
+                a = phases.setdefault(name, [0.0, 0])
+                a[0] += ms
+                a[1] += cnt
+    barrier()
+    wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    grem.set_profiling(False)
+    ms_step = sum(dev_ms) / len(dev_ms)
+    if dist:
+        t = torch.tensor([ms_step], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * E / (ms_step / 1e3)
+
+    import hashlib
+    labels_sha = hashlib.sha256(np.asarray(lab, dtype="<i4").tobytes()).hexdigest()
+
+    # e2e: public API from pinned host memory, labels read back every step
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((E, 2), dtype=torch.int32, pin_memory=True)
+        assert L.grem_memcpy_d2h(ctx, ctypes.c_void_p(host.data_ptr()), dptr, E * 8) == 0
+        hv = host.numpy().view(np.uint32)
+        grem.partition_edges(hv, n, k, cfg)        # warm the host path
+        barrier()
+        e_ms = []
+        te = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 2))):
+            lab2, rep2 = grem.partition_edges(hv, n, k, cfg)
+            e_ms.append(grem.last_stats()["ms_total"])
+        barrier()
+        e_wall = (time.perf_counter() - te) * 1e3 / len(e_ms)
+        assert np.array_equal(lab2, lab), "e2e labels differ from the device-resident run"
+        e_step = max(sum(e_ms) / len(e_ms), 0.0)
+        e_step = max(e_step, e_wall)   # include host-side staging the event window may not see
+        if dist:
+            t = torch.tensor([e_step], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_step = float(t.item())
+        e2e = {"value": world * E / (e_step / 1e3), "unit": "edges/s", "ms_per_step": e_step,
+               "h2d_bytes_per_step": E * 8, "d2h_bytes_per_step": n * 4}
+        del host
+
+    # roofline of the dominant streaming kernel (edge-count pass) and of the path
+    peak, peak_kind = measured_peak()
+    cnt_ms, cnt_n = phases.get("count", (0.0, 0))
+    count_bytes = st.get("count_bytes", 0)
+    roof = None
+    if cnt_ms > 0:
+        per_step_count_bytes = count_bytes
+        achieved = per_step_count_bytes / (cnt_ms / args.steps / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_count_init/k_count_delta (edge pass)", "achieved": achieved,
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "share_of_step": cnt_ms / sum(v[0] for v in phases.values())}
+    path_bytes = st.get("path_bytes")
+    roof_path = None
+    if path_bytes:
+        ach = path_bytes / (ms_step / 1e3) / 1e9
+        roof_path = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "algorithmic_bytes_per_step": path_bytes, "formula": "SURVEY.md 8(d)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_port(shape)
+
+    if rank == 0:
+        out = {
+            "metric": "GREM edges/s (partition to k, bit-equal labels/edge-cut)", "value": value,
+            "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "wall_ms_per_step": wall_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}-shaped power-law k={k}", "num_nodes": n, "num_edges": E,
+                       "k": k, "chunk_frac": 0.1, "capacity_slack": 0.0, "refine": True, "passes": 1,
+                       "seed": "bfs_grow/2", "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (edge list %.1f GB)" % (E * 8 / 1e9)},
+            "report": {"cut_edges": rep.cut_edges, "cut_fraction": rep.cut_fraction,
+                       "balance_ratio": rep.balance_ratio, "labels_sha256": labels_sha},
+            "e2e": e2e, "roofline": roof, "roofline_path": roof_path, "cpu_baseline": cpu,
+            "gpu_launches": kernels, "clocks": sampler.summary(),
+            "phases_ms_per_step": {kk: round(v[0] / args.steps, 3) for kk, v in sorted(phases.items())},
+            "stats": {kk: st[kk] for kk in ("rounds", "visits", "bisections", "chunks")},
+        }
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline_port(shape):
+    """The C restatement (oracle/, single thread) on a bounded sample of the
+    same workload: a 1/100-scale graph of the same shape family (same
+    generator, same average degree), partitioned to the same k."""
+    from oracle import oracle
+    from paper_2502_17846_b200 import synth
+    # ~1.5-2 M edges/s single-thread: size the sample for ~10-30 s of CPU work
+    scale = max(1, shape.num_edges // 30_000_000)
+    n = max(1000, shape.num_nodes // scale)
+    m = max(10000, shape.num_edges // scale)
+    e = synth.powerlaw_edges(n, m, beta=shape.beta, seed=shape.seed)
+    t = time.perf_counter()
+    oracle.partition(e, n, shape.k, chunk_frac=0.1)
+    dt = time.perf_counter() - t
+    return {"value": m / dt, "unit": "edges/s", "cores": 1, "kind": "port",
+            "sample": f"{shape.name}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator), k={shape.k}, "
+                      f"C restatement of streamcut (oracle/grem_oracle.c, bit-exact), {dt:.1f} s"}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (streamcut,
+    pure Python, from baseline/_ref) on a bounded sample of the workload on
+    this host; falls back to the C restatement if streamcut is absent."""
+    import tempfile
+
+    import numpy as np
+
+    from paper_2502_17846_b200 import synth
+    shape = synth.SHAPES[args.workload]
+    k = args.k or shape.k
+    scale = 1000 if shape.num_edges > 100_000_000 else 10
+    n = max(1000, shape.num_nodes // scale)
+    m = max(10000, shape.num_edges // scale)
+    e = synth.powerlaw_edges(n, m, beta=shape.beta, seed=shape.seed)
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref_dir):
+        sys.path.insert(0, ref_dir)
+    try:
+        import streamcut
+        from streamcut import GremConfig, open_edge_file
+        kind = "reference"
+    except Exception:  # noqa: BLE001
+        streamcut = None
+        kind = "port"
+    tmp = tempfile.mkdtemp()
+    path = os.path.join(tmp, "g.grpe")
+    synth.write_grpe(path, e, n)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        if streamcut is not None:
+            streamcut.partition(open_edge_file(path), k, GremConfig(chunk_frac=0.1), os.path.join(tmp, "w"))
+        else:
+            from oracle import oracle
+            oracle.partition(e, n, k, chunk_frac=0.1)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t)
+    dt = sum(times) / len(times)
+    value = m / dt
+    sample = (f"{shape.name}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator), k={k}, "
+              f"{'streamcut (pure Python, single thread)' if kind == 'reference' else 'C restatement'}")
+    out = {"impl": "reference", "metric": "GREM edges/s (partition to k, bit-equal labels/edge-cut)",
+           "value": value, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u32/f64", "data": "synthetic",
+           "config": {"workload": f"{args.workload}-shaped power-law k={k}", "sample_scale": f"1/{scale}"},
+           "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": kind, "sample": sample},
+           "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

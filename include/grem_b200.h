@@ -91,6 +91,8 @@ typedef struct {
     int64_t bisections;
     int64_t kernels;         /* kernel launches issued */
     double ms_total;         /* device time of the call (CUDA events) */
+    int64_t count_bytes;     /* algorithmic bytes of the edge count passes (10 B/edge init, 9 B/edge delta) */
+    int64_t path_bytes;      /* algorithmic bytes of the whole call, SURVEY.md 8(d) formula */
 } grem_stats;
 
 /* ------------------------------------------------------------------ life */

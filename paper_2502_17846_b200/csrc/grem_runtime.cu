@@ -457,6 +457,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     ChunkBufs b = chunk_bufs(c);
     CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, s));
     { PhaseScope ps(c, PH_COUNT); launch_count_init(e, mc, b, s); }
+    c->stats.count_bytes += 10 * mc;   // 8 B edge read + 2 x 1 B label gather
     { PhaseScope ps(c, PH_SELECT); launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s); }
     c->kernels += 2;
     scal_read(c, c->d_scal, 1);
@@ -475,6 +476,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         if (r > 1) {
             PhaseScope ps(c, PH_COUNT);
             launch_count_delta(e, mc, b, s);
+            c->stats.count_bytes += 9 * mc;   // 8 B edge read + 1 B tentative-label gather
             c->kernels++;
         }
         { PhaseScope ps(c, PH_PREFS); launch_prefs(b, nc, r == 1, s); }
@@ -571,6 +573,12 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
                                   " nodes across two parts");
     if (a.chunk < 1) fail(GREM_E_FORMAT, "chunk_size must be >= 1");
     c->stats.bisections++;
+    // 8E (edge read) + 2E (label gathers) + 34 V (per visit)
+    int64_t v_before = c->stats.visits;
+    struct PathBytes {
+        grem_ctx* c; int64_t m, v0;
+        ~PathBytes() { c->stats.path_bytes += 10 * m + 34 * (c->stats.visits - v0); }
+    } path_bytes{c, a.m, v_before};
     ensure_nodes(c, a.n);
     int64_t nc_cap = a.n < 2 * a.chunk ? a.n : 2 * a.chunk;
     ensure_chunk(c, nc_cap, 0);
@@ -857,6 +865,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         e_off[side + 1] = e_off[side] + kept;
         n_off[side + 1] = n_off[side] + k;
     }
+    c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
     for (int side = 0; side < 2; ++side) {
         int64_t k = n_off[side + 1] - n_off[side];
         if (k == 0) continue;   // grem.py:308-309
@@ -884,6 +893,7 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
     try {
         recurse(c, pc, d, m, n, orig, p, 0, 0);
         count_cuts_dev(c, d, m, fin, n, rep);
+        c->stats.path_bytes += 10 * m;   // final cut pass
         if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     } catch (...) {
