@@ -216,7 +216,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down_chunk(Src src, int64
     if (mybad != kInf) atomicMin(&sbad, mybad);
     if (nb) atomicAdd((unsigned long long*)out.nbad, (unsigned long long)nb);
     __syncthreads();
-    if (threadIdx.x == 0) out.tile_bad[blockIdx.x] = sbad;
+    if (threadIdx.x == 0) {
+        out.tile_bad[blockIdx.x] = sbad;
+        if (sbad != kInf) atomicMin(out.nbad + 2, sbad);   // scal[6]: first mis-speculated tie of the chunk
+    }
 }
 
 template <class Src>
@@ -242,46 +245,183 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down_plain(Src src, int64
 
 // ------------------------------------------------------------- counting
 
+// ------------------------------------------------------------- hub table
+__device__ __forceinline__ uint32_t hub_hash(uint32_t u) { return (u * 0x9E3779B1u) >> (32 - 11); }   // 2048 slots
+
+__device__ __forceinline__ int hub_find(const uint32_t* s_keys, uint32_t u) {
+    uint32_t h = hub_hash(u);
+    while (true) {
+        uint32_t k = s_keys[h];
+        if (k == u) return (int)h;
+        if (k == kHubEmpty) return -1;
+        h = (h + 1) & (kHubSlots - 1);
+    }
+}
+
+__device__ __forceinline__ void hub_load(uint32_t* s_keys, const uint32_t* hub_keys) {
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_keys[k] = hub_keys ? hub_keys[k] : kHubEmpty;
+}
+
+// contiguous edge range of this CTA (keeps the per-CTA hub flush amortised)
+__device__ __forceinline__ void cta_range(int64_t m, int64_t& lo, int64_t& hi) {
+    int64_t per = (m + gridDim.x - 1) / gridDim.x;
+    lo = (int64_t)blockIdx.x * per;
+    hi = lo + per < m ? lo + per : m;
+}
+
+constexpr int kEdgeThreads = 512;
+
 // round 1: every chunk neighbour read with its pre-sweep label (cnt_nbrs,
 // grem.py:82-97 / 138-145); nodes whose counts stay zero get a flag so the
-// chunk node set (np.unique, model.py:59) still contains them.
-__global__ void k_count_init(const uint2* __restrict__ e, int64_t m, const int8_t* __restrict__ lab,
-                             unsigned long long* __restrict__ cnt, uint8_t* __restrict__ flag) {
-    GRID_STRIDE(i, m) {
+// chunk node set (np.unique, model.py:59) still contains them.  Hub endpoints
+// accumulate in shared memory.
+__global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __restrict__ e, int64_t m,
+                                                             const int8_t* __restrict__ lab,
+                                                             unsigned long long* __restrict__ cnt,
+                                                             uint8_t* __restrict__ flag,
+                                                             const uint32_t* __restrict__ hub_keys) {
+    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ unsigned long long s_cnt[kHubSlots];
+    __shared__ uint8_t s_flag[kHubSlots];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        s_cnt[k] = 0ULL;
+        s_flag[k] = 0;
+    }
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         uint2 ed = e[i];
         uint32_t u = ed.x, v = ed.y;
+        int hu = hub_find(s_keys, u);
         if (u == v) {   // self-loops never count (model.py:53-55) but make u a chunk node
-            flag[u] = 1;
+            if (hu >= 0) s_flag[hu] = 1;
+            else flag[u] = 1;
             continue;
         }
+        int hv = hub_find(s_keys, v);
         int lu = lab[u], lv = lab[v];
-        if (lv >= 0) atomicAdd(&cnt[u], lv == 0 ? 1ULL : (1ULL << 32));
-        else flag[u] = 1;
-        if (lu >= 0) atomicAdd(&cnt[v], lu == 0 ? 1ULL : (1ULL << 32));
-        else flag[v] = 1;
+        if (lv >= 0) {
+            unsigned long long inc = lv == 0 ? 1ULL : (1ULL << 32);
+            if (hu >= 0) atomicAdd(&s_cnt[hu], inc);
+            else atomicAdd(&cnt[u], inc);
+        } else if (hu >= 0) {
+            s_flag[hu] = 1;
+        } else {
+            flag[u] = 1;
+        }
+        if (lu >= 0) {
+            unsigned long long inc = lu == 0 ? 1ULL : (1ULL << 32);
+            if (hv >= 0) atomicAdd(&s_cnt[hv], inc);
+            else atomicAdd(&cnt[v], inc);
+        } else if (hv >= 0) {
+            s_flag[hv] = 1;
+        } else {
+            flag[v] = 1;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        uint32_t key = s_keys[k];
+        if (key == kHubEmpty) continue;
+        if (s_cnt[k]) atomicAdd(&cnt[key], s_cnt[k]);
+        if (s_flag[k]) flag[key] = 1;
     }
 }
 
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
-__global__ void k_count_delta(const uint2* __restrict__ e, int64_t m, const uint8_t* __restrict__ tl,
-                              unsigned long long* __restrict__ cnt) {
-    GRID_STRIDE(i, m) {
+__global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __restrict__ e, int64_t m,
+                                                              const uint8_t* __restrict__ tl,
+                                                              unsigned long long* __restrict__ cnt,
+                                                              const uint32_t* __restrict__ hub_keys) {
+    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ unsigned long long s_cnt[kHubSlots];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = 0ULL;
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         uint2 ed = e[i];
         uint32_t u = ed.x, v = ed.y;
         if (u == v) continue;
-        uint32_t lo = u < v ? u : v, hi = u < v ? v : u;
-        uint8_t t = tl[lo];
+        uint32_t a = u < v ? u : v, b = u < v ? v : u;
+        uint8_t t = tl[a];
         int cur = t & 0xF, prev = t >> 4;
-        if (cur != prev) atomicAdd(&cnt[hi], enc_label(cur) - enc_label(prev));
+        if (cur != prev) {
+            unsigned long long d = enc_label(cur) - enc_label(prev);
+            int hb = hub_find(s_keys, b);
+            if (hb >= 0) atomicAdd(&s_cnt[hb], d);
+            else atomicAdd(&cnt[b], d);
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        uint32_t key = s_keys[k];
+        if (key != kHubEmpty && s_cnt[k]) atomicAdd(&cnt[key], s_cnt[k]);
     }
 }
 
+static inline unsigned edge_grid(int64_t m) {
+    int64_t blocks = (m + 4 * kEdgeThreads - 1) / (4 * kEdgeThreads);
+    int64_t cap = (int64_t)num_sms() * 4;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
 void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_init<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, b.lab, b.cnt, b.flag);
+    k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, b.tl, b.cnt);
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.cnt, b.hub_keys);
+}
+
+// hub detection: endpoint histogram of a sample, candidates, top-K
+__global__ void k_sample_deg(const uint2* __restrict__ e, int64_t sample, int32_t* sdeg) {
+    GRID_STRIDE(i, sample) {
+        uint2 ed = e[i];
+        atomicAdd(&sdeg[ed.x], 1);
+        if (ed.y != ed.x) atomicAdd(&sdeg[ed.y], 1);
+    }
+}
+void launch_sample_degrees(const uint2* e, int64_t sample, int32_t* sdeg, cudaStream_t s) {
+    k_sample_deg<<<grid_for(sample, 256, 8), 256, 0, s>>>(e, sample, sdeg);
+}
+struct HubPred {
+    const int32_t* sdeg;
+    int32_t min_deg;
+    __device__ __forceinline__ bool operator()(const uint32_t& i) const { return sdeg[i] >= min_deg; }
+};
+size_t hub_select_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(nullptr, bytes, it, (uint32_t*)nullptr, (long long*)nullptr, (int)n, HubPred{nullptr, 0});
+    return bytes;
+}
+void launch_hub_select(const int32_t* sdeg, int64_t n, int32_t min_deg, uint32_t* ids, long long* d_count, void* temp,
+                       size_t temp_bytes, cudaStream_t s) {
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(temp, temp_bytes, it, ids, d_count, (int)n, HubPred{sdeg, min_deg}, s);
+}
+__global__ void k_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg, unsigned long long* keys) {
+    GRID_STRIDE(j, cnt) keys[j] = ((unsigned long long)(uint32_t)sdeg[ids[j]] << 32) | ids[j];
+}
+void launch_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg, unsigned long long* keys, cudaStream_t s) {
+    k_hub_keys<<<grid_for(cnt, 256), 256, 0, s>>>(ids, cnt, sdeg, keys);
+}
+__global__ void k_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table) {
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) table[k] = kHubEmpty;
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < nhubs; j += blockDim.x) {
+        uint32_t u = (uint32_t)(sorted_desc[j] & 0xFFFFFFFFULL);
+        uint32_t h = hub_hash(u);
+        while (atomicCAS(&table[h], kHubEmpty, u) != kHubEmpty) h = (h + 1) & (kHubSlots - 1);
+    }
+}
+void launch_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table, cudaStream_t s) {
+    k_build_hub_table<<<1, 1024, 0, s>>>(sorted_desc, nhubs, table);
 }
 
 __global__ void k_mark_all(const uint2* __restrict__ e, int64_t m, uint8_t* __restrict__ flag) {
@@ -584,53 +724,72 @@ void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_
     k_scan_down_half<HalfMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, xalt, b.scal + 4);
 }
 
-// per node: threshold t and lift o packed for the bundle loops (o = 2: inactive)
-__device__ __forceinline__ void bundle_params(uint8_t m, int32_t nb, long long cap, int32_t& t, int8_t& o) {
-    if (!meta_active(m)) {
-        t = 0;
-        o = 2;
-        return;
-    }
+// per node: threshold t and lift o packed for the bundle loops:
+// pk = t * 4 + o (arithmetic shift recovers t), o = 2 marks an inactive node.
+__device__ __forceinline__ int32_t bundle_pack(uint8_t m, int32_t nb, long long cap) {
+    if (!meta_active(m)) return 2;
     long long lift = meta_old(m) != -1 ? 1 : 0;
     NodeMap nm = node_map(m, (long long)nb - lift, cap);
-    t = (int32_t)nm.t;
-    o = (int8_t)nm.o;
+    return (int32_t)(nm.t * 4 + nm.o);
+}
+__device__ __forceinline__ long long bundle_step(long long x, int32_t pk) {
+    int o = pk & 3;
+    if (o == 2) return x;
+    long long xl = x - o;
+    return xl + (xl <= (long long)(pk >> 2) ? 1 : 0);
 }
 
 constexpr int kBundleWin = 64;      // trajectories per window
-constexpr int kBundleNWin = 3;      // windows: speculative x, second predictor, balance point
-constexpr int kBundle = kBundleWin * kBundleNWin;
+constexpr int kBundleMaxWin = 3;    // windows: speculative x, previous exact x / half-step, balance point
+constexpr int kBundleMax = kBundleWin * kBundleMaxWin;
 constexpr int kBundleBatch = 2048;  // nodes staged in shared memory at a time
+constexpr int kCkpt = 64;           // trajectory checkpoint stride (nodes)
 
-__global__ void __launch_bounds__(kBundle) k_bundle_sim(const uint8_t* __restrict__ meta,
-                                                        const int32_t* __restrict__ newb,
-                                                        const int32_t* __restrict__ xspec,
-                                                        const int32_t* __restrict__ xalt, int64_t nc, int64_t L,
-                                                        long long cap, int32_t* __restrict__ ends,
-                                                        const long long* nbad) {
+__device__ __forceinline__ int64_t bundle_seg0(const long long* first_bad, int64_t L) { return *first_bad / L; }
+
+__global__ void k_bundle_params(const uint8_t* __restrict__ meta, const int32_t* __restrict__ newb, int64_t nc,
+                                int64_t L, long long cap, int32_t* __restrict__ bp, const long long* nbad,
+                                const long long* first_bad) {
     if (*nbad == 0) return;
-    __shared__ int32_t st[kBundleBatch];
-    __shared__ int8_t so[kBundleBatch];
-    int64_t lo = (int64_t)blockIdx.x * L;
+    int64_t lo = bundle_seg0(first_bad, L) * L;   // from the start of the first repaired segment
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
+        bp[i] = bundle_pack(meta[i], newb[i], cap);
+}
+
+template <int NWIN>
+__global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t* __restrict__ bp,
+                                                                 const int32_t* __restrict__ newb,
+                                                                 const int32_t* __restrict__ xspec,
+                                                                 const int32_t* __restrict__ xalt, int64_t nc,
+                                                                 int64_t L, int32_t* __restrict__ ends,
+                                                                 int32_t* __restrict__ ckpt, const long long* nbad,
+                                                                 const long long* first_bad) {
+    constexpr int NT = kBundleWin * NWIN;
+    if (*nbad == 0) return;
+    int64_t seg = blockIdx.x;
+    if (seg < bundle_seg0(first_bad, L)) return;
+    __shared__ int32_t sp[kBundleBatch];
+    int64_t lo = seg * L;
     int64_t hi = lo + L < nc ? lo + L : nc;
     int tid = threadIdx.x;
     int win = tid / kBundleWin;
     long long c = win == 0 ? xspec[lo] : (win == 1 ? xalt[lo] : ((long long)newb[lo] + 1) / 2);
     long long x = c + (tid % kBundleWin) - kBundleWin / 2;
+    int64_t ncp = (L + kCkpt - 1) / kCkpt;
+    int32_t* ck = ckpt + seg * ncp * NT;
     for (int64_t b = lo; b < hi; b += kBundleBatch) {
         int cnt = (int)(hi - b < kBundleBatch ? hi - b : kBundleBatch);
         __syncthreads();
-        for (int k = tid; k < cnt; k += kBundle) bundle_params(meta[b + k], newb[b + k], cap, st[k], so[k]);
+        for (int k = tid; k < cnt; k += NT) sp[k] = bp[b + k];
         __syncthreads();
-        for (int k = 0; k < cnt; ++k) {
-            int o = so[k];
-            if (o != 2) {
-                long long xl = x - o;
-                x = xl + (xl <= st[k] ? 1 : 0);
-            }
+        for (int k0 = 0; k0 < cnt; k0 += kCkpt) {
+            ck[((b - lo + k0) / kCkpt) * NT + tid] = (int32_t)x;   // x before node b + k0
+            int lim = cnt - k0 < kCkpt ? cnt - k0 : kCkpt;
+#pragma unroll 8
+            for (int k = 0; k < lim; ++k) x = bundle_step(x, sp[k0 + k]);
         }
     }
-    ends[blockIdx.x * (int64_t)kBundle + tid] = (int32_t)x;
+    ends[seg * NT + tid] = (int32_t)x;
 }
 
 // single warp: exact chain over segments.  Segment tables are staged into
@@ -646,35 +805,37 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 constexpr int kChainSB = 16;   // segments per staged batch
 
-__global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__ meta,
-                                                     const int32_t* __restrict__ newb,
+template <int NWIN>
+__global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__ bp, const int32_t* __restrict__ newb,
                                                      const int32_t* __restrict__ xspec,
                                                      const int32_t* __restrict__ xalt, const int32_t* __restrict__ ends,
-                                                     int64_t nseg, int64_t nc, int64_t L, long long cap,
-                                                     const long long* sizes, int32_t* __restrict__ xin,
-                                                     const long long* nbad, long long* misses) {
+                                                     int64_t nseg, int64_t nc, int64_t L, int32_t* __restrict__ xin,
+                                                     int32_t* __restrict__ hit_out, const long long* nbad,
+                                                     const long long* first_bad, long long* misses) {
+    constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     const int lane = threadIdx.x;
-    __shared__ __align__(16) int32_t tab[2][kChainSB * kBundle];
-    __shared__ int32_t cen[2][kChainSB][kBundleNWin];
+    __shared__ __align__(16) int32_t tab[2][kChainSB * NT];
+    __shared__ int32_t cen[2][kChainSB][NWIN];
+    int64_t seg0 = bundle_seg0(first_bad, L);
     auto stage = [&](int buf, int64_t s0) {
         int cnt = (int)(nseg - s0 < kChainSB ? nseg - s0 : kChainSB);
-        const int32_t* src = ends + s0 * kBundle;
-        int n16 = cnt * kBundle / 4;   // kBundle is a multiple of 4
+        const int32_t* src = ends + s0 * NT;
+        int n16 = cnt * NT / 4;
         for (int k = lane; k < n16; k += 32) cp_async16(&tab[buf][k * 4], src + k * 4);
         if (lane < cnt) {
             int64_t lo = (s0 + lane) * L;
             cen[buf][lane][0] = xspec[lo];
-            cen[buf][lane][1] = xalt[lo];
-            cen[buf][lane][2] = (int32_t)(((long long)newb[lo] + 1) / 2);
+            if (NWIN > 1) cen[buf][lane][1] = xalt[lo];
+            if (NWIN > 2) cen[buf][lane][NWIN > 2 ? 2 : 0] = (int32_t)(((long long)newb[lo] + 1) / 2);
         }
         cp_async_commit();
     };
-    long long cur = sizes[0];
+    long long cur = xspec[seg0 * L];   // exact: every tie before first_bad was consistent
     long long nmiss = 0;
-    stage(0, 0);
+    stage(0, seg0);
     int buf = 0;
-    for (int64_t s0 = 0; s0 < nseg; s0 += kChainSB, buf ^= 1) {
+    for (int64_t s0 = seg0; s0 < nseg; s0 += kChainSB, buf ^= 1) {
         int cnt = (int)(nseg - s0 < kChainSB ? nseg - s0 : kChainSB);
         if (s0 + kChainSB < nseg) {
             stage(buf ^ 1, s0 + kChainSB);
@@ -685,32 +846,26 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__
         __syncwarp();
         for (int j = 0; j < cnt; ++j) {
             int64_t seg = s0 + j;
-            if (lane == 0) xin[seg] = (int32_t)cur;
             int hit = -1;
 #pragma unroll
-            for (int w = 0; w < kBundleNWin; ++w) {
+            for (int w = 0; w < NWIN; ++w) {
                 long long d = cur - cen[buf][j][w] + kBundleWin / 2;
                 if (hit < 0 && d >= 0 && d < kBundleWin) hit = w * kBundleWin + (int)d;
             }
+            if (lane == 0) {
+                xin[seg] = (int32_t)cur;
+                hit_out[seg] = hit;
+            }
             if (hit >= 0) {
-                cur = tab[buf][j * kBundle + hit];
+                cur = tab[buf][j * NT + hit];
             } else {   // window miss: simulate the segment (lanes prefetch 32 nodes)
                 nmiss++;
                 int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
                 for (int64_t b = lo; b < hi; b += 32) {
                     int64_t idx = b + lane;
-                    int32_t t = 0;
-                    int8_t o = 2;
-                    if (idx < hi) bundle_params(meta[idx], newb[idx], cap, t, o);
+                    int32_t pk = idx < hi ? bp[idx] : 2;
                     int lim = (int)(hi - b < 32 ? hi - b : 32);
-                    for (int k = 0; k < lim; ++k) {
-                        int ok = __shfl_sync(0xffffffffu, (int)o, k);
-                        int tk = __shfl_sync(0xffffffffu, t, k);
-                        if (ok != 2) {
-                            long long xl = cur - ok;
-                            cur = xl + (xl <= tk ? 1 : 0);
-                        }
-                    }
+                    for (int k = 0; k < lim; ++k) cur = bundle_step(cur, __shfl_sync(0xffffffffu, pk, k));
                 }
             }
         }
@@ -719,42 +874,76 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const uint8_t* __restrict__
     if (lane == 0) atomicAdd((unsigned long long*)misses, (unsigned long long)nmiss);
 }
 
-// every segment replays its exact trajectory: x before each node
-__global__ void k_bundle_final(const uint8_t* __restrict__ meta, const int32_t* __restrict__ newb,
-                               const int32_t* __restrict__ xin, int64_t nseg, int64_t nc, int64_t L, long long cap,
-                               int32_t* __restrict__ x, const long long* nbad) {
+// parallel replay of the exact trajectory: one thread per checkpoint interval
+template <int NWIN>
+__global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __restrict__ xin,
+                               const int32_t* __restrict__ hit, const int32_t* __restrict__ ckpt, int64_t nseg,
+                               int64_t nc, int64_t L, int32_t* __restrict__ x, const long long* nbad,
+                               const long long* first_bad) {
+    constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
-    int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (seg >= nseg) return;
-    int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
-    long long cur = xin[seg];
-    for (int64_t i = lo; i < hi; ++i) {
-        x[i] = (int32_t)cur;
-        int32_t t;
-        int8_t o;
-        bundle_params(meta[i], newb[i], cap, t, o);
-        if (o != 2) {
-            long long xl = cur - o;
-            cur = xl + (xl <= t ? 1 : 0);
+    int64_t ncp = (L + kCkpt - 1) / kCkpt;
+    int64_t seg0 = bundle_seg0(first_bad, L);
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nseg * ncp;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        int64_t seg = w / ncp, cp = w % ncp;
+        if (seg < seg0) continue;
+        int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
+        int h = hit[seg];
+        long long cur;
+        int64_t a, e;
+        if (h >= 0) {
+            a = lo + cp * kCkpt;
+            if (a >= hi) continue;
+            e = a + kCkpt < hi ? a + kCkpt : hi;
+            cur = ckpt[(seg * ncp + cp) * NT + h];
+        } else {   // window miss: one thread replays the segment
+            if (cp) continue;
+            a = lo;
+            e = hi;
+            cur = xin[seg];
         }
+        for (int64_t i = a; i < e; ++i) {
+            x[i] = (int32_t)cur;
+            cur = bundle_step(cur, bp[i]);
+        }
+        if (e == nc) x[nc] = (int32_t)cur;
     }
-    if (hi == nc) x[nc] = (int32_t)cur;
 }
 
 int64_t bundle_segment_len(int64_t nc) {
-    int64_t L = (nc + 1023) / 1024;   // <= 1024 segments: the exact chain stays short
-    return L < 64 ? 64 : L;
+    int64_t L = (nc + 4095) / 4096;   // <= 4096 segments
+    if (L < kCkpt) L = kCkpt;
+    return (L + kCkpt - 1) / kCkpt * kCkpt;
+}
+int64_t bundle_ckpt_ints(int64_t nc) {
+    int64_t L = bundle_segment_len(nc);
+    int64_t nseg = (nc + L - 1) / L;
+    return nseg * ((L + kCkpt - 1) / kCkpt) * kBundleMax;
 }
 
-void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, int32_t* ends, int32_t* xin,
+void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, const BundleBufs& bb, int nwin,
                    cudaStream_t s) {
     int64_t L = bundle_segment_len(nc);
     int64_t nseg = (nc + L - 1) / L;
-    k_bundle_sim<<<(unsigned)nseg, kBundle, 0, s>>>(b.meta, b.newb, b.x, xalt, nc, L, cap, ends, b.scal + 4);
-    k_bundle_chain<<<1, 32, 0, s>>>(b.meta, b.newb, b.x, xalt, ends, nseg, nc, L, cap, b.sizes, xin, b.scal + 4,
-                                    b.scal + 3);
-    k_bundle_final<<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(b.meta, b.newb, xin, nseg, nc, L, cap, b.x,
-                                                                 b.scal + 4);
+    int64_t ncp = (L + kCkpt - 1) / kCkpt;
+    const long long* nbad = b.scal + 4;
+    const long long* first_bad = b.scal + 6;
+    k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
+    unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
+    if (nwin == 3) {
+        k_bundle_sim<3><<<(unsigned)nseg, kBundleWin * 3, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
+                                                                 nbad, first_bad);
+        k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
+                                           first_bad, b.scal + 3);
+        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad);
+    } else {
+        k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
+                                                                 nbad, first_bad);
+        k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
+                                           first_bad, b.scal + 3);
+        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad);
+    }
 }
 
 __global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
@@ -828,36 +1017,81 @@ void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStrea
     k_set_rank<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, rank);
 }
 
-__global__ void k_degrees(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ rank,
-                          int32_t* __restrict__ deg) {
-    GRID_STRIDE(i, m) {
+__global__ void __launch_bounds__(kEdgeThreads) k_degrees(const uint2* __restrict__ e, int64_t m,
+                                                          const int32_t* __restrict__ rank, int32_t* __restrict__ deg,
+                                                          const uint32_t* __restrict__ hub_keys) {
+    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ uint32_t s_deg[kHubSlots];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_deg[k] = 0;
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         uint2 ed = e[i];
         if (ed.x == ed.y) continue;
-        atomicAdd(&deg[rank[ed.x]], 1);
-        atomicAdd(&deg[rank[ed.y]], 1);
+        int hu = hub_find(s_keys, ed.x), hv = hub_find(s_keys, ed.y);
+        if (hu >= 0) atomicAdd(&s_deg[hu], 1u);
+        else atomicAdd(&deg[rank[ed.x]], 1);
+        if (hv >= 0) atomicAdd(&s_deg[hv], 1u);
+        else atomicAdd(&deg[rank[ed.y]], 1);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        uint32_t key = s_keys[k];
+        if (key != kHubEmpty && s_deg[k]) atomicAdd(&deg[rank[key]], (int32_t)s_deg[k]);
     }
 }
-void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, cudaStream_t s) {
-    k_degrees<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, deg);
+void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, const uint32_t* hub_keys,
+                    cudaStream_t s) {
+    k_degrees<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, rank, deg, hub_keys);
 }
 
-__global__ void k_fill_csr(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ rank,
-                           int32_t* __restrict__ cursor, uint32_t* __restrict__ adj, uint32_t* __restrict__ row_of) {
-    GRID_STRIDE(i, m) {
+// CSR fill: hubs reserve one contiguous block per CTA (count pass over the
+// CTA's edge range, one global atomic per hub, then fill from the block).
+__global__ void __launch_bounds__(kEdgeThreads) k_fill_csr(const uint2* __restrict__ e, int64_t m,
+                                                           const int32_t* __restrict__ rank,
+                                                           int32_t* __restrict__ cursor, uint32_t* __restrict__ adj,
+                                                           uint32_t* __restrict__ row_of,
+                                                           const uint32_t* __restrict__ hub_keys) {
+    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ int32_t s_pos[kHubSlots];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_pos[k] = 0;
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    if (hub_keys) {
+        for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            uint2 ed = e[i];
+            if (ed.x == ed.y) continue;
+            int hu = hub_find(s_keys, ed.x), hv = hub_find(s_keys, ed.y);
+            if (hu >= 0) atomicAdd(&s_pos[hu], 1);
+            if (hv >= 0) atomicAdd(&s_pos[hv], 1);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+            uint32_t key = s_keys[k];
+            if (key != kHubEmpty && s_pos[k]) s_pos[k] = atomicAdd(&cursor[rank[key]], s_pos[k]);
+        }
+        __syncthreads();
+    }
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         uint2 ed = e[i];
         if (ed.x == ed.y) continue;
         int32_t a = rank[ed.x], c = rank[ed.y];
-        int32_t pa = atomicAdd(&cursor[a], 1);
+        int hu = hub_find(s_keys, ed.x), hv = hub_find(s_keys, ed.y);
+        int32_t pa = hu >= 0 ? atomicAdd(&s_pos[hu], 1) : atomicAdd(&cursor[a], 1);
         adj[pa] = (uint32_t)c;
         row_of[pa] = (uint32_t)a;
-        int32_t pc = atomicAdd(&cursor[c], 1);
+        int32_t pc = hv >= 0 ? atomicAdd(&s_pos[hv], 1) : atomicAdd(&cursor[c], 1);
         adj[pc] = (uint32_t)a;
         row_of[pc] = (uint32_t)c;
     }
 }
 void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
-                     uint32_t* row_of, cudaStream_t s) {
-    k_fill_csr<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, cursor, adj, row_of);
+                     uint32_t* row_of, const uint32_t* hub_keys, cudaStream_t s) {
+    k_fill_csr<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, rank, cursor, adj, row_of, hub_keys);
 }
 
 // union-find connected components (link larger root under smaller root)
@@ -1354,6 +1588,10 @@ size_t sort_temp_bytes(int64_t n) {
 void sort_pairs_u64_u32(const unsigned long long* kin, unsigned long long* kout, const uint32_t* vin, uint32_t* vout,
                         int64_t n, void* temp, size_t temp_bytes, cudaStream_t s) {
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kin, kout, vin, vout, (int)n, 0, 64, s);
+}
+void sort_keys_u64_desc(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp,
+                        size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceRadixSort::SortKeysDescending(temp, temp_bytes, kin, kout, (int)n, 0, 64, s);
 }
 void sort_keys_u64(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp, size_t temp_bytes,
                    cudaStream_t s) {

@@ -9,6 +9,14 @@
 
 namespace grem {
 
+// Hub privatisation (power-law hubs would serialise the counter atomics):
+// up to kMaxHubs high-degree nodes, found per bisection by sampling, live in
+// an open-addressing table (kHubSlots u32 keys, empty = kHubEmpty); edge
+// kernels accumulate their updates in shared memory and flush once per CTA.
+constexpr int kHubSlots = 2048;
+constexpr int kMaxHubs = 1024;
+constexpr uint32_t kHubEmpty = 0xFFFFFFFFu;
+
 struct ChunkBufs {
     // global per-node state (n)
     int8_t* lab;
@@ -28,7 +36,9 @@ struct ChunkBufs {
     long long* tile_bad;
     // device scalars
     long long* sizes;   // [2] live sizes (read-only during a chunk)
-    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0
+    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0,
+                        //     6 first mis-speculated tie
+    const uint32_t* hub_keys;   // kHubSlots table or nullptr (no hubs)
 };
 
 constexpr int kScanThreads = 256;
@@ -46,9 +56,17 @@ void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t
 void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 // exact repair of mis-speculated ties by trajectory bundles (replaces the walk)
+struct BundleBufs {
+    int32_t* params;   // nc packed node parameters
+    int32_t* ends;     // nseg * 192
+    int32_t* ckpt;     // bundle_ckpt_ints(nc)
+    int32_t* xin;      // nseg
+    int32_t* hit;      // nseg
+};
 int64_t bundle_segment_len(int64_t nc);
+int64_t bundle_ckpt_ints(int64_t nc);
 void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_t* xalt, cudaStream_t s);
-void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, int32_t* ends, int32_t* xin,
+void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, const BundleBufs& bb, int nwin,
                    cudaStream_t s);
 void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
@@ -91,9 +109,21 @@ struct SeedBufs {
 };
 
 void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStream_t s);
-void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, cudaStream_t s);
+void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg, const uint32_t* hub_keys,
+                    cudaStream_t s);
 void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
-                     uint32_t* row_of, cudaStream_t s);
+                     uint32_t* row_of, const uint32_t* hub_keys, cudaStream_t s);
+
+// hub detection from a sample of the level's edges
+void launch_sample_degrees(const uint2* e, int64_t sample, int32_t* sdeg, cudaStream_t s);
+void launch_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg, unsigned long long* keys,
+                     cudaStream_t s);
+void launch_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table, cudaStream_t s);
+size_t hub_select_temp_bytes(int64_t n);
+void launch_hub_select(const int32_t* sdeg, int64_t n, int32_t min_deg, uint32_t* ids, long long* d_count, void* temp,
+                       size_t temp_bytes, cudaStream_t s);
+void sort_keys_u64_desc(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp,
+                        size_t temp_bytes, cudaStream_t s);
 void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent, uint32_t* scratch, int64_t nc,
                cudaStream_t s);
 void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s);

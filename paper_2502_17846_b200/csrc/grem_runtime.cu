@@ -78,10 +78,10 @@ struct DBuf {
 // the call's final synchronisation.
 enum Phase {
     PH_COUNT = 0, PH_SELECT, PH_NODE, PH_PREFS, PH_SCAN, PH_BUNDLE, PH_DECIDE, PH_COMMIT,
-    PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_N
+    PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_HUBS, PH_N
 };
 static const char* kPhaseNames[PH_N] = {"count", "select", "node_init", "prefs", "scan", "bundle", "decide",
-                                        "commit", "seed", "fill", "extract", "count_cuts", "ingest"};
+                                        "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs"};
 
 struct grem_ctx {
     int device = 0;
@@ -102,7 +102,8 @@ struct grem_ctx {
     // per chunk node
     DBuf<uint32_t> nodes{"nodes"};
     DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
-    DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, bends{"bends"}, bxin{"bxin"};
+    DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
+        bckpt{"bckpt"};
     DBuf<Clamp> tile_agg{"tile_agg"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
     // seed
@@ -111,6 +112,10 @@ struct grem_ctx {
     DBuf<unsigned long long> ckey{"ckey"}, rkeys{"rkeys"}, rkeys2{"rkeys2"}, cand{"cand"}, cand2{"cand2"}, pair{"pair"};
     DBuf<int8_t> slab{"slab"}, slab2{"slab2"};
     DBuf<int64_t> fdeg{"fdeg"}, cum{"cum"};
+    // hubs
+    DBuf<uint32_t> hub_table{"hub_table"}, hub_ids{"hub_ids"};
+    DBuf<unsigned long long> hub_k1{"hub_k1"}, hub_k2{"hub_k2"};
+    bool hubs_on = false;
     // scalars
     long long* d_sizes = nullptr;   // [2]
     long long* d_scal = nullptr;    // [8]
@@ -212,6 +217,9 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
     c->bends.ensure(nseg * 192);
     c->bxin.ensure(nseg);
+    c->bhit.ensure(nseg);
+    c->bparams.ensure(nc_cap + 1);
+    c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
     c->tile_agg.ensure(tiles);
     c->tile_x.ensure(tiles);
@@ -264,6 +272,7 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.tile_bad = c->tile_bad.p;
     b.sizes = c->d_sizes;
     b.scal = c->d_scal;
+    b.hub_keys = c->hubs_on ? c->hub_table.p : nullptr;
     return b;
 }
 
@@ -331,7 +340,8 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     launch_set_rank(c->nodes.p, nc, c->rank.p, s);
     ensure_seed(c, nc, 0);
     CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));
-    launch_degrees(e, mc, c->rank.p, c->cursor.p, s);
+    const uint32_t* hubs = c->hubs_on ? c->hub_table.p : nullptr;
+    launch_degrees(e, mc, c->rank.p, c->cursor.p, hubs, s);
     exclusive_sum_i32(c->cursor.p, c->start.p, nc + 1, c->temp.p, c->temp.cap, s);
     c->kernels += 3;
     int32_t entries32 = 0;
@@ -342,7 +352,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     ensure_seed(c, nc, entries);
     SeedBufs sb = seed_bufs(c);
     CK(cudaMemcpyAsync(c->cursor.p, c->start.p, sizeof(int32_t) * nc, cudaMemcpyDeviceToDevice, s));
-    launch_fill_csr(e, mc, c->rank.p, c->cursor.p, c->adj.p, c->row_of.p, s);
+    launch_fill_csr(e, mc, c->rank.p, c->cursor.p, c->adj.p, c->row_of.p, hubs, s);
     c->kernels += 1;
     long long target = (nc + 1) / 2;   // ceil(n / 2), seed.py:57
 
@@ -482,18 +492,21 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         { PhaseScope ps(c, PH_PREFS); launch_prefs(b, nc, r == 1, s); }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
+        CK(cudaMemsetAsync(c->d_scal + 6, 0x7F, sizeof(long long), s));   // first bad = +large
         { PhaseScope ps(c, PH_SCAN); launch_chunk_scan(b, nc, a.cap, s); }
         {
             // exact repair by trajectory bundles, gated on the device by the
-            // number of mis-speculated ties (no host round trip); second window
-            // centre = previous round's exact x (round 1: the half-step predictor)
+            // number of mis-speculated ties (no host round trip); windows:
+            // speculative x, previous round's exact x (round 1: half-step
+            // predictor) and, in round 1, the balance point
             PhaseScope ps(c, PH_BUNDLE);
             if (r == 1) {
                 launch_half_predictor(b, nc, a.cap, c->xalt.p, s);
                 c->kernels += 4;
             }
-            launch_bundle(b, nc, a.cap, c->xalt.p, c->bends.p, c->bxin.p, s);
-            c->kernels += 7;
+            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
+            launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s);
+            c->kernels += 4;
         }
         if (getenv("GREM_DEBUG_BUNDLE")) {
             scal_read(c, c->d_scal + 3, 2);
@@ -539,6 +552,40 @@ struct Meter {
         prev = -1;
     }
 };
+
+// Hubs of this bisection: top-kMaxHubs endpoints of a 4M-edge sample of the
+// level's edge list (edges are in random order, so the sample ranks degrees);
+// only worthwhile for large chunks.  Performance only: results never depend
+// on which nodes are hubs.
+void detect_hubs(grem_ctx* c, const BisectArgs& a) {
+    c->hubs_on = false;
+    const char* env_min = getenv("GREM_HUB_MIN_CHUNK");   // tests force the hub path on small graphs
+    int64_t min_chunk = env_min ? atoll(env_min) : (1LL << 21);
+    if (a.chunk < min_chunk || a.m == 0) return;
+    cudaStream_t s = c->s;
+    PhaseScope ps(c, PH_HUBS);
+    int64_t S = a.m < (1LL << 22) ? a.m : (1LL << 22);
+    CK(cudaMemsetAsync(c->scratch.p, 0, sizeof(int32_t) * a.n, s));
+    launch_sample_degrees(a.e, S, c->scratch.p, s);
+    c->hub_ids.ensure(1 << 20);
+    ensure_temp(c, hub_select_temp_bytes(a.n));
+    const char* env_deg = getenv("GREM_HUB_MIN_DEG");
+    launch_hub_select(c->scratch.p, a.n, env_deg ? atoi(env_deg) : 16, c->hub_ids.p, c->d_sscal + 8, c->temp.p, c->temp.cap, s);
+    c->kernels += 3;
+    scal_read(c, c->d_sscal + 8, 1);
+    int64_t cnt = c->h_pin[0];
+    if (cnt <= 0) return;
+    if (cnt > (1 << 20)) cnt = 1 << 20;
+    c->hub_k1.ensure(cnt);
+    c->hub_k2.ensure(cnt);
+    c->hub_table.ensure(kHubSlots);
+    ensure_temp(c, sort_temp_bytes(cnt));
+    launch_hub_keys(c->hub_ids.p, cnt, c->scratch.p, c->hub_k1.p, s);
+    sort_keys_u64_desc(c->hub_k1.p, c->hub_k2.p, cnt, c->temp.p, c->temp.cap, s);
+    launch_build_hub_table(c->hub_k2.p, cnt < kMaxHubs ? cnt : kMaxHubs, c->hub_table.p, s);
+    c->kernels += 4;
+    c->hubs_on = true;
+}
 
 // bisect (grem.py:192-224) on device-resident edges; leaves labels in c->lab
 void bisect_core(grem_ctx* c, const BisectArgs& a) {
@@ -588,6 +635,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
     CK(cudaMemsetAsync(c->d_sizes, 0, sizeof(long long) * 2, s));
     c->live_n = a.n;
+    detect_hubs(c, a);
     int64_t num_chunks = a.m ? (a.m + a.chunk - 1) / a.chunk : 0;
     for (int pass = 0; pass < a.passes; ++pass) {
         Meter meter{a.hooks};
@@ -1160,12 +1208,14 @@ extern "C" int grem_debug_chunk_scan(grem_ctx* c, const uint8_t* meta, const int
         long long sz[2] = {x0, 0};
         scal_write(c, c->d_sizes, sz, 2);
         CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, c->s));
+        CK(cudaMemsetAsync(c->d_scal + 6, 0x7F, sizeof(long long), c->s));
         ChunkBufs b = chunk_bufs(c);
         launch_chunk_scan(b, nc, cap, c->s);
         if (do_walk == 1) launch_walk(b, nc, cap, c->s);
-        if (do_walk == 2) {   // production repair: half-step predictor + trajectory bundles
+        if (do_walk >= 2) {   // production repair: half-step predictor + trajectory bundles (2 or 3 windows)
             launch_half_predictor(b, nc, cap, c->xalt.p, c->s);
-            launch_bundle(b, nc, cap, c->xalt.p, c->bends.p, c->bxin.p, c->s);
+            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
+            launch_bundle(b, nc, cap, c->xalt.p, bb, do_walk == 2 ? 3 : 2, c->s);
         }
         CK(cudaMemcpyAsync(x_out, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost, c->s));
         CK(cudaMemcpyAsync(bad_out, c->bad.p, nc, cudaMemcpyDeviceToHost, c->s));

@@ -70,7 +70,7 @@ def test_chunk_scan_and_bundle_exact():
         nc = int(rng.choice([1, 5, 100, 4095, 4097, 20000, 150000]))
         meta, newb, x0, cap = _random_chain(rng, nc)
         ref = _seq(meta, newb, x0, cap)
-        for mode in (2, 1):   # 2: trajectory bundles (production), 1: sequential walk
+        for mode in (2, 3, 1):   # 2/3: trajectory bundles with 3/2 windows (production), 1: sequential walk
             xo = np.empty(nc + 1, np.int32)
             bo = np.empty(nc, np.uint8)
             nb = np.zeros(2, np.int64)

@@ -209,3 +209,49 @@ def test_products_k16_golden(golden_dir):
     lab, rep = grem.partition_edges(e, s.num_nodes, 16, GremConfig(chunk_frac=0.1))
     assert labels_sha(lab) == gs["labels_sha256"]
     assert rep.cut_edges == gs["cut_edges"] and list(rep.partition_sizes) == gs["partition_sizes"]
+
+
+def test_hub_privatisation_path_is_exact(golden_dir):
+    """Force the shared-memory hub path (normally only for chunks >= 2M edges)
+    on the arxiv shape and the random golden cases; labels must not change."""
+    import subprocess
+    import sys
+    code = r'''
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np
+from paper_2502_17846_b200 import GremConfig, grem, synth
+gs = json.load(open("tests/golden/golden_shapes.json"))["arxiv_k8"]
+s = synth.SHAPES["arxiv"]; e = synth.shape_edges(s)
+lab, rep = grem.partition_edges(e, s.num_nodes, 8, GremConfig(chunk_frac=0.1))
+import hashlib
+assert hashlib.sha256(lab.astype("<i4").tobytes()).hexdigest() == gs["labels_sha256"]
+print("hub path ok")
+'''
+    root = os.path.dirname(golden_dir.rstrip("/")).rsplit("/tests", 1)[0]
+    env = dict(os.environ, GREM_HUB_MIN_CHUNK="1", GREM_HUB_MIN_DEG="2")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "hub path ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_poisoned_buffers_do_not_change_results(golden_dir):
+    """GREM_DEBUG_POISON=all fills every new device buffer with 0xA5: a read of
+    memory not written in the call would change the labels."""
+    import subprocess
+    import sys
+    code = r'''
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+from paper_2502_17846_b200 import GremConfig, grem, synth
+import hashlib
+gs = json.load(open("tests/golden/golden_shapes.json"))["arxiv_k8"]
+s = synth.SHAPES["arxiv"]; e = synth.shape_edges(s)
+for _ in range(2):
+    lab, rep = grem.partition_edges(e, s.num_nodes, 8, GremConfig(chunk_frac=0.1))
+    assert hashlib.sha256(lab.astype("<i4").tobytes()).hexdigest() == gs["labels_sha256"]
+print("poison ok")
+'''
+    root = os.path.dirname(golden_dir.rstrip("/")).rsplit("/tests", 1)[0]
+    env = dict(os.environ, GREM_DEBUG_POISON="all")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "poison ok" in r.stdout, r.stdout + r.stderr
