@@ -19,6 +19,7 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 
 #include "grem_core.cuh"
@@ -912,8 +913,11 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
 }
 
 int64_t bundle_segment_len(int64_t nc) {
-    int64_t L = (nc + 4095) / 4096;   // <= 4096 segments
+    // the chain costs ~140 cycles per segment (dependent smem lookups) and a
+    // segment's simulation ~6 cycles per node: L ~ sqrt(24 nc) balances them
+    int64_t L = (int64_t)std::sqrt(24.0 * (double)nc);
     if (L < kCkpt) L = kCkpt;
+    if ((nc + L - 1) / L > 4096) L = (nc + 4095) / 4096;
     return (L + kCkpt - 1) / kCkpt * kCkpt;
 }
 int64_t bundle_ckpt_ints(int64_t nc) {
