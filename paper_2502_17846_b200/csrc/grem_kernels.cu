@@ -626,6 +626,172 @@ void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) 
     k_walk<<<1, 32, 0, s>>>(b.meta, b.newb, b.x, b.bad, b.tile_bad, nc, cap, b.scal + 4, b.scal + 3);
 }
 
+// ------------------------------------------------------- fused round kernels
+// One fixpoint round = k_round_reduce (preferences + tile clamp aggregates),
+// k_scan_top, k_round_down (exact-or-speculative x, tie verification,
+// speculative decisions, next tie guesses) and, only when a tie was
+// mis-speculated, the trajectory-bundle repair (which re-decides the repaired
+// suffix).  Node arrays are padded to whole tiles with inactive (identity)
+// nodes, so every thread moves kRI consecutive nodes with vector loads.
+constexpr int kRT = 512;             // threads per tile
+constexpr int kRI = 8;               // nodes per thread
+constexpr int kRTile = kRT * kRI;    // == kScanTile
+static_assert(kRTile == kScanTile, "round tiles reuse the scan tile buffers");
+
+struct RoundArgs {
+    const uint32_t* nodes;
+    uint8_t* meta;
+    const int32_t* newb;
+    const unsigned long long* cnt;
+    const double2* nbr;
+    const long long* sizes;
+    long long cap;
+    int64_t nc;
+};
+
+__device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t* v) {
+    uint2 w = *reinterpret_cast<const uint2*>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[k] = (uint8_t)(w.x >> (8 * k));
+        v[4 + k] = (uint8_t)(w.y >> (8 * k));
+    }
+}
+__device__ __forceinline__ void store8_u8(uint8_t* p, const uint8_t* v) {
+    uint2 w;
+    w.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
+    w.y = v[4] | (v[5] << 8) | (v[6] << 16) | ((uint32_t)v[7] << 24);
+    *reinterpret_cast<uint2*>(p) = w;
+}
+template <class T>
+__device__ __forceinline__ void load8_32(const T* p, T* v) {
+    int4 a = *reinterpret_cast<const int4*>(p), b = *reinterpret_cast<const int4*>(p + 4);
+    v[0] = (T)a.x; v[1] = (T)a.y; v[2] = (T)a.z; v[3] = (T)a.w;
+    v[4] = (T)b.x; v[5] = (T)b.y; v[6] = (T)b.z; v[7] = (T)b.w;
+}
+template <class T>
+__device__ __forceinline__ void store8_32(T* p, const T* v) {
+    *reinterpret_cast<int4*>(p) = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+    *reinterpret_cast<int4*>(p + 4) = make_int4((int)v[4], (int)v[5], (int)v[6], (int)v[7]);
+}
+
+__device__ __forceinline__ long long node_sl(uint8_t m, int32_t nb) {
+    return (long long)nb - ((meta_active(m) && meta_old(m) != -1) ? 1 : 0);
+}
+
+__global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_agg, int first_round) {
+    __shared__ Clamp smem[kRT / 32];
+    __shared__ Clamp stotal;
+    int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
+    uint8_t m[kRI];
+    int32_t nb[kRI];
+    uint32_t g[kRI];
+    load8_u8(a.meta + base, m);
+    load8_32(a.newb + base, nb);
+    load8_32(a.nodes + base, g);
+    long long x0 = a.sizes[0];
+    Clamp acc = clamp_identity();
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) {
+        uint8_t mm = m[j];
+        if (meta_active(mm)) {   // preferences: assign() inputs (grem.py:138-150)
+            unsigned long long c = a.cnt[g[j]];
+            double2 nbv = make_double2(0.0, 0.0);
+            if (meta_old(mm) != -1) nbv = a.nbr[g[j]];
+            double a0, a1;
+            averaged(mm, c, nbv, a0, a1);
+            int pref = a0 < a1 ? 1 : (a1 < a0 ? 0 : 2);
+            mm = (uint8_t)((mm & ~M_PREF) | (pref << M_PREF_SHIFT));
+            if (first_round) {
+                long long o = meta_old(mm) == 0 ? 1 : 0;
+                bool side0 = (x0 - o) <= (node_sl(mm, nb[j]) >> 1);
+                mm = (uint8_t)(side0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
+            }
+            m[j] = mm;
+        }
+        acc = clamp_then(acc, node_map(m[j], node_sl(m[j], nb[j]), a.cap).f);
+    }
+    store8_u8(a.meta + base, m);
+    block_excl_scan<kRT>(acc, smem, &stotal);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_agg[blockIdx.x] = stotal;
+}
+
+struct RoundOut {
+    int32_t* x;
+    int32_t* xalt;
+    uint8_t* tl;
+    long long* scal;   // [1] changed, [4] nbad, [6] first bad
+};
+
+__global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
+    __shared__ Clamp smem[kRT / 32];
+    __shared__ long long sbad;
+    if (threadIdx.x == 0) sbad = kInf;
+    int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
+    uint8_t m[kRI];
+    int32_t nb[kRI];
+    uint32_t g[kRI];
+    load8_u8(a.meta + base, m);
+    load8_32(a.newb + base, nb);
+    Clamp acc = clamp_identity();
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) acc = clamp_then(acc, node_map(m[j], node_sl(m[j], nb[j]), a.cap).f);
+    Clamp pre = block_excl_scan<kRT>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, tile_x[blockIdx.x]);
+    load8_32(a.nodes + base, g);
+    int32_t xs[kRI];
+    int nbad = 0, ch = 0;
+    long long mybad = kInf;
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) {
+        xs[j] = (int32_t)x;
+        uint8_t mm = m[j];
+        if (meta_active(mm)) {
+            long long sl = node_sl(mm, nb[j]);
+            NodeMap nm = node_map(mm, sl, a.cap);
+            int b = (x - nm.o <= nm.t) ? 0 : 1;
+            if (meta_pref(mm) == 2 && b != ((mm & M_SPEC) ? 1 : 0)) {   // mis-speculated tie
+                nbad++;
+                if (base + j < mybad) mybad = base + j;
+            }
+            // speculative decision (exact unless a repair follows) and tentative label update
+            uint8_t t8 = out.tl[g[j]];
+            int cur = t8 & 0xF, code = b + 1;
+            out.tl[g[j]] = (uint8_t)(code | (cur << 4));
+            ch += (code != cur);
+            // next round's tie guess: the tie rule at this x
+            bool tie0 = (x - nm.o) <= (sl >> 1);
+            m[j] = (uint8_t)(tie0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
+            x = clamp_apply(nm.f, x);
+        }
+    }
+    store8_32(out.x + base, xs);
+    store8_32(out.xalt + base, xs);
+    store8_u8(a.meta + base, m);
+    if (base + kRI > a.nc && base <= a.nc) out.x[a.nc] = xs[a.nc - base];   // padding is identity
+    for (int off = 16; off; off >>= 1) {
+        nbad += __shfl_down_sync(0xffffffffu, nbad, off);
+        ch += __shfl_down_sync(0xffffffffu, ch, off);
+    }
+    if (mybad != kInf) atomicMin(&sbad, mybad);
+    if ((threadIdx.x & 31) == 0) {
+        if (nbad) atomicAdd((unsigned long long*)(out.scal + 4), (unsigned long long)nbad);
+        if (ch) atomicAdd((unsigned long long*)(out.scal + 1), (unsigned long long)ch);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && sbad != kInf) atomicMin(out.scal + 6, sbad);
+}
+
+void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s) {
+    RoundArgs a{b.nodes, b.meta, b.newb, b.cnt, b.nbr, b.sizes, cap, nc};
+    int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
+    k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
+    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x);
+    RoundOut o{b.x, b.xnext, b.tl, b.scal};
+    k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
+}
+
 // ------------------------------------------------------- trajectory bundles
 // Exact repair when tie speculation failed.  Ties pull the
 // sizes chain toward balance, so trajectories started near the true value
@@ -875,16 +1041,28 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
     if (lane == 0) atomicAdd((unsigned long long*)misses, (unsigned long long)nmiss);
 }
 
-// parallel replay of the exact trajectory: one thread per checkpoint interval
+// parallel replay of the exact trajectory: one thread per checkpoint interval;
+// the repaired nodes are re-decided (their speculative decision, tentative
+// label and next tie guess from k_round_down are corrected).
+struct BundleFix {
+    const uint32_t* nodes;
+    uint8_t* meta;
+    const int32_t* newb;
+    uint8_t* tl;
+    int32_t* xalt;
+    long long* changed;
+};
+
 template <int NWIN>
 __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __restrict__ xin,
                                const int32_t* __restrict__ hit, const int32_t* __restrict__ ckpt, int64_t nseg,
                                int64_t nc, int64_t L, int32_t* __restrict__ x, const long long* nbad,
-                               const long long* first_bad) {
+                               const long long* first_bad, BundleFix fx) {
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
     int64_t seg0 = bundle_seg0(first_bad, L);
+    long long dch = 0;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nseg * ncp;
          w += (int64_t)gridDim.x * blockDim.x) {
         int64_t seg = w / ncp, cp = w % ncp;
@@ -906,10 +1084,30 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
         }
         for (int64_t i = a; i < e; ++i) {
             x[i] = (int32_t)cur;
-            cur = bundle_step(cur, bp[i]);
+            if (fx.xalt) fx.xalt[i] = (int32_t)cur;
+            int32_t pk = bp[i];
+            int o = pk & 3;
+            if (o != 2 && fx.tl) {
+                int b = (cur - o <= (long long)(pk >> 2)) ? 0 : 1;
+                uint32_t g = fx.nodes[i];
+                uint8_t t8 = fx.tl[g];
+                int spec_code = t8 & 0xF, prev = t8 >> 4;
+                if (b + 1 != spec_code) {
+                    fx.tl[g] = (uint8_t)((b + 1) | (prev << 4));
+                    dch += (long long)(b + 1 != prev) - (long long)(spec_code != prev);
+                }
+                uint8_t m = fx.meta[i];
+                bool tie0 = (cur - o) <= (node_sl(m, fx.newb[i]) >> 1);
+                fx.meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
+            }
+            cur = bundle_step(cur, pk);
         }
-        if (e == nc) x[nc] = (int32_t)cur;
+        if (e == nc) {
+            x[nc] = (int32_t)cur;
+            if (fx.xalt) fx.xalt[nc] = (int32_t)cur;
+        }
     }
+    if (fx.changed && dch) atomicAdd((unsigned long long*)fx.changed, (unsigned long long)dch);
 }
 
 int64_t bundle_segment_len(int64_t nc) {
@@ -927,12 +1125,14 @@ int64_t bundle_ckpt_ints(int64_t nc) {
 }
 
 void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, const BundleBufs& bb, int nwin,
-                   cudaStream_t s) {
+                   cudaStream_t s, bool fix_decisions) {
     int64_t L = bundle_segment_len(nc);
     int64_t nseg = (nc + L - 1) / L;
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
     const long long* nbad = b.scal + 4;
     const long long* first_bad = b.scal + 6;
+    BundleFix fx{b.nodes, b.meta, b.newb, fix_decisions ? b.tl : nullptr, fix_decisions ? b.xnext : nullptr,
+                 fix_decisions ? b.scal + 1 : nullptr};
     k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
     if (nwin == 3) {
@@ -940,13 +1140,15 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
                                                                  nbad, first_bad);
         k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3);
-        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad);
+        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad,
+                                               fx);
     } else {
         k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
                                                                  nbad, first_bad);
         k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3);
-        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad);
+        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad,
+                                               fx);
     }
 }
 

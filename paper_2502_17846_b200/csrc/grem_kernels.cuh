@@ -29,6 +29,8 @@ struct ChunkBufs {
     uint8_t* meta;
     int32_t* newb;      // exclusive count of active new nodes before i
     int32_t* x;         // sizes[0] before node i; x[N_c] = after the chunk
+    int32_t* xalt;      // exact x of the previous round (bundle window centre; read-only in a round)
+    int32_t* xnext;     // exact x of this round (becomes xalt of the next round)
     uint8_t* bad;       // tie speculation inconsistent at i
     // per scan tile
     Clamp* tile_agg;
@@ -66,8 +68,13 @@ struct BundleBufs {
 int64_t bundle_segment_len(int64_t nc);
 int64_t bundle_ckpt_ints(int64_t nc);
 void launch_half_predictor(const ChunkBufs& b, int64_t nc, long long cap, int32_t* xalt, cudaStream_t s);
+// fix_decisions: the repaired suffix's decisions / tentative labels / tie
+// guesses written by k_round_down are corrected (production rounds)
 void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t* xalt, const BundleBufs& bb, int nwin,
-                   cudaStream_t s);
+                   cudaStream_t s, bool fix_decisions);
+// fused round: preferences + clamp tile aggregates, top scan, x / tie check /
+// speculative decisions (node arrays padded to whole kScanTile tiles)
+void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s);
 void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);

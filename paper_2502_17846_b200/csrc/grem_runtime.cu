@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -102,7 +103,7 @@ struct grem_ctx {
     // per chunk node
     DBuf<uint32_t> nodes{"nodes"};
     DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
-    DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
+    DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
     DBuf<Clamp> tile_agg{"tile_agg"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
@@ -207,13 +208,15 @@ void ensure_nodes(grem_ctx* c, int64_t n) {
 }
 
 void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
-    c->nodes.ensure(nc_cap);
-    c->meta.ensure(nc_cap);
-    c->bad.ensure(nc_cap);
+    int64_t padded = (nc_cap + 1 + kScanTile - 1) / kScanTile * kScanTile + 16;   // whole round tiles
+    c->nodes.ensure(padded);
+    c->meta.ensure(padded);
+    c->bad.ensure(padded);
     c->want.ensure(nc_cap);
-    c->newb.ensure(nc_cap + 1);
-    c->x.ensure(nc_cap + 1);
-    c->xalt.ensure(nc_cap + 1);
+    c->newb.ensure(padded);
+    c->x.ensure(padded);
+    c->xalt.ensure(padded);
+    c->xnext.ensure(padded);
     int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
     c->bends.ensure(nseg * 192);
     c->bxin.ensure(nseg);
@@ -266,6 +269,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.meta = c->meta.p;
     b.newb = c->newb.p;
     b.x = c->x.p;
+    b.xalt = c->xalt.p;
+    b.xnext = c->xnext.p;
     b.bad = c->bad.p;
     b.tile_agg = c->tile_agg.p;
     b.tile_x = c->tile_x.p;
@@ -480,6 +485,11 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         launch_add_base(c->newb.p, nc, c->d_sizes, s);
     }
     c->kernels += 3;
+    // identity padding up to whole round tiles (inactive nodes, meta 0)
+    {
+        int64_t padded = (nc + 1 + kScanTile - 1) / kScanTile * kScanTile;
+        CK(cudaMemsetAsync(c->meta.p + nc, 0, padded - nc, s));
+    }
     int64_t rounds = 0;
     for (int r = 1;; ++r) {
         rounds++;
@@ -489,11 +499,14 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             c->stats.count_bytes += 9 * mc;   // 8 B edge read + 1 B tentative-label gather
             c->kernels++;
         }
-        { PhaseScope ps(c, PH_PREFS); launch_prefs(b, nc, r == 1, s); }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 6, 0x7F, sizeof(long long), s));   // first bad = +large
-        { PhaseScope ps(c, PH_SCAN); launch_chunk_scan(b, nc, a.cap, s); }
+        {
+            PhaseScope ps(c, PH_SCAN);
+            launch_round_scan(b, nc, a.cap, r == 1, s);
+            c->kernels += 3;
+        }
         {
             // exact repair by trajectory bundles, gated on the device by the
             // number of mis-speculated ties (no host round trip); windows:
@@ -505,7 +518,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
                 c->kernels += 4;
             }
             BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
-            launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s);
+            launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
             c->kernels += 4;
         }
         if (getenv("GREM_DEBUG_BUNDLE")) {
@@ -513,12 +526,10 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             fprintf(stderr, "[bundle] round %d nc %lld nbad %lld misses(cum) %lld\n", r, (long long)nc, c->h_pin[1],
                     c->h_pin[0]);
         }
-        {
-            PhaseScope ps(c, PH_DECIDE);
-            launch_decide(b, nc, a.cap, s);
-            CK(cudaMemcpyAsync(c->xalt.p, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToDevice, s));
-        }
-        c->kernels += 1;
+        // this round's exact x becomes the next round's second window centre
+        std::swap(c->xalt.p, c->xnext.p);
+        b.xalt = c->xalt.p;
+        b.xnext = c->xnext.p;
         scal_read(c, c->d_scal + 1, 1);
         if (c->h_pin[0] == 0) break;
         if (r > nc + 2) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
@@ -1215,7 +1226,7 @@ extern "C" int grem_debug_chunk_scan(grem_ctx* c, const uint8_t* meta, const int
         if (do_walk >= 2) {   // production repair: half-step predictor + trajectory bundles (2 or 3 windows)
             launch_half_predictor(b, nc, cap, c->xalt.p, c->s);
             BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
-            launch_bundle(b, nc, cap, c->xalt.p, bb, do_walk == 2 ? 3 : 2, c->s);
+            launch_bundle(b, nc, cap, c->xalt.p, bb, do_walk == 2 ? 3 : 2, c->s, false);
         }
         CK(cudaMemcpyAsync(x_out, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost, c->s));
         CK(cudaMemcpyAsync(bad_out, c->bad.p, nc, cudaMemcpyDeviceToHost, c->s));
