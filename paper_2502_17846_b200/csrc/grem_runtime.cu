@@ -14,6 +14,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <new>
 #include <utility>
@@ -52,18 +55,20 @@ struct DBuf {
     size_t cap = 0;   // elements
     DBuf() = default;
     explicit DBuf(const char* nm) : name(nm) {}
-    void ensure(size_t n) {
+    // stream-ordered growth from the device memory pool: no device-wide
+    // synchronisation, so concurrent sibling contexts never stall each other
+    void ensure(size_t n, cudaStream_t s) {
         if (n <= cap) return;
-        if (p) cudaFree(p);
+        if (p) CK(cudaFreeAsync(p, s));
         p = nullptr;
         size_t c = n + n / 8 + 64;
-        CK(cudaMalloc(&p, c * sizeof(T)));
+        CK(cudaMallocAsync((void**)&p, c * sizeof(T), s));
         cap = c;
         // debug: GREM_DEBUG_POISON=all|name,name fills new buffers with 0xA5 to
         // expose reads of memory that was never written in this call
         static const char* poison = getenv("GREM_DEBUG_POISON");
         if (poison && (strcmp(poison, "all") == 0 || strstr(poison, (std::string(",") + name + ",").c_str())))
-            CK(cudaMemset(p, 0xA5, c * sizeof(T)));
+            CK(cudaMemsetAsync(p, 0xA5, c * sizeof(T), s));
     }
     void release() {
         if (p) cudaFree(p);
@@ -87,6 +92,12 @@ static const char* kPhaseNames[PH_N] = {"count", "select", "node_init", "prefs",
 struct grem_ctx {
     int device = 0;
     int profiling = 0;
+    // sibling subtrees of partition() run concurrently on child contexts
+    // (own stream, workspaces, host thread); the root owns the pool
+    grem_ctx* root = nullptr;
+    std::mutex pool_mu;
+    std::vector<grem_ctx*> pool_all, pool_idle;
+    std::vector<std::pair<long long, grem_ctx*>> pool_keyed;   // subtree position -> context
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_open;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -132,6 +143,10 @@ struct grem_ctx {
     // count_cuts
     DBuf<unsigned long long> cc_sizes;
     DBuf<int32_t> lab32;
+    // recursion arena: per-level induced-subgraph buffers (reused across calls)
+    DBuf<uint2> rec_e[40];
+    DBuf<int32_t> rec_o[40];
+    DBuf<int32_t> part_fin{"part_fin"}, part_orig{"part_orig"};
     // live state for hooks
     int64_t live_n = 0;
     grem_stats stats{};
@@ -152,7 +167,7 @@ void scal_write(grem_ctx* c, long long* ddst, const long long* vals, int count) 
     CK(cudaStreamSynchronize(c->s));
 }
 
-void ensure_temp(grem_ctx* c, size_t bytes) { c->temp.ensure(bytes); }
+void ensure_temp(grem_ctx* c, size_t bytes) { c->temp.ensure(bytes, c->s); }
 
 cudaEvent_t prof_event(grem_ctx* c) {
     if (c->ev_used == c->ev_pool.size()) {
@@ -195,65 +210,65 @@ void prof_collect(grem_ctx* c) {
 }
 
 void ensure_nodes(grem_ctx* c, int64_t n) {
-    c->lab.ensure(n);
-    c->tl.ensure(n);
-    c->flag.ensure(n);
-    c->cnt.ensure(n);
-    c->nbr.ensure(n);
-    c->rank.ensure(n);
-    c->scratch.ensure(2 * n + 2);
-    c->newid.ensure(n + 1);
+    c->lab.ensure(n, c->s);
+    c->tl.ensure(n, c->s);
+    c->flag.ensure(n, c->s);
+    c->cnt.ensure(n, c->s);
+    c->nbr.ensure(n, c->s);
+    c->rank.ensure(n, c->s);
+    c->scratch.ensure(2 * n + 2, c->s);
+    c->newid.ensure(n + 1, c->s);
     ensure_temp(c, select_nodes_temp_bytes(n));
     ensure_temp(c, scan_temp_bytes(n + 1));
 }
 
 void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     int64_t padded = (nc_cap + 1 + kScanTile - 1) / kScanTile * kScanTile + 16;   // whole round tiles
-    c->nodes.ensure(padded);
-    c->meta.ensure(padded);
-    c->bad.ensure(padded);
-    c->want.ensure(nc_cap);
-    c->newb.ensure(padded);
-    c->x.ensure(padded);
-    c->xalt.ensure(padded);
-    c->xnext.ensure(padded);
+    c->nodes.ensure(padded, c->s);
+    c->meta.ensure(padded, c->s);
+    c->bad.ensure(padded, c->s);
+    c->want.ensure(nc_cap, c->s);
+    c->newb.ensure(padded, c->s);
+    c->x.ensure(padded, c->s);
+    c->xalt.ensure(padded, c->s);
+    c->xnext.ensure(padded, c->s);
     int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
-    c->bends.ensure(nseg * 192);
-    c->bxin.ensure(nseg);
-    c->bhit.ensure(nseg);
-    c->bparams.ensure(nc_cap + 1);
-    c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192);
+    c->bends.ensure(nseg * 192, c->s);
+    c->bxin.ensure(nseg, c->s);
+    c->bhit.ensure(nseg, c->s);
+    c->bparams.ensure(nc_cap + 1, c->s);
+    c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192, c->s);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
-    c->tile_agg.ensure(tiles);
-    c->tile_x.ensure(tiles);
-    c->tile_bad.ensure(tiles);
+    c->tile_agg.ensure(tiles, c->s);
+    c->tile_x.ensure(tiles, c->s);
+    c->tile_bad.ensure(tiles, c->s);
     ensure_temp(c, scan_temp_bytes(nc_cap + 1));
     ensure_temp(c, sort_temp_bytes(nc_cap));
 }
 
 void ensure_seed(grem_ctx* c, int64_t nc, int64_t entries) {
-    c->start.ensure(nc + 1);
-    c->cursor.ensure(nc + 1);
-    c->adj.ensure(entries + 1);
-    c->row_of.ensure(entries + 1);
-    c->parent.ensure(nc);
-    c->csize.ensure(nc);
-    c->roots.ensure(nc);
-    c->rvals.ensure(nc);
-    c->rvals2.ensure(nc);
-    c->cpos.ensure(nc);
-    c->disc.ensure(nc);
-    c->frontier.ensure(nc);
-    c->ckey.ensure(nc);
-    c->rkeys.ensure(nc);
-    c->rkeys2.ensure(nc);
-    c->cand.ensure(nc);
-    c->cand2.ensure(nc);
-    c->pair.ensure(nc);
-    c->slab.ensure(nc);
-    c->slab2.ensure(nc);
-    c->fdeg.ensure(nc + 1);
-    c->cum.ensure(nc + 1);
+    c->start.ensure(nc + 1, c->s);
+    c->cursor.ensure(nc + 1, c->s);
+    c->adj.ensure(entries + 1, c->s);
+    c->row_of.ensure(entries + 1, c->s);
+    c->parent.ensure(nc, c->s);
+    c->csize.ensure(nc, c->s);
+    c->roots.ensure(nc, c->s);
+    c->rvals.ensure(nc, c->s);
+    c->rvals2.ensure(nc, c->s);
+    c->cpos.ensure(nc, c->s);
+    c->disc.ensure(nc, c->s);
+    c->frontier.ensure(nc, c->s);
+    c->ckey.ensure(nc, c->s);
+    c->rkeys.ensure(nc, c->s);
+    c->rkeys2.ensure(nc, c->s);
+    c->cand.ensure(nc, c->s);
+    c->cand2.ensure(nc, c->s);
+    c->pair.ensure(nc, c->s);
+    c->slab.ensure(nc, c->s);
+    c->slab2.ensure(nc, c->s);
+    c->fdeg.ensure(nc + 1, c->s);
+    c->cum.ensure(nc + 1, c->s);
     ensure_temp(c, sort_temp_bytes(nc));
     ensure_temp(c, scan_temp_bytes(nc + 1));
 }
@@ -578,7 +593,7 @@ void detect_hubs(grem_ctx* c, const BisectArgs& a) {
     int64_t S = a.m < (1LL << 22) ? a.m : (1LL << 22);
     CK(cudaMemsetAsync(c->scratch.p, 0, sizeof(int32_t) * a.n, s));
     launch_sample_degrees(a.e, S, c->scratch.p, s);
-    c->hub_ids.ensure(1 << 20);
+    c->hub_ids.ensure(1 << 20, c->s);
     ensure_temp(c, hub_select_temp_bytes(a.n));
     const char* env_deg = getenv("GREM_HUB_MIN_DEG");
     launch_hub_select(c->scratch.p, a.n, env_deg ? atoi(env_deg) : 16, c->hub_ids.p, c->d_sscal + 8, c->temp.p, c->temp.cap, s);
@@ -587,9 +602,9 @@ void detect_hubs(grem_ctx* c, const BisectArgs& a) {
     int64_t cnt = c->h_pin[0];
     if (cnt <= 0) return;
     if (cnt > (1 << 20)) cnt = 1 << 20;
-    c->hub_k1.ensure(cnt);
-    c->hub_k2.ensure(cnt);
-    c->hub_table.ensure(kHubSlots);
+    c->hub_k1.ensure(cnt, c->s);
+    c->hub_k2.ensure(cnt, c->s);
+    c->hub_table.ensure(kHubSlots, c->s);
     ensure_temp(c, sort_temp_bytes(cnt));
     launch_hub_keys(c->hub_ids.p, cnt, c->scratch.p, c->hub_k1.p, s);
     sort_keys_u64_desc(c->hub_k1.p, c->hub_k2.p, cnt, c->temp.p, c->temp.cap, s);
@@ -702,7 +717,7 @@ void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, 
     cudaStream_t s = c->s;
     int64_t cap = rep && rep->sizes_cap > 0 ? rep->sizes_cap : 2;
     if (cap < 2) cap = 2;
-    c->cc_sizes.ensure(cap + 4);
+    c->cc_sizes.ensure(cap + 4, c->s);
     unsigned long long* d = c->cc_sizes.p;   // [0] cut, [1] max|neg, [2..] sizes
     CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * (cap + 4), s));
     int* d_max = (int*)(d + 1);
@@ -771,7 +786,7 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
     if (on_device || m == 0) {
         d = reinterpret_cast<const uint2*>(edges);
     } else {
-        c->edges_owned.ensure(m);
+        c->edges_owned.ensure(m, c->s);
         staged_upload(c, c->edges_owned.p, (uint64_t)m * 8,
                       [&](void* buf, uint64_t off, size_t len) { memcpy(buf, (const char*)edges + off, len); });
         d = c->edges_owned.p;
@@ -779,7 +794,7 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
     if (m > 0) {
         // _check_ids (edgefile.py:63-65)
         unsigned long long* tmp;
-        c->cc_sizes.ensure(4);
+        c->cc_sizes.ensure(4, c->s);
         tmp = c->cc_sizes.p;
         CK(cudaMemsetAsync(tmp, 0, sizeof(unsigned long long), c->s));
         launch_check_ids(d, m, (uint32_t*)tmp, c->s);
@@ -824,7 +839,7 @@ const uint2* load_grpe(grem_ctx* c, const char* path, GrpeHeader* hd) {
     *hd = read_grpe_header(path);
     int64_t m = hd->m;
     if (m == 0) return nullptr;
-    c->edges_owned.ensure(m);
+    c->edges_owned.ensure(m, c->s);
     FILE* f = fopen(path, "rb");
     if (!f) fail(GREM_E_FORMAT, std::string(path) + ": cannot open");
     fseek(f, 28, SEEK_SET);
@@ -852,12 +867,74 @@ void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_
     a.seed_passes = cfg->seed_refinement_passes;
     a.hooks = hooks;
     bisect_core(c, a);
-    c->lab32.ensure(n);
+    c->lab32.ensure(n, c->s);
     launch_labels_to_i32(c->lab.p, n, c->lab32.p, c->s);
     c->kernels++;
     if (rep) count_cuts_dev(c, d, m, c->lab32.p, n, rep);
     if (labels_out) CK(cudaMemcpyAsync(labels_out, c->lab32.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
+}
+
+void init_ctx(grem_ctx* c, int device) {
+    c->device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaMalloc(&c->d_sizes, sizeof(long long) * 2));
+    CK(cudaMalloc(&c->d_scal, sizeof(long long) * 8));
+    CK(cudaMalloc(&c->d_sscal, sizeof(long long) * 16));
+    CK(cudaHostAlloc(&c->h_pin, sizeof(long long) * 32, cudaHostAllocDefault));
+    ensure_temp(c, 1 << 20);
+}
+
+// A subtree position (level, leaf base) always gets the same child context,
+// so its workspaces are sized once and reused by later calls.
+grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
+    grem_ctx* ch = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(root->pool_mu);
+        for (auto& kv : root->pool_keyed)
+            if (kv.first == key) ch = kv.second;
+        if (!ch) {
+            ch = new grem_ctx();
+            ch->root = root;
+            init_ctx(ch, root->device);
+            root->pool_all.push_back(ch);
+            root->pool_keyed.push_back({key, ch});
+        }
+    }
+    memset(&ch->stats, 0, sizeof(ch->stats));
+    ch->kernels = 0;
+    for (int k = 0; k < PH_N; ++k) {
+        ch->phase_ms[k] = 0;
+        ch->phase_n[k] = 0;
+    }
+    ch->prof_open.clear();
+    ch->ev_used = 0;
+    ch->profiling = root->profiling;
+    return ch;
+}
+
+// fold a finished child's counters into its parent (stream already synchronised)
+void ctx_release(grem_ctx* parent, grem_ctx* ch) {
+    prof_collect(ch);
+    grem_ctx* root = parent->root;
+    (void)root;
+    parent->stats.chunks += ch->stats.chunks;
+    parent->stats.rounds += ch->stats.rounds;
+    if (ch->stats.max_rounds > parent->stats.max_rounds) parent->stats.max_rounds = ch->stats.max_rounds;
+    parent->stats.visits += ch->stats.visits;
+    parent->stats.walk_steps += ch->stats.walk_steps;
+    parent->stats.seed_bfs_levels += ch->stats.seed_bfs_levels;
+    parent->stats.bisections += ch->stats.bisections;
+    parent->stats.count_bytes += ch->stats.count_bytes;
+    parent->stats.path_bytes += ch->stats.path_bytes;
+    parent->kernels += ch->kernels;
+    for (int k = 0; k < PH_N; ++k) {
+        parent->phase_ms[k] += ch->phase_ms[k];
+        parent->phase_n[k] += ch->phase_n[k];
+    }
 }
 
 // partition (grem.py:277-319): depth-first like the reference; both sides
@@ -873,6 +950,7 @@ struct PartCtx {
 void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, const int32_t* orig, int64_t p_level,
              int level, int64_t leaf_base) {
     cudaStream_t s = c->s;
+    if (level >= 39) fail(GREM_E_FORMAT, "partition depth exceeds 2^39 parts");
     double capd = std::ceil((1.0 + pc.cfg->capacity_slack) * (double)pc.total_nodes / (double)(1LL << (level + 1)));
     BisectArgs a;
     a.e = e;
@@ -895,10 +973,10 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         return;
     }
     // extract both sides
-    uint2* sub_e = nullptr;
-    int32_t* sub_o = nullptr;
-    CK(cudaMallocAsync(&sub_e, sizeof(uint2) * (m > 0 ? m : 1), s));
-    CK(cudaMallocAsync(&sub_o, sizeof(int32_t) * n, s));
+    c->rec_e[level].ensure(m > 0 ? m : 1, s);
+    c->rec_o[level].ensure(n, s);
+    uint2* sub_e = c->rec_e[level].p;
+    int32_t* sub_o = c->rec_o[level].p;
     int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
     ensure_temp(c, extract_temp_bytes(m > 0 ? m : 1));
     for (int side = 0; side < 2; ++side) {
@@ -925,15 +1003,50 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         n_off[side + 1] = n_off[side] + k;
     }
     c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
-    for (int side = 0; side < 2; ++side) {
+    auto side_call = [&](grem_ctx* cc, int side) {
         int64_t k = n_off[side + 1] - n_off[side];
-        if (k == 0) continue;   // grem.py:308-309
+        if (k == 0) return;   // grem.py:308-309
         int64_t base = leaf_base + side * (p_level / 2);
-        recurse(c, pc, sub_e + e_off[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
+        recurse(cc, pc, sub_e + e_off[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
                 level + 1, base);
+    };
+    // The two sides are independent problems: side 1 runs concurrently on a
+    // child context (own stream + host thread) unless a meter is attached
+    // (the reference's residency accounting is sequential) or disabled.
+    bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0);
+    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
+    if (par) {
+        cudaEvent_t ready;
+        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(ready, s));
+        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + p_level / 2));
+        std::exception_ptr err = nullptr;
+        std::thread th([&] {
+            try {
+                CK(cudaSetDevice(ch->device));
+                CK(cudaStreamWaitEvent(ch->s, ready, 0));
+                side_call(ch, 1);
+                CK(cudaStreamSynchronize(ch->s));
+            } catch (...) {
+                err = std::current_exception();
+                cudaStreamSynchronize(ch->s);
+            }
+        });
+        std::exception_ptr err0 = nullptr;
+        try {
+            side_call(c, 0);
+        } catch (...) {
+            err0 = std::current_exception();
+        }
+        th.join();
+        cudaEventDestroy(ready);
+        ctx_release(c, ch);
+        if (err0) std::rethrow_exception(err0);
+        if (err) std::rethrow_exception(err);
+    } else {
+        side_call(c, 0);
+        side_call(c, 1);
     }
-    CK(cudaFreeAsync(sub_e, s));
-    CK(cudaFreeAsync(sub_o, s));
 }
 
 void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t p, const grem_config* cfg,
@@ -942,10 +1055,10 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
     validate_cfg(cfg);
     cudaStream_t s = c->s;
-    int32_t* fin = nullptr;
-    int32_t* orig = nullptr;
-    CK(cudaMallocAsync(&fin, sizeof(int32_t) * n, s));
-    CK(cudaMallocAsync(&orig, sizeof(int32_t) * n, s));
+    c->part_fin.ensure(n, s);
+    c->part_orig.ensure(n, s);
+    int32_t* fin = c->part_fin.p;
+    int32_t* orig = c->part_orig.p;
     CK(cudaMemsetAsync(fin, 0xFF, sizeof(int32_t) * n, s));
     launch_iota(orig, n, s);
     PartCtx pc{n, cfg, hooks, fin};
@@ -956,13 +1069,9 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     } catch (...) {
-        cudaFreeAsync(fin, s);
-        cudaFreeAsync(orig, s);
         cudaStreamSynchronize(s);
         throw;
     }
-    CK(cudaFreeAsync(fin, s));
-    CK(cudaFreeAsync(orig, s));
     CK(cudaStreamSynchronize(s));
 }
 
@@ -1014,22 +1123,14 @@ const char* grem_last_error(void) { return g_err.c_str(); }
 grem_ctx* grem_create(int device) {
     g_err.clear();
     grem_ctx* c = new grem_ctx();
-    c->device = device;
+    c->root = c;
     try {
-        CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
-        CK(cudaEventCreate(&c->ev0));
-        CK(cudaEventCreate(&c->ev1));
-        CK(cudaMalloc(&c->d_sizes, sizeof(long long) * 2));
-        CK(cudaMalloc(&c->d_scal, sizeof(long long) * 8));
-        CK(cudaMalloc(&c->d_sscal, sizeof(long long) * 16));
-        CK(cudaHostAlloc(&c->h_pin, sizeof(long long) * 32, cudaHostAllocDefault));
+        init_ctx(c, device);
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        ensure_temp(c, 1 << 20);
     } catch (const GremError& e) {
         g_err = e.msg;
         delete c;
@@ -1040,6 +1141,8 @@ grem_ctx* grem_create(int device) {
 
 void grem_destroy(grem_ctx* c) {
     if (!c) return;
+    for (grem_ctx* ch : c->pool_all) grem_destroy(ch);
+    c->pool_all.clear();
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->s);
     c->lab.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
@@ -1052,6 +1155,12 @@ void grem_destroy(grem_ctx* c) {
     c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
     c->fdeg.release(); c->cum.release(); c->temp.release(); c->edges_owned.release(); c->cc_sizes.release();
     c->lab32.release();
+    for (int l = 0; l < 40; ++l) {
+        c->rec_e[l].release();
+        c->rec_o[l].release();
+    }
+    c->part_fin.release();
+    c->part_orig.release();
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -1117,7 +1226,7 @@ int grem_count_cuts_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n
         const uint2* d = stage_edges(c, edges, m, n, on_device);
         const int32_t* dl = labels;
         if (!labels_on_device) {
-            c->lab32.ensure(n);
+            c->lab32.ensure(n, c->s);
             CK(cudaMemcpyAsync(c->lab32.p, labels, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->s));
             dl = c->lab32.p;
         }
