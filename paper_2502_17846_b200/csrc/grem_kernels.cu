@@ -379,6 +379,198 @@ void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStrea
     k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.cnt, b.hub_keys);
 }
 
+// -------------------------------------------------- binned round-1 counting
+__device__ __forceinline__ uint32_t lab2_code(const uint32_t* __restrict__ lab2, uint32_t u) {
+    return (lab2[u >> 4] >> ((u & 15) * 2)) & 3u;
+}
+
+__global__ void __launch_bounds__(kEdgeThreads) k_bin_count(const uint2* __restrict__ e, int64_t m,
+                                                            const uint32_t* __restrict__ hub_keys, int shift,
+                                                            int nbins, unsigned int* __restrict__ bin_count) {
+    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ unsigned int s_hist[kMaxBins];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kMaxBins; k += blockDim.x) s_hist[k] = 0;
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        uint2 ed = e[i];
+        if (hub_find(s_keys, ed.x) < 0) atomicAdd(&s_hist[ed.x >> shift], 1u);
+        if (ed.x != ed.y && hub_find(s_keys, ed.y) < 0) atomicAdd(&s_hist[ed.y >> shift], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nbins; k += blockDim.x)
+        if (s_hist[k]) atomicAdd(&bin_count[k], s_hist[k]);
+}
+
+__global__ void k_bin_offsets(unsigned int* bin_count, unsigned int* bin_cur, int nbins) {
+    if (threadIdx.x == 0) {
+        unsigned int acc = 0;
+        for (int b = 0; b < nbins; ++b) {
+            unsigned int c = bin_count[b];
+            bin_cur[b] = acc;
+            acc += c;
+        }
+        bin_count[kMaxBins] = acc;   // total records
+    }
+}
+
+constexpr int kBinBatch = 4096;                  // edges per CTA batch (<= 2 records each)
+constexpr size_t kBinSmem = (size_t)kHubSlots * (4 + 8 + 1) + (size_t)kMaxBins * 4 * 4 + (size_t)2 * kBinBatch * 4 * 2 + 16;
+
+__global__ void __launch_bounds__(kEdgeThreads) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
+                                                              const uint32_t* __restrict__ lab2,
+                                                              const uint32_t* __restrict__ hub_keys, int shift,
+                                                              int nbins, unsigned int* __restrict__ bin_cur,
+                                                              uint32_t* __restrict__ recs,
+                                                              unsigned long long* __restrict__ cnt,
+                                                              uint8_t* __restrict__ flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(smem_raw);
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_cnt + kHubSlots);
+    unsigned int* s_hist = s_keys + kHubSlots;
+    unsigned int* s_start = s_hist + kMaxBins;
+    unsigned int* s_fill = s_start + kMaxBins;
+    unsigned int* s_base = s_fill + kMaxBins;
+    uint32_t* s_rec = s_base + kMaxBins;
+    uint32_t* s_out = s_rec + 2 * kBinBatch;
+    unsigned int* s_n = s_out + 2 * kBinBatch;
+    uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_n + 4);
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        s_cnt[k] = 0ULL;
+        s_flag[k] = 0;
+    }
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t b0 = lo; b0 < hi; b0 += kBinBatch) {
+        int64_t b1 = b0 + kBinBatch < hi ? b0 + kBinBatch : hi;
+        for (int k = threadIdx.x; k < nbins; k += blockDim.x) {
+            s_hist[k] = 0;
+            s_fill[k] = 0;
+        }
+        if (threadIdx.x == 0) *s_n = 0;
+        __syncthreads();
+        // records: node << 2 | code (1: +c0, 2: +c1, 0: unassigned neighbour, 3: self-loop)
+        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+            uint2 ed = e[i];
+            uint32_t u = ed.x, v = ed.y;
+            int hu = hub_find(s_keys, u);
+            if (u == v) {
+                if (hu >= 0) s_flag[hu] = 1;
+                else {
+                    unsigned int p = atomicAdd(s_n, 1u);
+                    s_rec[p] = (u << 2) | 3u;
+                    atomicAdd(&s_hist[u >> shift], 1u);
+                }
+                continue;
+            }
+            int hv = hub_find(s_keys, v);
+            uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
+            if (hu >= 0) {
+                if (cv) atomicAdd(&s_cnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
+                else s_flag[hu] = 1;
+            } else {
+                unsigned int p = atomicAdd(s_n, 1u);
+                s_rec[p] = (u << 2) | cv;
+                atomicAdd(&s_hist[u >> shift], 1u);
+            }
+            if (hv >= 0) {
+                if (cu) atomicAdd(&s_cnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
+                else s_flag[hv] = 1;
+            } else {
+                unsigned int p = atomicAdd(s_n, 1u);
+                s_rec[p] = (v << 2) | cu;
+                atomicAdd(&s_hist[v >> shift], 1u);
+            }
+        }
+        __syncthreads();
+        // block counting sort by bin: starts (exclusive scan) and global reservations
+        if (threadIdx.x < 32) {
+            unsigned int carry = 0;
+            for (int c0 = 0; c0 < nbins; c0 += 32) {
+                int k = c0 + threadIdx.x;
+                unsigned int v = k < nbins ? s_hist[k] : 0u;
+                unsigned int incl = v;
+                for (int off = 1; off < 32; off <<= 1) {
+                    unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+                    if ((int)threadIdx.x >= off) incl += o;
+                }
+                if (k < nbins) {
+                    s_start[k] = carry + incl - v;
+                    s_base[k] = v ? atomicAdd(&bin_cur[k], v) : 0u;
+                }
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+        unsigned int nrec = *s_n;
+        for (unsigned int k = threadIdx.x; k < nrec; k += blockDim.x) {
+            uint32_t r = s_rec[k];
+            unsigned int bb = (r >> 2) >> shift;
+            s_out[s_start[bb] + atomicAdd(&s_fill[bb], 1u)] = r;
+        }
+        __syncthreads();
+        for (unsigned int k = threadIdx.x; k < nrec; k += blockDim.x) {   // runs of a bin are contiguous
+            uint32_t r = s_out[k];
+            unsigned int bb = (r >> 2) >> shift;
+            recs[s_base[bb] + (k - s_start[bb])] = r;
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        uint32_t key = s_keys[k];
+        if (key == kHubEmpty) continue;
+        if (s_cnt[k]) atomicAdd(&cnt[key], s_cnt[k]);
+        if (s_flag[k]) flag[key] = 1;
+    }
+}
+
+// apply records bin by bin: work items are handed out in array order from a
+// global counter, so the whole GPU stays within ~one bin at a time and that
+// bin's counter slice is L2-hot (a grid-stride loop lets warps drift apart
+// across many bins and the REDs miss L2).
+constexpr int kApplyItem = 2048;
+__global__ void __launch_bounds__(256) k_bin_apply(const uint32_t* __restrict__ recs,
+                                                   const unsigned int* __restrict__ bin_count,
+                                                   unsigned long long* __restrict__ cnt, uint8_t* __restrict__ flag,
+                                                   unsigned int* __restrict__ work) {
+    __shared__ unsigned int s_item;
+    int64_t total = bin_count[kMaxBins];
+    while (true) {
+        if (threadIdx.x == 0) s_item = atomicAdd(work, 1u);
+        __syncthreads();
+        int64_t base = (int64_t)s_item * kApplyItem;
+        __syncthreads();
+        if (base >= total) break;
+        int64_t end = base + kApplyItem < total ? base + kApplyItem : total;
+        for (int64_t i = base + threadIdx.x; i < end; i += blockDim.x) {
+            uint32_t r = recs[i];
+            uint32_t node = r >> 2, c = r & 3u;
+            if (c == 1) atomicAdd(&cnt[node], 1ULL);
+            else if (c == 2) atomicAdd(&cnt[node], 1ULL << 32);
+            else flag[node] = 1;
+        }
+    }
+}
+
+void launch_count_init_binned(const uint2* e, int64_t m, const ChunkBufs& b, const BinBufs& bb, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem);
+        attr = true;
+    }
+    cudaMemsetAsync(bb.bin_count, 0, sizeof(unsigned int) * (kMaxBins + 2), s);   // counts, total, apply cursor
+    k_bin_count<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.bin_count);
+    k_bin_offsets<<<1, 32, 0, s>>>(bb.bin_count, bb.bin_cur, bb.nbins);
+    unsigned grid = (unsigned)(num_sms() * 2);
+    k_bin_scatter<<<grid, kEdgeThreads, kBinSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.bin_cur,
+                                                     bb.recs, b.cnt, b.flag);
+    k_bin_apply<<<(unsigned)(num_sms() * 8), 256, 0, s>>>(bb.recs, bb.bin_count, b.cnt, b.flag,
+                                                        bb.bin_count + kMaxBins + 1);
+}
+
 // hub detection: endpoint histogram of a sample, candidates, top-K
 __global__ void k_sample_deg(const uint2* __restrict__ e, int64_t sample, int32_t* sdeg) {
     GRID_STRIDE(i, sample) {
@@ -1183,7 +1375,7 @@ void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s
 
 __global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const uint8_t* __restrict__ meta,
                          unsigned long long* __restrict__ cnt, double2* __restrict__ nbr, int8_t* __restrict__ lab,
-                         const uint8_t* __restrict__ tl, uint8_t* __restrict__ flag) {
+                         const uint8_t* __restrict__ tl, uint8_t* __restrict__ flag, uint32_t* __restrict__ lab2) {
     GRID_STRIDE(i, nc) {
         uint32_t g = nodes[i];
         uint8_t m = meta[i];
@@ -1193,7 +1385,10 @@ __global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const u
             double a0, a1;
             averaged(m, cnt[g], nb, a0, a1);
             nbr[g] = make_double2(a0, a1);
-            lab[g] = (int8_t)((tl[g] & 0xF) - 1);
+            int code = tl[g] & 0xF;
+            lab[g] = (int8_t)(code - 1);
+            uint32_t diff = (uint32_t)((code ^ (m & M_OLD)) & 3);
+            if (diff) atomicXor(&lab2[g >> 4], diff << ((g & 15) * 2));
         }
         cnt[g] = 0ULL;
         flag[g] = 0;
@@ -1201,7 +1396,7 @@ __global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const u
 }
 
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
-    k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cnt, b.nbr, b.lab, b.tl, b.flag);
+    k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cnt, b.nbr, b.lab, b.tl, b.flag, b.lab2);
 }
 
 __global__ void k_sizes_update(long long* sizes, const int32_t* x, int64_t nc, const long long* total_new) {
@@ -1597,11 +1792,12 @@ void launch_refine_decide(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, lo
 
 __global__ void k_seed_commit(const uint32_t* nodes, int64_t nc, const int8_t* slab,
                               const unsigned long long* pair, int8_t* lab, double2* nbr, uint8_t* flag,
-                              long long* zeros) {
+                              long long* zeros, uint32_t* lab2) {
     int z = 0;
     GRID_STRIDE(i, nc) {
         uint32_t g = nodes[i];
         lab[g] = slab[i];
+        atomicXor(&lab2[g >> 4], (uint32_t)(slab[i] + 1) << ((g & 15) * 2));   // from code 0 (unassigned)
         unsigned long long p = pair[i];
         nbr[g] = make_double2((double)(uint32_t)(p & 0xFFFFFFFFULL), (double)(uint32_t)(p >> 32));
         flag[g] = 0;
@@ -1611,7 +1807,8 @@ __global__ void k_seed_commit(const uint32_t* nodes, int64_t nc, const int8_t* s
     if ((threadIdx.x & 31) == 0 && z) atomicAdd((unsigned long long*)zeros, (unsigned long long)z);
 }
 void launch_seed_commit(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* nodes, int64_t nc, cudaStream_t s) {
-    k_seed_commit<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, sb.slab, sb.pair, b.lab, b.nbr, b.flag, sb.scal + 7);
+    k_seed_commit<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, sb.slab, sb.pair, b.lab, b.nbr, b.flag, sb.scal + 7,
+                                                     b.lab2);
 }
 
 // ------------------------------------------------------------ after stream

@@ -41,7 +41,21 @@ struct ChunkBufs {
     long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0,
                         //     6 first mis-speculated tie
     const uint32_t* hub_keys;   // kHubSlots table or nullptr (no hubs)
+    uint32_t* lab2;             // 2-bit mirror of lab (code = label + 1), L2-resident gathers
 };
+
+// Propagation blocking for the round-1 counts: edges emit (node, label code)
+// records binned by node-id range (coalesced writes through a per-CTA counting
+// sort), then the records are applied bin by bin so each bin's counter slice
+// stays in L2.  kMaxBins bins of 2^shift node ids.
+constexpr int kMaxBins = 256;
+struct BinBufs {
+    uint32_t* recs;          // >= 2 * edges of the chunk
+    unsigned int* bin_count; // kMaxBins + 1
+    unsigned int* bin_cur;   // kMaxBins
+    int shift, nbins;
+};
+void launch_count_init_binned(const uint2* e, int64_t m, const ChunkBufs& b, const BinBufs& bb, cudaStream_t s);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;

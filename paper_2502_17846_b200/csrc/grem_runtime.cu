@@ -107,6 +107,8 @@ struct grem_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // per node
     DBuf<int8_t> lab{"lab"};
+    DBuf<uint32_t> lab2{"lab2"}, bin_recs{"bin_recs"};
+    DBuf<unsigned int> bin_count{"bin_count"}, bin_cur{"bin_cur"};
     DBuf<uint8_t> tl{"tl"}, flag{"flag"};
     DBuf<unsigned long long> cnt{"cnt"};
     DBuf<double2> nbr{"nbr"};
@@ -211,6 +213,7 @@ void prof_collect(grem_ctx* c) {
 
 void ensure_nodes(grem_ctx* c, int64_t n) {
     c->lab.ensure(n, c->s);
+    c->lab2.ensure(n / 16 + 2, c->s);
     c->tl.ensure(n, c->s);
     c->flag.ensure(n, c->s);
     c->cnt.ensure(n, c->s);
@@ -293,6 +296,7 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.sizes = c->d_sizes;
     b.scal = c->d_scal;
     b.hub_keys = c->hubs_on ? c->hub_table.p : nullptr;
+    b.lab2 = c->lab2.p;
     return b;
 }
 
@@ -486,7 +490,25 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     cudaStream_t s = c->s;
     ChunkBufs b = chunk_bufs(c);
     CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, s));
-    { PhaseScope ps(c, PH_COUNT); launch_count_init(e, mc, b, s); }
+    {
+        PhaseScope ps(c, PH_COUNT);
+        // propagation blocking when the per-node counters do not fit in L2
+        const char* nb_env = getenv("GREM_NO_BINNING");
+        const char* fb_env = getenv("GREM_FORCE_BINNING");   // tests: exercise the binned path on small graphs
+        if (!nb_env && (fb_env || (a.n * 9 > (48LL << 20) && mc >= (1 << 20)))) {
+            int shift = 0;
+            while (((a.n + (1LL << shift) - 1) >> shift) > kMaxBins) ++shift;
+            int nbins = (int)((a.n + (1LL << shift) - 1) >> shift);
+            c->bin_recs.ensure(2 * mc + 16, s);
+            c->bin_count.ensure(kMaxBins + 2, s);
+            c->bin_cur.ensure(kMaxBins, s);
+            BinBufs bb{c->bin_recs.p, c->bin_count.p, c->bin_cur.p, shift, nbins};
+            launch_count_init_binned(e, mc, b, bb, s);
+            c->kernels += 4;
+        } else {
+            launch_count_init(e, mc, b, s);
+        }
+    }
     c->stats.count_bytes += 10 * mc;   // 8 B edge read + 2 x 1 B label gather
     { PhaseScope ps(c, PH_SELECT); launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s); }
     c->kernels += 2;
@@ -656,6 +678,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     int64_t nc_cap = a.n < 2 * a.chunk ? a.n : 2 * a.chunk;
     ensure_chunk(c, nc_cap, 0);
     CK(cudaMemsetAsync(c->lab.p, 0xFF, a.n, s));
+    CK(cudaMemsetAsync(c->lab2.p, 0, sizeof(uint32_t) * (a.n / 16 + 2), s));
     CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
     CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
     CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
@@ -787,8 +810,17 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
         d = reinterpret_cast<const uint2*>(edges);
     } else {
         c->edges_owned.ensure(m, c->s);
-        staged_upload(c, c->edges_owned.p, (uint64_t)m * 8,
-                      [&](void* buf, uint64_t off, size_t len) { memcpy(buf, (const char*)edges + off, len); });
+        cudaPointerAttributes at{};
+        bool pinned = cudaPointerGetAttributes(&at, edges) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (pinned) {   // page-locked source: DMA straight into HBM
+            PhaseScope ps(c, PH_INGEST);
+            CK(cudaMemcpyAsync(c->edges_owned.p, edges, (size_t)m * 8, cudaMemcpyHostToDevice, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        } else {        // pageable: two pinned staging buffers, copy engine overlapped with memcpy
+            staged_upload(c, c->edges_owned.p, (uint64_t)m * 8,
+                          [&](void* buf, uint64_t off, size_t len) { memcpy(buf, (const char*)edges + off, len); });
+        }
         d = c->edges_owned.p;
     }
     if (m > 0) {
@@ -1145,7 +1177,11 @@ void grem_destroy(grem_ctx* c) {
     c->pool_all.clear();
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->s);
-    c->lab.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
+    c->lab.release();
+    c->lab2.release();
+    c->bin_recs.release();
+    c->bin_count.release();
+    c->bin_cur.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
     c->rank.release(); c->scratch.release(); c->newid.release();
     c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
     c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();

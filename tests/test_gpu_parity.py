@@ -234,6 +234,28 @@ print("hub path ok")
     assert r.returncode == 0 and "hub path ok" in r.stdout, r.stdout + r.stderr
 
 
+def test_binned_counting_path_is_exact(golden_dir):
+    """Force the propagation-blocking count path (normally for > 5M nodes) and
+    the hub path together on the arxiv shape and the products golden."""
+    import subprocess
+    import sys
+    code = r'''
+import json, os, sys, hashlib
+sys.path.insert(0, os.getcwd())
+from paper_2502_17846_b200 import GremConfig, grem, synth
+gs = json.load(open("tests/golden/golden_shapes.json"))
+for key, name, k in (("arxiv_k8", "arxiv", 8), ("products_k16", "products", 16)):
+    s = synth.SHAPES[name]; e = synth.shape_edges(s)
+    lab, rep = grem.partition_edges(e, s.num_nodes, k, GremConfig(chunk_frac=0.1))
+    assert hashlib.sha256(lab.astype("<i4").tobytes()).hexdigest() == gs[key]["labels_sha256"], key
+print("binned ok")
+'''
+    root = os.path.dirname(golden_dir.rstrip("/")).rsplit("/tests", 1)[0]
+    env = dict(os.environ, GREM_FORCE_BINNING="1", GREM_HUB_MIN_CHUNK="1", GREM_HUB_MIN_DEG="2")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "binned ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_poisoned_buffers_do_not_change_results(golden_dir):
     """GREM_DEBUG_POISON=all fills every new device buffer with 0xA5: a read of
     memory not written in the call would change the labels."""
