@@ -277,3 +277,26 @@ print("poison ok")
     env = dict(os.environ, GREM_DEBUG_POISON="all")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "poison ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_papers100m_k16_golden(golden_dir):
+    """papers100M-shaped 111M nodes / 1.6B edges, k=16, edges generated on the
+    device (bit-identical to the host generator): labels sha256 and report
+    pinned by the C oracle (51 min single-thread run, tests/golden)."""
+    import ctypes
+    import hashlib
+    from paper_2502_17846_b200 import _abi
+    gs = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))["papers100m_k16"]
+    s = synth.SHAPES["papers100m"]
+    L = _abi.lib()
+    ctx = grem.context()
+    ptr = ctypes.c_void_p()
+    assert L.grem_device_alloc(ctx, s.num_edges * 8, ctypes.byref(ptr)) == 0
+    try:
+        assert L.grem_gen_edges_device(ctx, s.num_nodes, s.beta, s.seed, 0, s.num_edges, ptr) == 0
+        lab, rep = grem.partition_edges(None, s.num_nodes, 16, GremConfig(chunk_frac=0.1), on_device_ptr=ptr.value,
+                                        num_edges=s.num_edges)
+    finally:
+        L.grem_device_free(ctx, ptr)
+    assert hashlib.sha256(lab.astype("<i4").tobytes()).hexdigest() == gs["labels_sha256"]
+    assert rep.cut_edges == gs["cut_edges"] and list(rep.partition_sizes) == gs["partition_sizes"]
