@@ -1767,6 +1767,166 @@ void launch_refine_scan(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long
     k_scan_down_plain<RefineMapSrc><<<(unsigned)ntiles, kScanThreads, 0, s>>>(src, nc, b.tile_x, b.x);
 }
 
+// ------------------------------------------- refinement rounds on bitmaps
+// Seed labels are 0/1: the pre-pass labels P and the tentative labels T of a
+// refinement pass are bitmaps (N_c bits, L2-resident), a thread owns one
+// 32-node word, and one round = per-row same/other counts + a fused
+// want/clamp-reduce + top scan + fused x/decision pass.
+constexpr int kRfT = 256;
+constexpr int kRfTile = kRfT * 32;
+
+__device__ __forceinline__ uint32_t bit_of(const uint32_t* __restrict__ bits, uint32_t i) {
+    return (bits[i >> 5] >> (i & 31)) & 1u;
+}
+
+__global__ void k_row_counts_bits(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ row_of,
+                                  int64_t entries, const uint32_t* __restrict__ Pb, const uint32_t* __restrict__ Tb,
+                                  int mode, unsigned long long* __restrict__ pair) {
+    int lane = threadIdx.x & 31;
+    int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < entries; base += stride) {
+        int64_t k = base + lane;
+        bool valid = k < entries;
+        uint32_t row = valid ? row_of[k] : 0xFFFFFFFFu;
+        unsigned long long v = 0;
+        if (valid) {
+            uint32_t w = adj[k];
+            if (mode == 0) {   // seed.py:99-104: lower index -> this pass's label, else pre-pass
+                uint32_t lw = w < row ? bit_of(Tb, w) : bit_of(Pb, w);
+                v = (lw == bit_of(Pb, row)) ? 1ULL : (1ULL << 32);
+            } else {           // grem.py:166-174 estimates against the final labels
+                v = bit_of(Pb, w) == 0 ? 1ULL : (1ULL << 32);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned long long ov = __shfl_up_sync(0xffffffffu, v, off);
+            uint32_t orow = __shfl_up_sync(0xffffffffu, row, off);
+            if (lane >= off && orow == row) v += ov;
+        }
+        uint32_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        bool tail = (lane == 31) || (nrow != row);
+        if (valid && tail && v) atomicAdd(&pair[row], v);
+    }
+}
+
+__device__ __forceinline__ Clamp refine_map(uint32_t want, uint32_t p, long long s, long long cap) {
+    if (!want) return clamp_identity();
+    return p == 0 ? Clamp{-1, s - cap, kInf} : Clamp{1, -kInf, cap};
+}
+
+__global__ void __launch_bounds__(kRfT) k_refine_reduce(const unsigned long long* __restrict__ pair,
+                                                        const uint32_t* __restrict__ Pb, uint32_t* __restrict__ wantb,
+                                                        int64_t nc, long long cap, Clamp* tile_agg) {
+    __shared__ Clamp smem[kRfT / 32];
+    __shared__ Clamp stotal;
+    int64_t w = (int64_t)blockIdx.x * kRfT + threadIdx.x;
+    int64_t base = w * 32;
+    uint32_t P = 0, wb = 0;
+    if (base < nc) {
+        P = Pb[w];
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+            int64_t i = base + j;
+            if (i >= nc) break;
+            unsigned long long pp = pair[i];
+            uint32_t same = (uint32_t)(pp & 0xFFFFFFFFULL), other = (uint32_t)(pp >> 32);
+            if (other > same) wb |= 1u << j;   // move iff it strictly reduces the local cut (seed.py:110-111)
+        }
+        wantb[w] = wb;
+    }
+    Clamp acc = clamp_identity();
+    for (int j = 0; j < 32; ++j) acc = clamp_then(acc, refine_map((wb >> j) & 1u, (P >> j) & 1u, nc, cap));
+    block_excl_scan<kRfT>(acc, smem, &stotal);
+    __syncthreads();
+    if (threadIdx.x == 0) tile_agg[blockIdx.x] = stotal;
+}
+
+__global__ void __launch_bounds__(kRfT) k_refine_down(const uint32_t* __restrict__ Pb, uint32_t* __restrict__ Tb,
+                                                      const uint32_t* __restrict__ wantb, int64_t nc, long long cap,
+                                                      const long long* tile_x, long long* changed, long long* xend) {
+    __shared__ Clamp smem[kRfT / 32];
+    int64_t w = (int64_t)blockIdx.x * kRfT + threadIdx.x;
+    int64_t nwords = (nc + 31) / 32;
+    uint32_t P = 0, wb = 0;
+    if (w < nwords) {
+        P = Pb[w];
+        wb = wantb[w];
+    }
+    Clamp acc = clamp_identity();
+    for (int j = 0; j < 32; ++j) acc = clamp_then(acc, refine_map((wb >> j) & 1u, (P >> j) & 1u, nc, cap));
+    Clamp pre = block_excl_scan<kRfT>(acc, smem, nullptr);
+    long long x = clamp_apply(pre, tile_x[blockIdx.x]);
+    uint32_t Tn = P;
+    for (int j = 0; j < 32; ++j) {
+        uint32_t want = (wb >> j) & 1u, p = (P >> j) & 1u;
+        if (want) {   // receiving side must have room (seed.py:110)
+            bool room = p == 0 ? (x > nc - cap) : (x < cap);
+            if (room) Tn ^= 1u << j;
+        }
+        x = clamp_apply(refine_map(want, p, nc, cap), x);
+    }
+    int ch = 0;
+    if (w < nwords) {
+        ch = __popc(Tn ^ Tb[w]);
+        Tb[w] = Tn;
+        if (w == nwords - 1) *xend = x;
+    }
+    for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
+    if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
+}
+
+__global__ void k_pack_bits(const int8_t* __restrict__ lab, int64_t nc, uint32_t* __restrict__ bits, int64_t nwords) {
+    GRID_STRIDE(w, nwords) {
+        uint32_t b = 0;
+        for (int j = 0; j < 32; ++j) {
+            int64_t i = w * 32 + j;
+            if (i < nc && lab[i] == 1) b |= 1u << j;
+        }
+        bits[w] = b;
+    }
+}
+__global__ void k_unpack_bits(const uint32_t* __restrict__ bits, int64_t nc, int8_t* __restrict__ lab) {
+    GRID_STRIDE(i, nc) lab[i] = (int8_t)((bits[i >> 5] >> (i & 31)) & 1u);
+}
+__global__ void k_xor_popc(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t nwords,
+                           long long* out) {
+    int d = 0;
+    GRID_STRIDE(w, nwords) d += __popc(a[w] ^ b[w]);
+    for (int off = 16; off; off >>= 1) d += __shfl_down_sync(0xffffffffu, d, off);
+    if ((threadIdx.x & 31) == 0 && d) atomicAdd((unsigned long long*)out, (unsigned long long)d);
+}
+
+void launch_pack_bits(const int8_t* lab, int64_t nc, uint32_t* bits, cudaStream_t s) {
+    int64_t nw = (nc + 31) / 32;
+    k_pack_bits<<<grid_for(nw, 256), 256, 0, s>>>(lab, nc, bits, nw);
+}
+void launch_unpack_bits(const uint32_t* bits, int64_t nc, int8_t* lab, cudaStream_t s) {
+    k_unpack_bits<<<grid_for(nc, 256), 256, 0, s>>>(bits, nc, lab);
+}
+void launch_xor_popc(const uint32_t* a, const uint32_t* b, int64_t nc, long long* out, cudaStream_t s) {
+    int64_t nw = (nc + 31) / 32;
+    k_xor_popc<<<grid_for(nw, 256), 256, 0, s>>>(a, b, nw, out);
+}
+void launch_row_counts_bits(const SeedBufs& sb, const uint32_t* Pb, const uint32_t* Tb, int mode, int64_t entries,
+                            int64_t nc, cudaStream_t s) {
+    cudaMemsetAsync(sb.pair, 0, sizeof(unsigned long long) * nc, s);
+    if (entries > 0)
+        k_row_counts_bits<<<grid_for(entries, 256, 16), 256, 0, s>>>(sb.adj, sb.row_of, entries, Pb, Tb, mode,
+                                                                    sb.pair);
+}
+// one refinement round after the row counts: want bits + exact sizes chain +
+// decisions; x at pass start in sb.scal[6], changed -> sb.scal[5], x at the
+// end of the pass -> sb.scal[9]
+void launch_refine_round(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* Pb, uint32_t* Tb, uint32_t* wantb,
+                         int64_t nc, long long cap, cudaStream_t s) {
+    int64_t nwords = (nc + 31) / 32;
+    int64_t ntiles = (nwords + kRfT - 1) / kRfT;
+    k_refine_reduce<<<(unsigned)ntiles, kRfT, 0, s>>>(sb.pair, Pb, wantb, nc, cap, b.tile_agg);
+    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, sb.scal + 6, b.tile_x);
+    k_refine_down<<<(unsigned)ntiles, kRfT, 0, s>>>(Pb, Tb, wantb, nc, cap, b.tile_x, sb.scal + 5, sb.scal + 9);
+}
+
 // x at pass start = number of label-0 chunk nodes, passed via scal[6] (host)
 __global__ void k_refine_decide(const uint8_t* want, const int8_t* pre, const int32_t* x, int64_t nc, long long cap,
                                 int8_t* tent, long long* changed) {

@@ -163,6 +163,14 @@ void launch_row_counts(const SeedBufs& sb, const int8_t* cur, const int8_t* pre,
                        int64_t nc, cudaStream_t s);
 void launch_refine_scan(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_refine_decide(const SeedBufs& sb, const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
+// refinement on bitmaps (preferred path)
+void launch_pack_bits(const int8_t* lab, int64_t nc, uint32_t* bits, cudaStream_t s);
+void launch_unpack_bits(const uint32_t* bits, int64_t nc, int8_t* lab, cudaStream_t s);
+void launch_xor_popc(const uint32_t* a, const uint32_t* b, int64_t nc, long long* out, cudaStream_t s);
+void launch_row_counts_bits(const SeedBufs& sb, const uint32_t* Pb, const uint32_t* Tb, int mode, int64_t entries,
+                            int64_t nc, cudaStream_t s);
+void launch_refine_round(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* Pb, uint32_t* Tb, uint32_t* wantb,
+                         int64_t nc, long long cap, cudaStream_t s);
 void launch_seed_commit(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* nodes, int64_t nc,
                         cudaStream_t s);
 

@@ -126,6 +126,7 @@ struct grem_ctx {
     DBuf<unsigned long long> ckey{"ckey"}, rkeys{"rkeys"}, rkeys2{"rkeys2"}, cand{"cand"}, cand2{"cand2"}, pair{"pair"};
     DBuf<int8_t> slab{"slab"}, slab2{"slab2"};
     DBuf<int64_t> fdeg{"fdeg"}, cum{"cum"};
+    DBuf<uint32_t> bitsP{"bitsP"}, bitsT{"bitsT"}, bitsW{"bitsW"};
     // hubs
     DBuf<uint32_t> hub_table{"hub_table"}, hub_ids{"hub_ids"};
     DBuf<unsigned long long> hub_k1{"hub_k1"}, hub_k2{"hub_k2"};
@@ -442,40 +443,48 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         launch_seed_finalize(sb, nc, s);
         c->kernels += 1;
         // ---- boundary refinement passes (seed.py:96-116): rounds to a
-        // fixpoint with the exact sizes scan (moves are clamps, no ties)
+        // fixpoint with the exact sizes scan (moves are clamps, no ties), on
+        // 1-bit label maps
+        int64_t nwords = (nc + 31) / 32;
+        c->bitsP.ensure(nwords + 8, s);
+        c->bitsT.ensure(nwords + 8, s);
+        c->bitsW.ensure(nwords + 8, s);
+        uint32_t* Pb = c->bitsP.p;
+        uint32_t* Tb = c->bitsT.p;
+        launch_pack_bits(sb.slab, nc, Pb, s);
         long long xstart = target;
-        SeedBufs cur = sb;   // cur.slab = pre-pass labels P, cur.slab2 = tentative T
         for (int pass = 0; pass < a.seed_passes; ++pass) {
-            CK(cudaMemcpyAsync(cur.slab2, cur.slab, nc, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(Tb, Pb, sizeof(uint32_t) * nwords, cudaMemcpyDeviceToDevice, s));
             scal_write(c, c->d_sscal + 6, &xstart, 1);
             for (int round = 0;; ++round) {
-                launch_row_counts(cur, cur.slab2, cur.slab, 0, entries, nc, s);
-                launch_refine_scan(cur, b, nc, a.cap, s);
+                launch_row_counts_bits(sb, Pb, Tb, 0, entries, nc, s);
                 CK(cudaMemsetAsync(c->d_sscal + 5, 0, sizeof(long long), s));
-                launch_refine_decide(cur, b, nc, a.cap, s);
-                c->kernels += 6;
+                launch_refine_round(sb, b, Pb, Tb, c->bitsW.p, nc, a.cap, s);
+                c->kernels += 4;
                 scal_read(c, c->d_sscal + 5, 1);
                 if (c->h_pin[0] == 0) break;
                 if (round > nc + 2) fail(GREM_E_FORMAT, "internal: refinement rounds did not converge");
             }
             CK(cudaMemsetAsync(c->d_sscal + 7, 0, sizeof(long long), s));
-            k_count_diff<<<148 * 4, 256, 0, s>>>(cur.slab, cur.slab2, nc, c->d_sscal + 7);
+            launch_xor_popc(Pb, Tb, nc, c->d_sscal + 7, s);
             c->kernels += 1;
-            scal_read(c, c->d_sscal + 7, 1);
+            scal_read(c, c->d_sscal + 7, 3);
             if (c->h_pin[0] == 0) break;   // "if not moved: break"
-            CK(cudaMemcpyAsync(&c->h_pin[0], c->x.p + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            int32_t xe32;
-            memcpy(&xe32, &c->h_pin[0], sizeof(int32_t));
-            xstart = xe32;
-            int8_t* t = cur.slab;
-            cur.slab = cur.slab2;
-            cur.slab2 = t;
+            xstart = c->h_pin[2];          // sscal[9]: x at the end of the pass
+            std::swap(Pb, Tb);
         }
-        sb = cur;
+        launch_unpack_bits(Pb, nc, sb.slab, s);
+        c->kernels += 2;
+    }
+    {
+        // estimates against the final seed labels (bitmap gathers)
+        int64_t nwords = (nc + 31) / 32;
+        c->bitsP.ensure(nwords + 8, s);
+        launch_pack_bits(c->slab.p, nc, c->bitsP.p, s);
+        launch_row_counts_bits(sb, c->bitsP.p, c->bitsP.p, 1, entries, nc, s);
+        sb.slab = c->slab.p;
     }
     // ---- _seed_chunk (grem.py:158-174): labels, sizes recount, estimates
-    launch_row_counts(sb, sb.slab, sb.slab, 1, entries, nc, s);
     CK(cudaMemsetAsync(c->d_sscal + 7, 0, sizeof(long long), s));
     launch_seed_commit(sb, b, c->nodes.p, nc, s);
     c->kernels += 2;
