@@ -2027,15 +2027,18 @@ __global__ void k_cut(const uint2* __restrict__ e, int64_t m, const int32_t* __r
     }
 }
 __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long long* sizes, int64_t cap,
-                       int* mx) {
+                       int* mx, int* neg) {
     extern __shared__ unsigned long long sh[];
     int64_t nb = cap < 1024 ? cap : 1024;
     for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) sh[j] = 0;
     __syncthreads();
-    int lm = -1;
+    int lm = -1, anyneg = 0;
     GRID_STRIDE(i, n) {
         int l = lab[i];
-        if (l < 0) continue;
+        if (l < 0) {
+            anyneg = 1;
+            continue;
+        }
         lm = l > lm ? l : lm;
         if (l < nb) atomicAdd(&sh[l], 1ULL);
         else if (l < cap) atomicAdd(&sizes[l], 1ULL);
@@ -2045,15 +2048,17 @@ __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long
         lm = o > lm ? o : lm;
     }
     if ((threadIdx.x & 31) == 0 && lm >= 0) atomicMax(mx, lm);
+    if (anyneg) atomicOr(neg, 4);   // some node is unlabeled (allowed unless it is an endpoint)
     __syncthreads();
     for (int64_t j = threadIdx.x; j < nb; j += blockDim.x)
         if (sh[j]) atomicAdd(&sizes[j], sh[j]);
 }
 void launch_count_cuts(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* d_cut,
                        unsigned long long* d_sizes, int64_t sizes_cap, int* d_max, int* d_neg, cudaStream_t s) {
-    if (m > 0) k_cut<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, lab, d_cut, d_neg);
+    if (m > 0 && d_cut) k_cut<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, lab, d_cut, d_neg);
     int64_t nb = sizes_cap < 1024 ? sizes_cap : 1024;
-    k_hist<<<grid_for(n, 256, 4), 256, nb * sizeof(unsigned long long), s>>>(lab, n, d_sizes, sizes_cap, d_max);
+    k_hist<<<grid_for(n, 256, 4), 256, nb * sizeof(unsigned long long), s>>>(lab, n, d_sizes, sizes_cap, d_max,
+                                                                            d_neg);
 }
 
 __global__ void k_max_id(const uint2* __restrict__ e, int64_t m, uint32_t* mx) {
@@ -2070,6 +2075,126 @@ void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_
 }
 
 // --------------------------------------------------------------- recursion
+
+// ------------------------------------------------ succinct side bitmaps
+// After a bisection every node is 0 or 1: side-1 bitmap (n bits) + exclusive
+// per-word prefix of popcounts.  Dense id of node g inside its side (rank
+// among ascending members, grem.py:265-266) = rank1(g) or g - rank1(g);
+// both gathers hit the L2-resident 2 x n/8 bytes instead of an n x 4 B table.
+__global__ void k_side_bits(const int8_t* __restrict__ lab, int64_t n, uint32_t* __restrict__ bits,
+                            uint32_t* __restrict__ wpop, int64_t nwords) {
+    GRID_STRIDE(w, nwords) {
+        uint32_t b = 0;
+        int64_t base = w * 32;
+        if (base + 32 <= n) {
+            const uint4* p4 = reinterpret_cast<const uint4*>(lab + base);
+            uint4 v0 = p4[0], v1 = p4[1];
+            uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (((words[q] >> (8 * k)) & 0xFF) == 1) b |= 1u << (q * 4 + k);
+        } else {
+            for (int j = 0; j < 32; ++j)
+                if (base + j < n && lab[base + j] == 1) b |= 1u << j;
+        }
+        bits[w] = b;
+        wpop[w] = __popc(b);
+    }
+}
+__device__ __forceinline__ uint32_t side_rank1(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ pre,
+                                               uint32_t g) {
+    uint32_t w = g >> 5;
+    return pre[w] + __popc(bits[w] & ((1u << (g & 31)) - 1u));
+}
+__device__ __forceinline__ uint32_t side_newid(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ pre,
+                                               uint32_t g, int side) {
+    uint32_t r1 = side_rank1(bits, pre, g);
+    return side ? r1 : g - r1;
+}
+struct SideBitPred {
+    const uint32_t* bits;
+    uint32_t side;
+    __device__ __forceinline__ bool operator()(const uint2& ed) const {
+        return ((bits[ed.x >> 5] >> (ed.x & 31)) & 1u) == side && ((bits[ed.y >> 5] >> (ed.y & 31)) & 1u) == side;
+    }
+};
+size_t extract_bits_temp_bytes(int64_t m) {
+    size_t bytes = 0;
+    cub::DeviceSelect::If(nullptr, bytes, (const uint2*)nullptr, (uint2*)nullptr, (long long*)nullptr, (int)m,
+                          SideBitPred{nullptr, 0});
+    return bytes;
+}
+__global__ void k_remap_bits(uint2* e, const long long* cnt, const uint32_t* __restrict__ bits,
+                             const uint32_t* __restrict__ pre, int side) {
+    int64_t m = *cnt;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        e[i] = make_uint2(side_newid(bits, pre, ed.x, side), side_newid(bits, pre, ed.y, side));
+    }
+}
+__global__ void k_sub_orig_bits(const int8_t* __restrict__ lab, int64_t n, int side, const uint32_t* __restrict__ bits,
+                                const uint32_t* __restrict__ pre, const int32_t* __restrict__ orig,
+                                int32_t* __restrict__ sub) {
+    GRID_STRIDE(i, n) if (lab[i] == side) sub[side_newid(bits, pre, (uint32_t)i, side)] = orig[i];
+}
+void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wpop, uint32_t* pre, void* temp,
+                      size_t temp_bytes, cudaStream_t s) {
+    int64_t nw = (n + 31) / 32;
+    k_side_bits<<<grid_for(nw, 256), 256, 0, s>>>(lab, n, bits, wpop, nw);
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, wpop, pre, (int)(nw + 1), s);
+}
+void launch_extract_bits(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int side, uint2* out,
+                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s) {
+    cub::DeviceSelect::If(temp, temp_bytes, e, out, d_count, (int)m, SideBitPred{bits, (uint32_t)side}, s);
+    k_remap_bits<<<grid_for(m, 256, 8), 256, 0, s>>>(out, d_count, bits, pre, side);
+}
+void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t* bits, const uint32_t* pre,
+                          const int32_t* orig, int32_t* sub, cudaStream_t s) {
+    k_sub_orig_bits<<<grid_for(n, 256), 256, 0, s>>>(lab, n, side, bits, pre, orig, sub);
+}
+
+// count_cuts with bit-packed labels: 2^lb bits per label (lb <= 5)
+__global__ void k_pack_labels(const int32_t* __restrict__ lab, int64_t n, int lb, uint32_t* __restrict__ out,
+                              int64_t nwords, int* neg) {
+    int per = 32 >> lb, width = 1 << lb;
+    int ng = 0;
+    GRID_STRIDE(w, nwords) {
+        uint32_t v = 0;
+        for (int j = 0; j < per; ++j) {
+            int64_t i = w * per + j;
+            if (i < n) {
+                int32_t l = lab[i];
+                ng |= l < 0;
+                v |= ((uint32_t)l & (width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1))) << (j * width);
+            }
+        }
+        out[w] = v;
+    }
+    if (ng) atomicOr(neg, 2);
+}
+__global__ void k_cut_packed(const uint2* __restrict__ e, int64_t m, const uint32_t* __restrict__ pl, int lb,
+                             unsigned long long* cut) {
+    int width = 1 << lb, lpw = 5 - lb;
+    uint32_t mask = width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1);
+    unsigned long long c = 0;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        uint32_t a = (pl[ed.x >> lpw] >> ((ed.x & ((1u << lpw) - 1)) << lb)) & mask;
+        uint32_t b = (pl[ed.y >> lpw] >> ((ed.y & ((1u << lpw) - 1)) << lb)) & mask;
+        c += (a != b);
+    }
+    for (int off = 16; off; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cut, c);
+}
+void launch_count_cuts_packed(const uint2* e, int64_t m, const int32_t* lab, int64_t n, int lb, uint32_t* packed,
+                              unsigned long long* d_cut, int* d_neg, cudaStream_t s) {
+    int per = 32 >> lb;
+    int64_t nw = (n + per - 1) / per;
+    k_pack_labels<<<grid_for(nw, 256), 256, 0, s>>>(lab, n, lb, packed, nw, d_neg);
+    if (m > 0) k_cut_packed<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, packed, lb, d_cut);
+}
 
 __global__ void k_side_flags(const int8_t* lab, int64_t n, int side, int32_t* f) {
     GRID_STRIDE(i, n) f[i] = lab[i] == side ? 1 : 0;

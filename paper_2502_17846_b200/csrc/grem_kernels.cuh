@@ -194,6 +194,17 @@ void launch_sub_orig(const int8_t* lab, int64_t n, int side, const int32_t* newi
 void launch_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_t leaf_base, int32_t* final_lab,
                        cudaStream_t s);
 void launch_iota(int32_t* a, int64_t n, cudaStream_t s);
+// succinct side maps for the recursion (preferred path)
+void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wpop, uint32_t* pre, void* temp,
+                      size_t temp_bytes, cudaStream_t s);
+size_t extract_bits_temp_bytes(int64_t m);
+void launch_extract_bits(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int side, uint2* out,
+                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t* bits, const uint32_t* pre,
+                          const int32_t* orig, int32_t* sub, cudaStream_t s);
+// cut count with labels packed to 2^lb bits (d_neg gets bit 1 on negative labels)
+void launch_count_cuts_packed(const uint2* e, int64_t m, const int32_t* lab, int64_t n, int lb, uint32_t* packed,
+                              unsigned long long* d_cut, int* d_neg, cudaStream_t s);
 
 // generic CUB helpers
 size_t scan_temp_bytes(int64_t n);

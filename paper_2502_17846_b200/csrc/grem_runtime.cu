@@ -146,6 +146,7 @@ struct grem_ctx {
     // count_cuts
     DBuf<unsigned long long> cc_sizes;
     DBuf<int32_t> lab32;
+    DBuf<uint32_t> packed_lab{"packed_lab"}, side_bits{"side_bits"}, side_pop{"side_pop"}, side_pre{"side_pre"};
     // recursion arena: per-level induced-subgraph buffers (reused across calls)
     DBuf<uint2> rec_e[40];
     DBuf<int32_t> rec_o[40];
@@ -755,15 +756,33 @@ void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, 
     int* d_max = (int*)(d + 1);
     int* d_neg = d_max + 1;
     CK(cudaMemsetAsync(d_max, 0xFF, sizeof(int), s));   // -1
-    { PhaseScope ps(c, PH_CUTS); launch_count_cuts(e, m, lab, n, d, d + 2, cap, d_max, d_neg, s); }
-    c->kernels += 2;
+    PhaseScope ps(c, PH_CUTS);
+    // sizes + max label first; the cut pass then gathers labels packed to the
+    // narrowest power-of-two width (1 bit for a bisection, 4 for k=16)
+    launch_count_cuts(e, m, lab, n, nullptr, d + 2, cap, d_max, d_neg, s);
+    c->kernels += 1;
     std::vector<unsigned long long> h(cap + 2);
-    CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * (cap + 2), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     int mx, neg;
     memcpy(&mx, &h[1], sizeof(int));
     memcpy(&neg, ((char*)&h[1]) + sizeof(int), sizeof(int));
-    if (neg) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+    if (neg & 4) {   // unlabeled nodes exist: exact int32 pass also checks endpoints (grem.py:238-239)
+        launch_count_cuts(e, m, lab, n, d, nullptr, 0, d_max, d_neg, s);
+        c->kernels += 1;
+    } else if (m > 0) {
+        int bits = 1;
+        while (bits < 32 && (uint64_t)mx >= (1ULL << bits)) bits *= 2;
+        int lb = 0;
+        while ((1 << lb) < bits) ++lb;
+        c->packed_lab.ensure(n / (32 >> lb) + 2, s);
+        launch_count_cuts_packed(e, m, lab, n, lb, c->packed_lab.p, d, d_neg, s);
+        c->kernels += 2;
+    }
+    CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * (cap + 2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    memcpy(&neg, ((char*)&h[1]) + sizeof(int), sizeof(int));
+    if (neg & 1) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
     int64_t np = mx >= 0 ? (int64_t)mx + 1 : 1;
     if (rep) {
         rep->total_edges = m;
@@ -1019,29 +1038,36 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     uint2* sub_e = c->rec_e[level].p;
     int32_t* sub_o = c->rec_o[level].p;
     int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
-    ensure_temp(c, extract_temp_bytes(m > 0 ? m : 1));
+    ensure_temp(c, extract_bits_temp_bytes(m > 0 ? m : 1));
+    int64_t nw = (n + 31) / 32;
+    c->side_bits.ensure(nw + 2, s);
+    c->side_pop.ensure(nw + 2, s);
+    c->side_pre.ensure(nw + 2, s);
+    ensure_temp(c, scan_temp_bytes(nw + 2));
+    {
+        PhaseScope ps(c, PH_EXTRACT);
+        CK(cudaMemsetAsync(c->side_pop.p + nw, 0, sizeof(uint32_t), s));
+        launch_side_bits(c->lab.p, n, c->side_bits.p, c->side_pop.p, c->side_pre.p, c->temp.p, c->temp.cap, s);
+        CK(cudaMemcpyAsync(&c->h_pin[0], c->side_pre.p + nw, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        c->kernels += 2;
+    }
+    uint32_t ones;
+    memcpy(&ones, &c->h_pin[0], sizeof(uint32_t));
+    n_off[1] = n - (int64_t)ones;
+    n_off[2] = n;
     for (int side = 0; side < 2; ++side) {
         PhaseScope ps(c, PH_EXTRACT);
-        int32_t* flags = c->scratch.p;
-        launch_side_flags(c->lab.p, n, side, flags, s);
-        exclusive_sum_i32(flags, c->newid.p, n, c->temp.p, c->temp.cap, s);
-        CK(cudaMemcpyAsync(&c->h_pin[0], c->newid.p + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(((int32_t*)&c->h_pin[0]) + 1, flags + n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        int32_t v[2];
-        memcpy(v, &c->h_pin[0], sizeof(v));
-        int64_t k = (int64_t)v[0] + v[1];
-        launch_sub_orig(c->lab.p, n, side, c->newid.p, orig, sub_o + n_off[side], s);
+        launch_sub_orig_bits(c->lab.p, n, side, c->side_bits.p, c->side_pre.p, orig, sub_o + n_off[side], s);
         int64_t kept = 0;
         if (m > 0) {
-            launch_extract(e, m, c->lab.p, side, c->newid.p, sub_e + e_off[side], c->d_scal + 7, c->temp.p,
-                           c->temp.cap, s);
+            launch_extract_bits(e, m, c->side_bits.p, c->side_pre.p, side, sub_e + e_off[side], c->d_scal + 7,
+                                c->temp.p, c->temp.cap, s);
             scal_read(c, c->d_scal + 7, 1);
             kept = c->h_pin[0];
         }
-        c->kernels += 5;
+        c->kernels += 3;
         e_off[side + 1] = e_off[side] + kept;
-        n_off[side + 1] = n_off[side] + k;
     }
     c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
     auto side_call = [&](grem_ctx* cc, int side) {
@@ -1200,6 +1226,10 @@ void grem_destroy(grem_ctx* c) {
     c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
     c->fdeg.release(); c->cum.release(); c->temp.release(); c->edges_owned.release(); c->cc_sizes.release();
     c->lab32.release();
+    c->packed_lab.release();
+    c->side_bits.release();
+    c->side_pop.release();
+    c->side_pre.release();
     for (int l = 0; l < 40; ++l) {
         c->rec_e[l].release();
         c->rec_o[l].release();
