@@ -15,8 +15,11 @@ events on the library's stream (grem_stats.ms_total); max over ranks.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload papers100m|friendster|products|arxiv|tiny] [--k K]
 
-N > 1: one process per GPU (torchrun); every rank partitions its own replica
-("scaling": "weak", replicas — see DESIGN.md §7 for the sharded design).
+N > 1: one process per GPU (torchrun), ONE partition of the same graph
+sharded across the ranks ("scaling": "strong"): recursion subtrees are split
+between GPUs in proportion to their edges (paper_2502_17846_b200/shard.py),
+labels merged with one NCCL all-reduce, count_cuts on the merged labels.
+`--replicas` instead has every rank partition its own copy ("weak").
 """
 
 from __future__ import annotations
@@ -107,6 +110,7 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas (weak scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -147,9 +151,31 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    sharded = world > 1 and not args.replicas
+    if sharded:
+        from paper_2502_17846_b200 import shard
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
     def step_device():
-        lab, rep = grem.partition_edges(None, n, k, cfg, on_device_ptr=dptr.value, num_edges=E)
-        return lab, rep, grem.last_stats()
+        if not sharded:
+            lab, rep = grem.partition_edges(None, n, k, cfg, on_device_ptr=dptr.value, num_edges=E)
+            return lab, rep, grem.last_stats()
+        # events on torch's stream bracket the whole step: the library call
+        # (its own stream, synchronised inside), the NCCL merge and count_cuts
+        torch.cuda.synchronize()
+        ev0.record()
+        labels = torch.empty(n, dtype=torch.int32, device="cuda")
+        shard.partition_shard(dptr.value, E, n, k, cfg, rank, world, labels)
+        st = grem.last_stats()
+        st["_phases"] = grem.phase_times()
+        shard.merge_labels(labels)
+        torch.cuda.synchronize()
+        rep = shard.count_cuts_device(dptr.value, E, n, labels, k)
+        ev1.record()
+        torch.cuda.synchronize()
+        st["ms_total"] = ev0.elapsed_time(ev1)
+        st["kernels"] += 2    # the count_cuts launches (hist + cut)
+        return labels, rep, st
 
     for _ in range(args.warmup):
         lab, rep, st = step_device()
@@ -165,7 +191,7 @@ def main():
             lab, rep, st = step_device()
             dev_ms.append(st["ms_total"])
             kernels += st["kernels"]
-            for name, (ms, cnt) in grem.phase_times().items():
+            for name, (ms, cnt) in (st.pop("_phases", None) or grem.phase_times()).items():
                 a = phases.setdefault(name, [0.0, 0])
                 a[0] += ms
                 a[1] += cnt
@@ -177,9 +203,12 @@ def main():
         t = torch.tensor([ms_step], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    value = world * E / (ms_step / 1e3)
+    units = E if sharded else world * E
+    value = units / (ms_step / 1e3)
 
     import hashlib
+    if sharded:
+        lab = lab.cpu().numpy()
     labels_sha = hashlib.sha256(np.asarray(lab, dtype="<i4").tobytes()).hexdigest()
 
     # e2e: public API from pinned host memory, labels read back every step
@@ -188,13 +217,26 @@ def main():
         host = torch.empty((E, 2), dtype=torch.int32, pin_memory=True)
         assert L.grem_memcpy_d2h(ctx, ctypes.c_void_p(host.data_ptr()), dptr, E * 8) == 0
         hv = host.numpy().view(np.uint32)
-        grem.partition_edges(hv, n, k, cfg)        # warm the host path
+
+        def e2e_step():
+            if not sharded:
+                lab2, _ = grem.partition_edges(hv, n, k, cfg)
+                return lab2, grem.last_stats()["ms_total"]
+            # every rank stages the edge list from pinned host memory into its
+            # own HBM, then the sharded partition; labels read back to the host
+            t_0 = time.perf_counter()
+            assert L.grem_memcpy_h2d(ctx, dptr, ctypes.c_void_p(host.data_ptr()), E * 8) == 0
+            labels, _ = shard.partition_distributed(dptr.value, E, n, k, cfg)
+            lab2 = labels.cpu().numpy()
+            return lab2, (time.perf_counter() - t_0) * 1e3
+
+        e2e_step()        # warm the host path
         barrier()
         e_ms = []
         te = time.perf_counter()
         for _ in range(max(1, min(args.steps, 2))):
-            lab2, rep2 = grem.partition_edges(hv, n, k, cfg)
-            e_ms.append(grem.last_stats()["ms_total"])
+            lab2, ms_ = e2e_step()
+            e_ms.append(ms_)
         barrier()
         e_wall = (time.perf_counter() - te) * 1e3 / len(e_ms)
         assert np.array_equal(lab2, lab), "e2e labels differ from the device-resident run"
@@ -204,7 +246,7 @@ def main():
             t = torch.tensor([e_step], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_step = float(t.item())
-        e2e = {"value": world * E / (e_step / 1e3), "unit": "edges/s", "ms_per_step": e_step,
+        e2e = {"value": units / (e_step / 1e3), "unit": "edges/s", "ms_per_step": e_step,
                "h2d_bytes_per_step": E * 8, "d2h_bytes_per_step": n * 4}
         del host
 
@@ -235,10 +277,12 @@ def main():
             "metric": "GREM edges/s (partition to k, bit-equal labels/edge-cut)", "value": value,
             "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "wall_ms_per_step": wall_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "u32/f64",
+            "data": "synthetic",
             "config": {"workload": f"{args.workload}-shaped power-law k={k}", "num_nodes": n, "num_edges": E,
                        "k": k, "chunk_frac": 0.1, "capacity_slack": 0.0, "refine": True, "passes": 1,
-                       "seed": "bfs_grow/2", "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "seed": "bfs_grow/2", "parallelism": (f"subtree-sharded x{world}" if sharded else
+                                       f"replicas x{world}" if world > 1 else "single"),
                        "l2": "inputs larger than L2 (edge list %.1f GB)" % (E * 8 / 1e9)},
             "report": {"cut_edges": rep.cut_edges, "cut_fraction": rep.cut_fraction,
                        "balance_ratio": rep.balance_ratio, "labels_sha256": labels_sha},

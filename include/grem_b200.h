@@ -121,6 +121,16 @@ int grem_partition_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, 
                        int edges_on_device, int64_t p, const grem_config* cfg, const grem_hooks* hooks,
                        int32_t* labels_out, grem_report* rep);
 
+/* Multi-GPU subtree sharding of partition(): every rank calls this with the
+ * same edges; the owners of a recursion node are split between its two sides
+ * in proportion to their edge counts (ancestors are computed redundantly and
+ * bit-identically).  labels_out gets this rank's leaves, -1 elsewhere; the
+ * caller merges ranks with an element-wise max (e.g. one NCCL all-reduce) and
+ * runs grem_count_cuts_u32 on the merged labels. */
+int grem_partition_shard_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                             int edges_on_device, int64_t p, const grem_config* cfg, int rank, int world,
+                             int32_t* labels_out);
+
 /* count_cuts (grem.py:227-252).  labels_on_device as for edges. */
 int grem_count_cuts_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
                         int edges_on_device, const int32_t* labels, int labels_on_device,

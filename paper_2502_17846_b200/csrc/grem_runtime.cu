@@ -1005,10 +1005,13 @@ struct PartCtx {
     const grem_config* cfg;
     const grem_hooks* hooks;
     int32_t* final_lab;
+    int shard_rank = 0;   // multi-GPU subtree sharding: this process's rank
 };
 
+// ranks [r0, r1) own this recursion node; a node with several owners is
+// computed redundantly (bit-identical) by each of them
 void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, const int32_t* orig, int64_t p_level,
-             int level, int64_t leaf_base) {
+             int level, int64_t leaf_base, int r0 = 0, int r1 = 1) {
     cudaStream_t s = c->s;
     if (level >= 39) fail(GREM_E_FORMAT, "partition depth exceeds 2^39 parts");
     double capd = std::ceil((1.0 + pc.cfg->capacity_slack) * (double)pc.total_nodes / (double)(1LL << (level + 1)));
@@ -1070,17 +1073,33 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         e_off[side + 1] = e_off[side] + kept;
     }
     c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
+    // split the owning ranks between the sides in proportion to their edges
+    int W = r1 - r0, split = r1;
+    int sr0[2] = {r0, r0}, sr1[2] = {r1, r1};
+    if (W >= 2) {
+        double m0 = (double)(e_off[1] - e_off[0]), m1 = (double)(e_off[2] - e_off[1]);
+        int w0 = (int)std::floor(W * (m0 + 1.0) / (m0 + m1 + 2.0) + 0.5);
+        if (w0 < 1) w0 = 1;
+        if (w0 > W - 1) w0 = W - 1;
+        split = r0 + w0;
+        sr1[0] = split;
+        sr0[1] = split;
+    }
     auto side_call = [&](grem_ctx* cc, int side) {
         int64_t k = n_off[side + 1] - n_off[side];
         if (k == 0) return;   // grem.py:308-309
+        if (pc.shard_rank < sr0[side] || pc.shard_rank >= sr1[side]) return;   // another rank's subtree
         int64_t base = leaf_base + side * (p_level / 2);
         recurse(cc, pc, sub_e + e_off[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
-                level + 1, base);
+                level + 1, base, sr0[side], sr1[side]);
     };
+    (void)split;
     // The two sides are independent problems: side 1 runs concurrently on a
     // child context (own stream + host thread) unless a meter is attached
     // (the reference's residency accounting is sequential) or disabled.
-    bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0);
+    bool mine0 = pc.shard_rank >= sr0[0] && pc.shard_rank < sr1[0];
+    bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
+    bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
     bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
     if (par) {
         cudaEvent_t ready;
@@ -1117,7 +1136,8 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
 }
 
 void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t p, const grem_config* cfg,
-                     const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
+                     const grem_hooks* hooks, int32_t* labels_out, grem_report* rep, int shard_rank = 0,
+                     int shard_world = 1) {
     if (p < 2 || (p & (p - 1)) != 0)
         fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
     validate_cfg(cfg);
@@ -1128,12 +1148,14 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
     int32_t* orig = c->part_orig.p;
     CK(cudaMemsetAsync(fin, 0xFF, sizeof(int32_t) * n, s));
     launch_iota(orig, n, s);
-    PartCtx pc{n, cfg, hooks, fin};
+    PartCtx pc{n, cfg, hooks, fin, shard_rank};
     try {
-        recurse(c, pc, d, m, n, orig, p, 0, 0);
-        count_cuts_dev(c, d, m, fin, n, rep);
-        c->stats.path_bytes += 10 * m;   // final cut pass
-        if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+        recurse(c, pc, d, m, n, orig, p, 0, 0, 0, shard_world);
+        if (shard_world == 1) {
+            count_cuts_dev(c, d, m, fin, n, rep);
+            c->stats.path_bytes += 10 * m;   // final cut pass
+        }
+        if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, s));
         CK(cudaStreamSynchronize(s));
     } catch (...) {
         cudaStreamSynchronize(s);
@@ -1291,6 +1313,17 @@ int grem_partition_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n,
             fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
         const uint2* d = stage_edges(c, edges, m, n, on_device);
         partition_entry(c, d, m, n, p, cfg, hooks, labels_out, rep);
+    });
+}
+
+int grem_partition_shard_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device, int64_t p,
+                             const grem_config* cfg, int rank, int world, int32_t* labels_out) {
+    if (!c || !cfg || world < 1 || rank < 0 || rank >= world) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        if (p < 2 || (p & (p - 1)) != 0)
+            fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
+        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        partition_entry(c, d, m, n, p, cfg, nullptr, labels_out, nullptr, rank, world);
     });
 }
 
