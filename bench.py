@@ -260,7 +260,7 @@ def main():
         achieved = per_step_count_bytes / (cnt_ms / args.steps / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": "k_count_init/k_count_delta (edge pass)", "achieved": achieved,
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                "share_of_step": cnt_ms / sum(v[0] for v in phases.values())}
+                "share_of_step": cnt_ms / sum(v[0] for kk, v in phases.items() if "." not in kk)}
     path_bytes = st.get("path_bytes")
     roof_path = None
     if path_bytes:

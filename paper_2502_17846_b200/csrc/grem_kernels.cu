@@ -1495,6 +1495,57 @@ void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cu
     k_fill_csr<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, rank, cursor, adj, row_of, hub_keys);
 }
 
+// Chunk-0 CSR by sorting (no random scatter): both directions of every edge
+// as (key = row id, value = column id) pairs, one radix sort over the id bits,
+// run-length encoding of the sorted keys -> ascending chunk nodes (= ranks)
+// and row lengths, then a gather of ranks.  Self-loops become (x, x) entries
+// that every consumer skips (w == row); their count per row is subtracted
+// where the reference's degree is used (seed.py:69-75 restart order).
+__global__ void k_seed_pairs(const uint2* __restrict__ e, int64_t m, uint2* __restrict__ keys,
+                             uint2* __restrict__ vals) {
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        keys[i] = ed;
+        vals[i] = make_uint2(ed.y, ed.x);
+    }
+}
+__global__ void k_seed_map(const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals, int64_t entries,
+                           const int32_t* __restrict__ rank, uint32_t* row_of, uint32_t* adj,
+                           int32_t* __restrict__ selfc) {
+    GRID_STRIDE(j, entries) {
+        uint32_t r = (uint32_t)rank[skeys[j]], w = (uint32_t)rank[svals[j]];
+        row_of[j] = r;
+        adj[j] = w;
+        if (r == w) atomicAdd(&selfc[r], 1);
+    }
+}
+size_t seed_csr_temp_bytes(int64_t entries) {
+    size_t a = 0, b = 0;
+    cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)entries);
+    cub::DeviceRunLengthEncode::Encode(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                       (long long*)nullptr, (int)entries);
+    return a > b ? a : b;
+}
+// keysA/valsA, keysB/valsB: two entries-sized buffer pairs (A = row_of/adj of
+// the SeedBufs); the sorted CSR ends in row_of/adj (a swap is reported).
+// nodes <- ascending chunk node ids, counts <- row lengths, nruns -> *d_nruns.
+void launch_seed_sort(const uint2* e, int64_t m, uint32_t* keysA, uint32_t* valsA, uint32_t* keysB, uint32_t* valsB,
+                      int end_bit, uint32_t* nodes, int32_t* counts, long long* d_nruns, void* temp,
+                      size_t temp_bytes, bool* sorted_in_b, cudaStream_t s) {
+    int64_t entries = 2 * m;
+    k_seed_pairs<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, reinterpret_cast<uint2*>(keysA),
+                                                      reinterpret_cast<uint2*>(valsA));
+    cub::DoubleBuffer<uint32_t> dk(keysA, keysB), dv(valsA, valsB);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk, dv, (int)entries, 0, end_bit, s);
+    *sorted_in_b = dk.Current() == keysB;
+    cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, dk.Current(), nodes, counts, d_nruns, (int)entries, s);
+}
+void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const int32_t* rank,
+                     uint32_t* row_of, uint32_t* adj, int32_t* selfc, cudaStream_t s) {
+    k_seed_map<<<grid_for(entries, 256, 16), 256, 0, s>>>(skeys, svals, entries, rank, row_of, adj, selfc);
+}
+
 // union-find connected components (link larger root under smaller root)
 __device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
     uint32_t p = ((volatile uint32_t*)parent)[x];
@@ -1551,15 +1602,16 @@ void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent,
 
 // restart order of _bfs_grow (seed.py:69-75): a component is entered at its
 // highest-degree, lowest-index node; key = (~degree << 32) | index, min wins.
-__global__ void k_comp_keys(const int32_t* __restrict__ start, const uint32_t* __restrict__ parent, int64_t nc,
-                            unsigned long long* ckey, uint32_t* csize) {
+__global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __restrict__ selfc,
+                            const uint32_t* __restrict__ parent, int64_t nc, unsigned long long* ckey,
+                            uint32_t* csize) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nc; base += stride) {
         int64_t i = base + (threadIdx.x & 31);
         bool valid = i < nc;
         uint32_t r = valid ? parent[i] : 0xFFFFFFFFu;
         if (valid) {
-            uint32_t d = (uint32_t)(start[i + 1] - start[i]);
+            uint32_t d = (uint32_t)(start[i + 1] - start[i] - selfc[i]);
             unsigned long long key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
             if (key < ((volatile unsigned long long*)ckey)[r]) atomicMin(&ckey[r], key);
         }
@@ -1571,7 +1623,7 @@ __global__ void k_comp_keys(const int32_t* __restrict__ start, const uint32_t* _
 void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
     cudaMemsetAsync(sb.ckey, 0xFF, sizeof(unsigned long long) * nc, s);
     cudaMemsetAsync(sb.csize, 0, sizeof(uint32_t) * nc, s);
-    k_comp_keys<<<grid_for(nc, 256), 256, 0, s>>>(sb.start, sb.parent, nc, sb.ckey, sb.csize);
+    k_comp_keys<<<grid_for(nc, 256), 256, 0, s>>>(sb.start, sb.cursor, sb.parent, nc, sb.ckey, sb.csize);
 }
 
 struct RootPred {
@@ -1721,7 +1773,9 @@ __global__ void k_row_counts(const uint32_t* __restrict__ adj, const uint32_t* _
         unsigned long long v = 0;
         if (valid) {
             uint32_t w = adj[k];
-            if (mode == 0) {
+            if (w == row) {
+                v = 0;
+            } else if (mode == 0) {
                 int lw = w < row ? cur[w] : pre[w];
                 v = (lw == pre[row]) ? 1ULL : (1ULL << 32);
             } else {
@@ -1791,7 +1845,9 @@ __global__ void k_row_counts_bits(const uint32_t* __restrict__ adj, const uint32
         unsigned long long v = 0;
         if (valid) {
             uint32_t w = adj[k];
-            if (mode == 0) {   // seed.py:99-104: lower index -> this pass's label, else pre-pass
+            if (w == row) {
+                v = 0;         // self-loop entry: not an adjacency (model.py: loops are skipped)
+            } else if (mode == 0) {   // seed.py:99-104: lower index -> this pass's label, else pre-pass
                 uint32_t lw = w < row ? bit_of(Tb, w) : bit_of(Pb, w);
                 v = (lw == bit_of(Pb, row)) ? 1ULL : (1ULL << 32);
             } else {           // grem.py:166-174 estimates against the final labels
@@ -1844,7 +1900,8 @@ __global__ void __launch_bounds__(kRfT) k_refine_reduce(const unsigned long long
 
 __global__ void __launch_bounds__(kRfT) k_refine_down(const uint32_t* __restrict__ Pb, uint32_t* __restrict__ Tb,
                                                       const uint32_t* __restrict__ wantb, int64_t nc, long long cap,
-                                                      const long long* tile_x, long long* changed, long long* xend) {
+                                                      const long long* tile_x, long long* changed, long long* xend,
+                                                      uint32_t* __restrict__ Db) {
     __shared__ Clamp smem[kRfT / 32];
     int64_t w = (int64_t)blockIdx.x * kRfT + threadIdx.x;
     int64_t nwords = (nc + 31) / 32;
@@ -1868,12 +1925,59 @@ __global__ void __launch_bounds__(kRfT) k_refine_down(const uint32_t* __restrict
     }
     int ch = 0;
     if (w < nwords) {
-        ch = __popc(Tn ^ Tb[w]);
+        uint32_t d = Tn ^ Tb[w];
+        ch = __popc(d);
+        Db[w] = d;
         Tb[w] = Tn;
         if (w == nwords - 1) *xend = x;
     }
     for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
     if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
+}
+
+// Incremental row counts between refinement rounds of one pass: only rows
+// above a node whose tentative label flipped read it (seed.py:99-104), so
+// the flipped nodes' adjacency rows move one count between same and other.
+__global__ void k_refine_list(const uint32_t* __restrict__ Db, int64_t nwords, const int32_t* __restrict__ start,
+                              uint32_t* __restrict__ list, int64_t* __restrict__ deg, long long* count) {
+    GRID_STRIDE(w, nwords) {
+        uint32_t d = Db[w];
+        while (d) {
+            int j = __ffs(d) - 1;
+            d &= d - 1;
+            uint32_t i = (uint32_t)(w * 32 + j);
+            long long idx = (long long)atomicAdd((unsigned long long*)count, 1ULL);
+            list[idx] = i;
+            deg[idx] = start[i + 1] - start[i];
+        }
+    }
+}
+__global__ void k_refine_delta(const uint32_t* __restrict__ list, int64_t cnt, const int64_t* __restrict__ cum,
+                               const int32_t* __restrict__ start, const uint32_t* __restrict__ adj,
+                               const uint32_t* __restrict__ Pb, const uint32_t* __restrict__ Tb,
+                               unsigned long long* __restrict__ pair) {
+    int64_t total = cum[cnt];
+    GRID_STRIDE(k, total) {
+        int64_t lo = 0, hi = cnt - 1;
+        while (lo < hi) {
+            int64_t mid = (lo + hi + 1) >> 1;
+            if (cum[mid] <= k) lo = mid; else hi = mid - 1;
+        }
+        uint32_t w = list[lo];
+        uint32_t row = adj[start[w] + (k - cum[lo])];
+        if (row <= w) continue;   // lower rows read the pre-pass label; self-loop entries are skipped
+        bool same_now = bit_of(Tb, w) == bit_of(Pb, row);
+        atomicAdd(&pair[row], same_now ? 0xFFFFFFFF00000001ULL : 0x00000000FFFFFFFFULL);
+    }
+}
+void launch_refine_delta(const SeedBufs& sb, const uint32_t* Db, int64_t nc, int64_t changed, const uint32_t* Pb,
+                         const uint32_t* Tb, void* temp, size_t temp_bytes, cudaStream_t s) {
+    int64_t nwords = (nc + 31) / 32;
+    cudaMemsetAsync(sb.scal + 12, 0, sizeof(long long), s);
+    cudaMemsetAsync(sb.fdeg + changed, 0, sizeof(int64_t), s);
+    k_refine_list<<<grid_for(nwords, 256), 256, 0, s>>>(Db, nwords, sb.start, sb.frontier, sb.fdeg, sb.scal + 12);
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, sb.fdeg, sb.cum, (int)(changed + 1), s);
+    k_refine_delta<<<num_sms() * 8, 256, 0, s>>>(sb.frontier, changed, sb.cum, sb.start, sb.adj, Pb, Tb, sb.pair);
 }
 
 __global__ void k_pack_bits(const int8_t* __restrict__ lab, int64_t nc, uint32_t* __restrict__ bits, int64_t nwords) {
@@ -1919,12 +2023,12 @@ void launch_row_counts_bits(const SeedBufs& sb, const uint32_t* Pb, const uint32
 // decisions; x at pass start in sb.scal[6], changed -> sb.scal[5], x at the
 // end of the pass -> sb.scal[9]
 void launch_refine_round(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* Pb, uint32_t* Tb, uint32_t* wantb,
-                         int64_t nc, long long cap, cudaStream_t s) {
+                         uint32_t* Db, int64_t nc, long long cap, cudaStream_t s) {
     int64_t nwords = (nc + 31) / 32;
     int64_t ntiles = (nwords + kRfT - 1) / kRfT;
     k_refine_reduce<<<(unsigned)ntiles, kRfT, 0, s>>>(sb.pair, Pb, wantb, nc, cap, b.tile_agg);
     k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, sb.scal + 6, b.tile_x);
-    k_refine_down<<<(unsigned)ntiles, kRfT, 0, s>>>(Pb, Tb, wantb, nc, cap, b.tile_x, sb.scal + 5, sb.scal + 9);
+    k_refine_down<<<(unsigned)ntiles, kRfT, 0, s>>>(Pb, Tb, wantb, nc, cap, b.tile_x, sb.scal + 5, sb.scal + 9, Db);
 }
 
 // x at pass start = number of label-0 chunk nodes, passed via scal[6] (host)

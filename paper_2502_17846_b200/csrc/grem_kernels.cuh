@@ -104,8 +104,8 @@ void launch_select_nodes(const uint8_t* flag, const unsigned long long* cnt, int
 struct SeedBufs {
     int32_t* rank;        // n: local index of a chunk node
     int32_t* start;       // nc+1 CSR row starts
-    int32_t* cursor;      // nc
-    uint32_t* adj;        // entries: local neighbour ids (rows unsorted)
+    int32_t* cursor;      // nc: self-loop entries per row (chunk-0 CSR by sort)
+    uint32_t* adj;        // entries: local neighbour ids (self-loops as w == row)
     uint32_t* row_of;     // entries: owning row
     uint32_t* parent;     // nc: union-find
     unsigned long long* ckey;  // nc: component (-degree, index) min key
@@ -134,6 +134,12 @@ void launch_degrees(const uint2* e, int64_t m, const int32_t* rank, int32_t* deg
                     cudaStream_t s);
 void launch_fill_csr(const uint2* e, int64_t m, const int32_t* rank, int32_t* cursor, uint32_t* adj,
                      uint32_t* row_of, const uint32_t* hub_keys, cudaStream_t s);
+size_t seed_csr_temp_bytes(int64_t entries);
+void launch_seed_sort(const uint2* e, int64_t m, uint32_t* keysA, uint32_t* valsA, uint32_t* keysB, uint32_t* valsB,
+                      int end_bit, uint32_t* nodes, int32_t* counts, long long* d_nruns, void* temp,
+                      size_t temp_bytes, bool* sorted_in_b, cudaStream_t s);
+void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const int32_t* rank,
+                     uint32_t* row_of, uint32_t* adj, int32_t* selfc, cudaStream_t s);
 
 // hub detection from a sample of the level's edges
 void launch_sample_degrees(const uint2* e, int64_t sample, int32_t* sdeg, cudaStream_t s);
@@ -170,7 +176,9 @@ void launch_xor_popc(const uint32_t* a, const uint32_t* b, int64_t nc, long long
 void launch_row_counts_bits(const SeedBufs& sb, const uint32_t* Pb, const uint32_t* Tb, int mode, int64_t entries,
                             int64_t nc, cudaStream_t s);
 void launch_refine_round(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* Pb, uint32_t* Tb, uint32_t* wantb,
-                         int64_t nc, long long cap, cudaStream_t s);
+                         uint32_t* Db, int64_t nc, long long cap, cudaStream_t s);
+void launch_refine_delta(const SeedBufs& sb, const uint32_t* Db, int64_t nc, int64_t changed, const uint32_t* Pb,
+                         const uint32_t* Tb, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_seed_commit(const SeedBufs& sb, const ChunkBufs& b, const uint32_t* nodes, int64_t nc,
                         cudaStream_t s);
 

@@ -84,10 +84,13 @@ struct DBuf {
 // the call's final synchronisation.
 enum Phase {
     PH_COUNT = 0, PH_SELECT, PH_NODE, PH_PREFS, PH_SCAN, PH_BUNDLE, PH_DECIDE, PH_COMMIT,
-    PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_HUBS, PH_N
+    PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_HUBS,
+    PH_SEED_CSR, PH_SEED_CC, PH_SEED_BFS, PH_SEED_REFINE, PH_SEED_COMMIT,   // inside "seed"
+    PH_N
 };
 static const char* kPhaseNames[PH_N] = {"count", "select", "node_init", "prefs", "scan", "bundle", "decide",
-                                        "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs"};
+                                        "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs",
+                                        "seed.csr", "seed.cc", "seed.bfs", "seed.refine", "seed.commit"};
 
 struct grem_ctx {
     int device = 0;
@@ -122,11 +125,12 @@ struct grem_ctx {
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
     // seed
     DBuf<int32_t> start{"start"}, cursor{"cursor"};
+    DBuf<uint32_t> sortk{"sortk"}, sortv{"sortv"};
     DBuf<uint32_t> adj{"adj"}, row_of{"row_of"}, parent{"parent"}, csize{"csize"}, roots{"roots"}, rvals{"rvals"}, rvals2{"rvals2"}, cpos{"cpos"}, disc{"disc"}, frontier{"frontier"};
     DBuf<unsigned long long> ckey{"ckey"}, rkeys{"rkeys"}, rkeys2{"rkeys2"}, cand{"cand"}, cand2{"cand2"}, pair{"pair"};
     DBuf<int8_t> slab{"slab"}, slab2{"slab2"};
     DBuf<int64_t> fdeg{"fdeg"}, cum{"cum"};
-    DBuf<uint32_t> bitsP{"bitsP"}, bitsT{"bitsT"}, bitsW{"bitsW"};
+    DBuf<uint32_t> bitsP{"bitsP"}, bitsT{"bitsT"}, bitsW{"bitsW"}, bitsD{"bitsD"};
     // hubs
     DBuf<uint32_t> hub_table{"hub_table"}, hub_ids{"hub_ids"};
     DBuf<unsigned long long> hub_k1{"hub_k1"}, hub_k2{"hub_k2"};
@@ -199,6 +203,23 @@ struct PhaseScope {
             c->prof_open.push_back({ph, {a, b}});
         }
     }
+};
+
+// consecutive sub-phases: to(ph) closes the open one and opens ph
+struct PhaseSeq {
+    grem_ctx* c;
+    int ph = -1;
+    cudaEvent_t a = nullptr;
+    explicit PhaseSeq(grem_ctx* c_) : c(c_) {}
+    void to(int nph) {
+        if (!c->profiling) return;
+        cudaEvent_t e = prof_event(c);
+        cudaEventRecord(e, c->s);
+        if (ph >= 0) c->prof_open.push_back({ph, {a, e}});
+        ph = nph;
+        a = e;
+    }
+    ~PhaseSeq() { to(-1); }
 };
 
 void prof_collect(grem_ctx* c) {
@@ -353,9 +374,23 @@ __global__ void k_count_diff(const int8_t* a, const int8_t* b, int64_t n, long l
 void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     cudaStream_t s = c->s;
     ChunkBufs b = chunk_bufs(c);
-    launch_mark_all(e, mc, c->flag.p, s);
-    launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
-    c->kernels += 2;
+    PhaseSeq seq(c);
+    seq.to(PH_SEED_CSR);
+    // chunk-0 CSR by one radix sort of (row id, column id) pairs: the sorted
+    // keys' runs are the chunk nodes in ascending id order (= ranks)
+    int64_t entries = 2 * mc;
+    int64_t nc_cap = a.n < entries ? a.n : entries;
+    ensure_seed(c, nc_cap, entries);
+    c->sortk.ensure(entries + 1, s);
+    c->sortv.ensure(entries + 1, s);
+    ensure_temp(c, seed_csr_temp_bytes(entries));
+    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc_cap + 1), s));
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)(a.n - 1) >> end_bit) != 0) ++end_bit;
+    bool in_b = false;
+    launch_seed_sort(e, mc, c->row_of.p, c->adj.p, c->sortk.p, c->sortv.p, end_bit, c->nodes.p, c->cursor.p,
+                     c->d_scal, c->temp.p, c->temp.cap, &in_b, s);
+    c->kernels += 1 + 2 * ((end_bit + 7) / 8) + 3;
     scal_read(c, c->d_scal, 1);
     int64_t nc = c->h_pin[0];
     if (nc == 0) fail(GREM_E_FORMAT, "cannot seed an empty chunk");
@@ -363,23 +398,13 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         fail(GREM_E_CAPACITY, "capacity " + std::to_string(a.cap) + " infeasible for " + std::to_string(nc) +
                                   " chunk nodes");
     c->stats.visits += nc;
-    launch_set_rank(c->nodes.p, nc, c->rank.p, s);
-    ensure_seed(c, nc, 0);
-    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));
-    const uint32_t* hubs = c->hubs_on ? c->hub_table.p : nullptr;
-    launch_degrees(e, mc, c->rank.p, c->cursor.p, hubs, s);
     exclusive_sum_i32(c->cursor.p, c->start.p, nc + 1, c->temp.p, c->temp.cap, s);
-    c->kernels += 3;
-    int32_t entries32 = 0;
-    CK(cudaMemcpyAsync(&c->h_pin[0], c->start.p + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    memcpy(&entries32, &c->h_pin[0], sizeof(int32_t));
-    int64_t entries = entries32;
-    ensure_seed(c, nc, entries);
+    launch_set_rank(c->nodes.p, nc, c->rank.p, s);
+    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));   // now: self-loop entries per row
+    launch_seed_map(in_b ? c->sortk.p : c->row_of.p, in_b ? c->sortv.p : c->adj.p, entries, c->rank.p, c->row_of.p,
+                    c->adj.p, c->cursor.p, s);
+    c->kernels += 4;
     SeedBufs sb = seed_bufs(c);
-    CK(cudaMemcpyAsync(c->cursor.p, c->start.p, sizeof(int32_t) * nc, cudaMemcpyDeviceToDevice, s));
-    launch_fill_csr(e, mc, c->rank.p, c->cursor.p, c->adj.p, c->row_of.p, hubs, s);
-    c->kernels += 1;
     long long target = (nc + 1) / 2;   // ceil(n / 2), seed.py:57
 
     if (a.seed_algo == 1) {
@@ -392,6 +417,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     } else {
         // ---- _bfs_grow (seed.py:56-94): components in restart order, BFS only
         // inside the component where the pick count crosses `target`.
+        seq.to(PH_SEED_CC);
         launch_cc(e, mc, c->rank.p, c->parent.p, c->roots.p, nc, s);
         launch_comp_keys(sb, nc, s);
         ensure_temp(c, select_nodes_temp_bytes(nc));
@@ -408,6 +434,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         long long sstar = c->h_pin[3];
         launch_seed_labels(sb, nc, s);
         c->kernels += 1;
+        seq.to(PH_SEED_BFS);
         long long count = 1;
         if (count < quota) {
             long long h = sstar;
@@ -446,10 +473,12 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         // ---- boundary refinement passes (seed.py:96-116): rounds to a
         // fixpoint with the exact sizes scan (moves are clamps, no ties), on
         // 1-bit label maps
+        seq.to(PH_SEED_REFINE);
         int64_t nwords = (nc + 31) / 32;
         c->bitsP.ensure(nwords + 8, s);
         c->bitsT.ensure(nwords + 8, s);
         c->bitsW.ensure(nwords + 8, s);
+        c->bitsD.ensure(nwords + 8, s);
         uint32_t* Pb = c->bitsP.p;
         uint32_t* Tb = c->bitsT.p;
         launch_pack_bits(sb.slab, nc, Pb, s);
@@ -457,13 +486,20 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         for (int pass = 0; pass < a.seed_passes; ++pass) {
             CK(cudaMemcpyAsync(Tb, Pb, sizeof(uint32_t) * nwords, cudaMemcpyDeviceToDevice, s));
             scal_write(c, c->d_sscal + 6, &xstart, 1);
+            int64_t changed = -1;
             for (int round = 0;; ++round) {
-                launch_row_counts_bits(sb, Pb, Tb, 0, entries, nc, s);
+                if (changed < 0 || changed > nc / 16) {
+                    launch_row_counts_bits(sb, Pb, Tb, 0, entries, nc, s);
+                } else {
+                    launch_refine_delta(sb, c->bitsD.p, nc, changed, Pb, Tb, c->temp.p, c->temp.cap, s);
+                    c->kernels += 2;
+                }
                 CK(cudaMemsetAsync(c->d_sscal + 5, 0, sizeof(long long), s));
-                launch_refine_round(sb, b, Pb, Tb, c->bitsW.p, nc, a.cap, s);
+                launch_refine_round(sb, b, Pb, Tb, c->bitsW.p, c->bitsD.p, nc, a.cap, s);
                 c->kernels += 4;
                 scal_read(c, c->d_sscal + 5, 1);
-                if (c->h_pin[0] == 0) break;
+                changed = c->h_pin[0];
+                if (changed == 0) break;
                 if (round > nc + 2) fail(GREM_E_FORMAT, "internal: refinement rounds did not converge");
             }
             CK(cudaMemsetAsync(c->d_sscal + 7, 0, sizeof(long long), s));
@@ -477,6 +513,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         launch_unpack_bits(Pb, nc, sb.slab, s);
         c->kernels += 2;
     }
+    seq.to(PH_SEED_COMMIT);
     {
         // estimates against the final seed labels (bitmap gathers)
         int64_t nwords = (nc + 31) / 32;
@@ -1242,7 +1279,8 @@ void grem_destroy(grem_ctx* c) {
     c->rank.release(); c->scratch.release(); c->newid.release();
     c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
     c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
-    c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release(); c->parent.release();
+    c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release();
+    c->sortk.release(); c->sortv.release(); c->parent.release();
     c->csize.release(); c->roots.release(); c->rvals.release(); c->rvals2.release(); c->cpos.release();
     c->disc.release(); c->frontier.release(); c->ckey.release(); c->rkeys.release(); c->rkeys2.release();
     c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
