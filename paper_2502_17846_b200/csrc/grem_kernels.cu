@@ -16,6 +16,7 @@
 //   decide   b = [x - o <= t]; labels that changed feed the next round.
 // A fixpoint equals the sequential result (by induction over the sweep).
 #include <cub/cub.cuh>
+#include <climits>
 #include <thrust/iterator/counting_iterator.h>
 #include <cuda_runtime.h>
 
@@ -1115,6 +1116,11 @@ __global__ void k_bundle_params(const uint8_t* __restrict__ meta, const int32_t*
         bp[i] = bundle_pack(meta[i], newb[i], cap);
 }
 
+// Segment simulation in offset coordinates: with O = the number of lifted
+// (o = 1) active nodes since the segment start and z = x + O, one node is
+// z' = z + [z < K] with K = t + o + O + 1 (inactive nodes: K = INT_MIN), a
+// two-deep min/max chain in 32-bit registers; K is built per staged batch by
+// a block scan of o.  Checkpoints and segment ends are stored as x = z - O.
 template <int NWIN>
 __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t* __restrict__ bp,
                                                                  const int32_t* __restrict__ newb,
@@ -1124,31 +1130,71 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
                                                                  int32_t* __restrict__ ckpt, const long long* nbad,
                                                                  const long long* first_bad) {
     constexpr int NT = kBundleWin * NWIN;
+    constexpr int IPT = (kBundleBatch + NT - 1) / NT;
     if (*nbad == 0) return;
     int64_t seg = blockIdx.x;
     if (seg < bundle_seg0(first_bad, L)) return;
-    __shared__ int32_t sp[kBundleBatch];
+    __shared__ int32_t sK[kBundleBatch];
+    __shared__ int32_t sO[kBundleBatch / kCkpt + 1];
+    __shared__ int32_t swarp[NT / 32 + 1];
     int64_t lo = seg * L;
     int64_t hi = lo + L < nc ? lo + L : nc;
-    int tid = threadIdx.x;
+    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int win = tid / kBundleWin;
     long long c = win == 0 ? xspec[lo] : (win == 1 ? xalt[lo] : ((long long)newb[lo] + 1) / 2);
-    long long x = c + (tid % kBundleWin) - kBundleWin / 2;
+    int32_t z = (int32_t)(c + (tid % kBundleWin) - kBundleWin / 2);
+    int32_t ocarry = 0;   // O at the start of the staged batch
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
     int32_t* ck = ckpt + seg * ncp * NT;
     for (int64_t b = lo; b < hi; b += kBundleBatch) {
         int cnt = (int)(hi - b < kBundleBatch ? hi - b : kBundleBatch);
         __syncthreads();
-        for (int k = tid; k < cnt; k += NT) sp[k] = bp[b + k];
+        // stage: o and t of this thread's IPT consecutive nodes, block scan of o
+        int32_t pk[IPT];
+        int osum = 0;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            int k = tid * IPT + j;
+            pk[j] = k < cnt ? bp[b + k] : 2;
+            osum += (pk[j] & 3) == 1;
+        }
+        int incl = osum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        if (lane == 31) swarp[wid] = incl;
+        __syncthreads();
+        int before = ocarry;
+        for (int w = 0; w < wid; ++w) before += swarp[w];
+        before += incl - osum;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            int k = tid * IPT + j;
+            if (k < cnt) {
+                int o = pk[j] & 3;
+                if ((k & (kCkpt - 1)) == 0) sO[k / kCkpt] = before;
+                sK[k] = o == 2 ? INT_MIN : (pk[j] >> 2) + o + before + 1;
+                before += o == 1;
+            }
+        }
+        int total = 0;
+        for (int w = 0; w < NT / 32; ++w) total += swarp[w];
         __syncthreads();
         for (int k0 = 0; k0 < cnt; k0 += kCkpt) {
-            ck[((b - lo + k0) / kCkpt) * NT + tid] = (int32_t)x;   // x before node b + k0
+            ck[((b - lo + k0) / kCkpt) * NT + tid] = z - sO[k0 / kCkpt];   // x before node b + k0
             int lim = cnt - k0 < kCkpt ? cnt - k0 : kCkpt;
-#pragma unroll 8
-            for (int k = 0; k < lim; ++k) x = bundle_step(x, sp[k0 + k]);
+            if (lim == kCkpt) {
+#pragma unroll 16
+                for (int k = 0; k < kCkpt; ++k) z = min(max(z, sK[k0 + k]), z + 1);
+            } else {
+                for (int k = 0; k < lim; ++k) z = min(max(z, sK[k0 + k]), z + 1);
+            }
         }
+        ocarry += total;
     }
-    ends[seg * NT + tid] = (int32_t)x;
+    ends[seg * NT + tid] = z - ocarry;
 }
 
 // single warp: exact chain over segments.  Segment tables are staged into
@@ -1157,6 +1203,10 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
@@ -1184,9 +1234,9 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
         for (int k = lane; k < n16; k += 32) cp_async16(&tab[buf][k * 4], src + k * 4);
         if (lane < cnt) {
             int64_t lo = (s0 + lane) * L;
-            cen[buf][lane][0] = xspec[lo];
-            if (NWIN > 1) cen[buf][lane][1] = xalt[lo];
-            if (NWIN > 2) cen[buf][lane][NWIN > 2 ? 2 : 0] = (int32_t)(((long long)newb[lo] + 1) / 2);
+            cp_async4(&cen[buf][lane][0], xspec + lo);
+            if (NWIN > 1) cp_async4(&cen[buf][lane][1], xalt + lo);
+            if (NWIN > 2) cp_async4(&cen[buf][lane][NWIN > 2 ? 2 : 0], newb + lo);   // balance point: (s + 1) / 2
         }
         cp_async_commit();
     };
@@ -1208,7 +1258,8 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
             int hit = -1;
 #pragma unroll
             for (int w = 0; w < NWIN; ++w) {
-                long long d = cur - cen[buf][j][w] + kBundleWin / 2;
+                long long cw = w == 2 ? ((long long)cen[buf][j][w] + 1) / 2 : (long long)cen[buf][j][w];
+                long long d = cur - cw + kBundleWin / 2;
                 if (hit < 0 && d >= 0 && d < kBundleWin) hit = w * kBundleWin + (int)d;
             }
             if (lane == 0) {
@@ -1248,13 +1299,12 @@ struct BundleFix {
 template <int NWIN>
 __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __restrict__ xin,
                                const int32_t* __restrict__ hit, const int32_t* __restrict__ ckpt, int64_t nseg,
-                               int64_t nc, int64_t L, int32_t* __restrict__ x, const long long* nbad,
-                               const long long* first_bad, BundleFix fx) {
+                               int64_t nc, int64_t L, int32_t* __restrict__ x, int32_t* __restrict__ xalt,
+                               const long long* nbad, const long long* first_bad) {
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
     int64_t seg0 = bundle_seg0(first_bad, L);
-    long long dch = 0;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nseg * ncp;
          w += (int64_t)gridDim.x * blockDim.x) {
         int64_t seg = w / ncp, cp = w % ncp;
@@ -1276,30 +1326,42 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
         }
         for (int64_t i = a; i < e; ++i) {
             x[i] = (int32_t)cur;
-            if (fx.xalt) fx.xalt[i] = (int32_t)cur;
-            int32_t pk = bp[i];
-            int o = pk & 3;
-            if (o != 2 && fx.tl) {
-                int b = (cur - o <= (long long)(pk >> 2)) ? 0 : 1;
-                uint32_t g = fx.nodes[i];
-                uint8_t t8 = fx.tl[g];
-                int spec_code = t8 & 0xF, prev = t8 >> 4;
-                if (b + 1 != spec_code) {
-                    fx.tl[g] = (uint8_t)((b + 1) | (prev << 4));
-                    dch += (long long)(b + 1 != prev) - (long long)(spec_code != prev);
-                }
-                uint8_t m = fx.meta[i];
-                bool tie0 = (cur - o) <= (node_sl(m, fx.newb[i]) >> 1);
-                fx.meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
-            }
-            cur = bundle_step(cur, pk);
+            if (xalt) xalt[i] = (int32_t)cur;
+            cur = bundle_step(cur, bp[i]);
         }
         if (e == nc) {
             x[nc] = (int32_t)cur;
-            if (fx.xalt) fx.xalt[nc] = (int32_t)cur;
+            if (xalt) xalt[nc] = (int32_t)cur;
         }
     }
-    if (fx.changed && dch) atomicAdd((unsigned long long*)fx.changed, (unsigned long long)dch);
+}
+
+// the repaired suffix re-decided from its exact x, one thread per node
+__global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __restrict__ x, int64_t nc, int64_t L,
+                             const long long* nbad, const long long* first_bad, BundleFix fx) {
+    if (*nbad == 0) return;
+    int64_t lo = bundle_seg0(first_bad, L) * L;
+    long long dch = 0;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t pk = bp[i];
+        int o = pk & 3;
+        if (o == 2) continue;
+        long long cur = x[i];
+        int b = (cur - o <= (long long)(pk >> 2)) ? 0 : 1;
+        uint32_t g = fx.nodes[i];
+        uint8_t t8 = fx.tl[g];
+        int spec_code = t8 & 0xF, prev = t8 >> 4;
+        if (b + 1 != spec_code) {
+            fx.tl[g] = (uint8_t)((b + 1) | (prev << 4));
+            dch += (long long)(b + 1 != prev) - (long long)(spec_code != prev);
+        }
+        uint8_t m = fx.meta[i];
+        bool tie0 = (cur - o) <= (node_sl(m, fx.newb[i]) >> 1);
+        fx.meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
+    }
+    for (int off = 16; off; off >>= 1) dch += __shfl_down_sync(0xffffffffu, dch, off);
+    if ((threadIdx.x & 31) == 0 && dch) atomicAdd((unsigned long long*)fx.changed, (unsigned long long)dch);
 }
 
 int64_t bundle_segment_len(int64_t nc) {
@@ -1327,21 +1389,23 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
                  fix_decisions ? b.scal + 1 : nullptr};
     k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
+    int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;
     if (nwin == 3) {
         k_bundle_sim<3><<<(unsigned)nseg, kBundleWin * 3, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
                                                                  nbad, first_bad);
         k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3);
-        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad,
-                                               fx);
+        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
+                                               first_bad);
     } else {
         k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
                                                                  nbad, first_bad);
         k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3);
-        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, nbad, first_bad,
-                                               fx);
+        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
+                                               first_bad);
     }
+    if (fix_decisions) k_bundle_fix<<<grid_for(nc, 256), 256, 0, s>>>(bb.params, b.x, nc, L, nbad, first_bad, fx);
 }
 
 __global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
@@ -1596,6 +1660,64 @@ void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent,
                cudaStream_t s) {
     k_iota_u32<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
     k_cc_link<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, rank, parent);
+    k_cc_roots<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc, scratch);
+    cudaMemcpyAsync(parent, scratch, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, s);
+}
+
+// Components over the chunk-0 CSR with sampled linking (the Afforest scheme):
+// link every row to its first two neighbours, flatten, find the most common
+// root (the giant component) from a sample, then link the remaining
+// neighbours of rows outside it only.  An edge skipped at a giant row is
+// linked from its other endpoint's row unless that row was in the giant
+// component too, so the final components equal the full union-find's.
+__device__ __forceinline__ void uf_link(uint32_t* parent, uint32_t a, uint32_t b) {
+    while (true) {
+        uint32_t ra = uf_find(parent, a), rb = uf_find(parent, b);
+        if (ra == rb) return;
+        if (ra > rb) { uint32_t t = ra; ra = rb; rb = t; }
+        if (atomicCAS(&parent[rb], rb, ra) == rb) return;
+        a = ra;
+        b = rb;
+    }
+}
+__global__ void k_cc_link_rows(const int32_t* __restrict__ start, const uint32_t* __restrict__ adj, int64_t nc,
+                               uint32_t* parent, int first, int count, const unsigned long long* giant) {
+    uint32_t g = giant ? (uint32_t)*giant : 0xFFFFFFFFu;
+    GRID_STRIDE(i, nc) {
+        int64_t b = start[i] + first, e = start[i + 1];
+        if (count > 0 && b + count < e) e = b + count;
+        if (b >= e) continue;
+        if (giant && uf_find(parent, (uint32_t)i) == g) continue;
+        for (int64_t j = b; j < e; ++j) {
+            uint32_t w = adj[j];
+            if (w != (uint32_t)i) uf_link(parent, (uint32_t)i, w);
+        }
+    }
+}
+// the most frequent root among 1024 sampled nodes (flattened forest)
+__global__ void k_cc_giant(const uint32_t* __restrict__ parent, int64_t nc, unsigned long long* giant) {
+    __shared__ uint32_t smp[1024];
+    __shared__ unsigned long long best;
+    uint32_t t = threadIdx.x;
+    uint64_t h = (uint64_t)(t + 1) * 0x9E3779B97F4A7C15ULL;
+    h ^= h >> 29;
+    smp[t] = parent[h % (uint64_t)nc];
+    if (t == 0) best = 0;
+    __syncthreads();
+    uint32_t c = 0;
+    for (int j = 0; j < 1024; ++j) c += smp[j] == smp[t];
+    atomicMax(&best, ((unsigned long long)c << 32) | (0xFFFFFFFFu - smp[t]));   // ties: smaller root
+    __syncthreads();
+    if (t == 0) *giant = 0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFULL);
+}
+void launch_cc_csr(const int32_t* start, const uint32_t* adj, int64_t nc, uint32_t* parent, uint32_t* scratch,
+                   unsigned long long* d_giant, cudaStream_t s) {
+    k_iota_u32<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc);
+    k_cc_link_rows<<<grid_for(nc, 256, 16), 256, 0, s>>>(start, adj, nc, parent, 0, 2, nullptr);
+    k_cc_roots<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc, scratch);
+    cudaMemcpyAsync(parent, scratch, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, s);
+    k_cc_giant<<<1, 1024, 0, s>>>(parent, nc, d_giant);
+    k_cc_link_rows<<<grid_for(nc, 256, 16), 256, 0, s>>>(start, adj, nc, parent, 2, 0, d_giant);
     k_cc_roots<<<grid_for(nc, 256), 256, 0, s>>>(parent, nc, scratch);
     cudaMemcpyAsync(parent, scratch, sizeof(uint32_t) * nc, cudaMemcpyDeviceToDevice, s);
 }

@@ -418,11 +418,12 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         // ---- _bfs_grow (seed.py:56-94): components in restart order, BFS only
         // inside the component where the pick count crosses `target`.
         seq.to(PH_SEED_CC);
-        launch_cc(e, mc, c->rank.p, c->parent.p, c->roots.p, nc, s);
+        launch_cc_csr(c->start.p, c->adj.p, nc, c->parent.p, c->roots.p,
+                      reinterpret_cast<unsigned long long*>(c->d_sscal + 13), s);
         launch_comp_keys(sb, nc, s);
         ensure_temp(c, select_nodes_temp_bytes(nc));
         launch_select_roots(sb, nc, c->temp.p, c->temp.cap, s);
-        c->kernels += 5;
+        c->kernels += 8;
         scal_read(c, c->d_sscal, 1);
         int64_t nr = c->h_pin[0];
         launch_root_keys(sb, nr, s);
@@ -603,12 +604,12 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             }
             BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
             launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
-            c->kernels += 4;
+            c->kernels += 5;
         }
         if (getenv("GREM_DEBUG_BUNDLE")) {
-            scal_read(c, c->d_scal + 3, 2);
-            fprintf(stderr, "[bundle] round %d nc %lld nbad %lld misses(cum) %lld\n", r, (long long)nc, c->h_pin[1],
-                    c->h_pin[0]);
+            scal_read(c, c->d_scal + 1, 4);
+            fprintf(stderr, "[bundle] round %d nc %lld changed %lld nbad %lld misses(cum) %lld\n", r, (long long)nc,
+                    c->h_pin[0], c->h_pin[3], c->h_pin[2]);
         }
         // this round's exact x becomes the next round's second window centre
         std::swap(c->xalt.p, c->xnext.p);
@@ -710,6 +711,8 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
         }
     } level_log{c, lv0, lv1, a, r0, v0, b0};
     if (a.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+    // bundle tables pack a threshold and a lift into one int32 (t * 4 + o)
+    if (a.n >= (1LL << 29)) fail(GREM_E_FORMAT, "bisections over 2^29 or more nodes are not supported");
     if (2 * a.cap < a.n)
         fail(GREM_E_CAPACITY, "capacity " + std::to_string(a.cap) + " cannot hold " + std::to_string(a.n) +
                                   " nodes across two parts");

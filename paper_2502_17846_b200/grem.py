@@ -55,6 +55,20 @@ def context():
     return c
 
 
+def _host_labels(n: int) -> np.ndarray:
+    """Label output buffer in page-locked memory (torch's caching host
+    allocator, reused across calls) so the device->host copy of the labels
+    runs at DMA speed; the array keeps its block alive."""
+    if n >= (1 << 20):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        except Exception:  # noqa: BLE001
+            pass
+    return np.empty(n, dtype=np.int32)
+
+
 def _raise(rc: int, pending=None):
     if pending:
         raise pending[0]
@@ -188,7 +202,7 @@ def bisect(efile, config, *, capacity=None, meter=None, on_chunk=None, prefetch:
     state = _StateProxy(ctx, n, cap) if on_chunk is not None else None
     hooks, keep, pending = _hooks(config, meter, on_chunk, state)
     cfg = _cfg_struct(config, plan.chunk_size)
-    labels = np.empty(n, dtype=np.int32)
+    labels = _host_labels(n)
     rep, sizes = _report_struct(2)
     if is_native_binary(efile):
         rc = L.grem_bisect_file(ctx, os.fsencode(efile.path), ctypes.byref(cfg), int(cap), ctypes.byref(hooks),
@@ -214,7 +228,7 @@ def partition(efile, p: int, config, workdir: str, *, meter=None):
     L = _abi.lib()
     hooks, keep, pending = _hooks(config, meter, None, None)
     cfg = _cfg_struct(config, None)
-    labels = np.empty(n, dtype=np.int32)
+    labels = _host_labels(n)
     rep, sizes = _report_struct(max(2, int(p)))
     if is_native_binary(efile):
         rc = L.grem_partition_file(ctx, os.fsencode(efile.path), int(p), ctypes.byref(cfg), ctypes.byref(hooks),
@@ -255,7 +269,7 @@ def bisect_edges(edges, num_nodes: int, config, capacity=None, on_device_ptr: in
     plan = plan_for(config, m)
     hooks, keep, pending = _hooks(config)
     cfg = _cfg_struct(config, plan.chunk_size)
-    labels = np.empty(n, dtype=np.int32)
+    labels = _host_labels(n)
     rep, sizes = _report_struct(2)
     if on_device_ptr is None:
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
@@ -276,7 +290,7 @@ def partition_edges(edges, num_nodes: int, p: int, config, on_device_ptr: int | 
         raise FormatError(f"number of parts must be a power of two >= 2, got {p}")
     hooks, keep, pending = _hooks(config)
     cfg = _cfg_struct(config, None)
-    labels = np.empty(n, dtype=np.int32)
+    labels = _host_labels(n)
     rep, sizes = _report_struct(max(2, int(p)))
     if on_device_ptr is None:
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
