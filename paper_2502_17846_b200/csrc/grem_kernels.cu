@@ -336,7 +336,9 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
 // tentative label; apply the change since the previous round.
 __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
-                                                              unsigned long long* __restrict__ cnt,
+                                                              const uint32_t* __restrict__ chg,
+                                                              const int32_t* __restrict__ pos,
+                                                              unsigned long long* __restrict__ cntc,
                                                               const uint32_t* __restrict__ hub_keys) {
     __shared__ uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
@@ -350,19 +352,18 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
         uint32_t u = ed.x, v = ed.y;
         if (u == v) continue;
         uint32_t a = u < v ? u : v, b = u < v ? v : u;
+        if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
         uint8_t t = tl[a];
         int cur = t & 0xF, prev = t >> 4;
-        if (cur != prev) {
-            unsigned long long d = enc_label(cur) - enc_label(prev);
-            int hb = hub_find(s_keys, b);
-            if (hb >= 0) atomicAdd(&s_cnt[hb], d);
-            else atomicAdd(&cnt[b], d);
-        }
+        unsigned long long d = enc_label(cur) - enc_label(prev);
+        int hb = hub_find(s_keys, b);
+        if (hb >= 0) atomicAdd(&s_cnt[hb], d);
+        else atomicAdd(&cntc[pos[b]], d);
     }
     __syncthreads();
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
         uint32_t key = s_keys[k];
-        if (key != kHubEmpty && s_cnt[k]) atomicAdd(&cnt[key], s_cnt[k]);
+        if (key != kHubEmpty && s_cnt[k]) atomicAdd(&cntc[pos[key]], s_cnt[k]);
     }
 }
 
@@ -377,7 +378,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.cnt, b.hub_keys);
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys);
 }
 
 // -------------------------------------------------- binned round-1 counting
@@ -650,8 +651,11 @@ void launch_select_nodes(const uint8_t* flag, const unsigned long long* cnt, int
 
 // ------------------------------------------------------------ node passes
 
+// chunk node i: meta, compact round state (counts, estimates, label codes),
+// the id -> index map; the id-indexed counters and flags are cleared for the
+// next chunk here.
 __global__ void k_node_init(const uint32_t* __restrict__ nodes, int64_t nc, const int8_t* __restrict__ lab,
-                            int refine, uint8_t* __restrict__ meta, uint8_t* __restrict__ tl,
+                            int refine, uint8_t* __restrict__ meta, ChunkBufs b,
                             int32_t* __restrict__ newflag, long long* total_new) {
     int cnt_new = 0;
     GRID_STRIDE(i, nc) {
@@ -661,7 +665,12 @@ __global__ void k_node_init(const uint32_t* __restrict__ nodes, int64_t nc, cons
         bool isnew = old == -1;
         bool active = isnew || refine;
         meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
-        tl[g] = (uint8_t)(code | (code << 4));
+        b.tlc[i] = (uint8_t)(code | (code << 4));
+        b.pos[g] = (int32_t)i;
+        b.cntc[i] = b.cnt[g];
+        b.cnt[g] = 0ULL;
+        b.flag[g] = 0;
+        b.nbrc[i] = isnew ? make_double2(0.0, 0.0) : b.nbr[g];
         int nf = (active && isnew) ? 1 : 0;
         newflag[i] = nf;
         cnt_new += nf;
@@ -671,7 +680,7 @@ __global__ void k_node_init(const uint32_t* __restrict__ nodes, int64_t nc, cons
 }
 
 void launch_node_init(const ChunkBufs& b, int64_t nc, int refine, cudaStream_t s) {
-    k_node_init<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.lab, refine, b.meta, b.tl, b.x, b.scal + 2);
+    k_node_init<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.lab, refine, b.meta, b, b.x, b.scal + 2);
 }
 
 __device__ __forceinline__ void averaged(uint8_t m, unsigned long long c, double2 nb, double& a0, double& a1) {
@@ -686,36 +695,6 @@ __device__ __forceinline__ void averaged(uint8_t m, unsigned long long c, double
     }
 }
 
-__global__ void k_prefs(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
-                        const int32_t* __restrict__ newb, const unsigned long long* __restrict__ cnt,
-                        const double2* __restrict__ nbr, const long long* __restrict__ sizes, int first_round) {
-    long long x0 = sizes[0];
-    GRID_STRIDE(i, nc) {
-        uint8_t m = meta[i];
-        if (!meta_active(m)) continue;
-        uint32_t g = nodes[i];
-        unsigned long long c = cnt[g];
-        double2 nb = make_double2(0.0, 0.0);
-        if (meta_old(m) != -1) nb = nbr[g];
-        double a0, a1;
-        averaged(m, c, nb, a0, a1);
-        int pref = a0 < a1 ? 1 : (a1 < a0 ? 0 : 2);   // assign(), grem.py:106-110
-        m = (uint8_t)((m & ~M_PREF) | (pref << M_PREF_SHIFT));
-        if (first_round) {
-            // first guess for ties: smaller side at the chunk's starting sizes
-            long long o = meta_old(m) == 0 ? 1 : 0;
-            long long lift = meta_old(m) != -1 ? 1 : 0;
-            long long sl = newb[i] - lift;   // newb holds s0 + new nodes before i
-            bool side0 = (x0 - o) <= (sl >> 1);
-            m = (uint8_t)(side0 ? (m & ~M_SPEC) : (m | M_SPEC));
-        }
-        meta[i] = m;
-    }
-}
-
-void launch_prefs(const ChunkBufs& b, int64_t nc, int first_round, cudaStream_t s) {
-    k_prefs<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.newb, b.cnt, b.nbr, b.sizes, first_round);
-}
 
 template <class Src>
 static void run_scan_chunk(const Src& src, int64_t N, const ChunkBufs& b, cudaStream_t s) {
@@ -878,19 +857,17 @@ __global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_a
     int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
     uint8_t m[kRI];
     int32_t nb[kRI];
-    uint32_t g[kRI];
     load8_u8(a.meta + base, m);
     load8_32(a.newb + base, nb);
-    load8_32(a.nodes + base, g);
     long long x0 = a.sizes[0];
     Clamp acc = clamp_identity();
 #pragma unroll
     for (int j = 0; j < kRI; ++j) {
         uint8_t mm = m[j];
         if (meta_active(mm)) {   // preferences: assign() inputs (grem.py:138-150)
-            unsigned long long c = a.cnt[g[j]];
+            unsigned long long c = a.cnt[base + j];
             double2 nbv = make_double2(0.0, 0.0);
-            if (meta_old(mm) != -1) nbv = a.nbr[g[j]];
+            if (meta_old(mm) != -1) nbv = a.nbr[base + j];
             double a0, a1;
             averaged(mm, c, nbv, a0, a1);
             int pref = a0 < a1 ? 1 : (a1 < a0 ? 0 : 2);
@@ -913,7 +890,9 @@ __global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_a
 struct RoundOut {
     int32_t* x;
     int32_t* xalt;
-    uint8_t* tl;
+    uint8_t* tlc;      // compact codes (cur | prev << 4)
+    uint8_t* tl;       // id-indexed codes, written for changed nodes only
+    uint32_t* chg;     // id-indexed changed bits
     long long* scal;   // [1] changed, [4] nbad, [6] first bad
 };
 
@@ -933,6 +912,8 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     Clamp pre = block_excl_scan<kRT>(acc, smem, nullptr);
     long long x = clamp_apply(pre, tile_x[blockIdx.x]);
     load8_32(a.nodes + base, g);
+    uint8_t tc[kRI];
+    load8_u8(out.tlc + base, tc);
     int32_t xs[kRI];
     int nbad = 0, ch = 0;
     long long mybad = kInf;
@@ -949,10 +930,13 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
                 if (base + j < mybad) mybad = base + j;
             }
             // speculative decision (exact unless a repair follows) and tentative label update
-            uint8_t t8 = out.tl[g[j]];
-            int cur = t8 & 0xF, code = b + 1;
-            out.tl[g[j]] = (uint8_t)(code | (cur << 4));
-            ch += (code != cur);
+            int cur = tc[j] & 0xF, code = b + 1;
+            tc[j] = (uint8_t)(code | (cur << 4));
+            if (code != cur) {
+                ch++;
+                out.tl[g[j]] = tc[j];
+                atomicOr(&out.chg[g[j] >> 5], 1u << (g[j] & 31));
+            }
             // next round's tie guess: the tie rule at this x
             bool tie0 = (x - nm.o) <= (sl >> 1);
             m[j] = (uint8_t)(tie0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
@@ -962,6 +946,7 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     store8_32(out.x + base, xs);
     store8_32(out.xalt + base, xs);
     store8_u8(a.meta + base, m);
+    store8_u8(out.tlc + base, tc);
     if (base + kRI > a.nc && base <= a.nc) out.x[a.nc] = xs[a.nc - base];   // padding is identity
     for (int off = 16; off; off >>= 1) {
         nbad += __shfl_down_sync(0xffffffffu, nbad, off);
@@ -977,11 +962,11 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
 }
 
 void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s) {
-    RoundArgs a{b.nodes, b.meta, b.newb, b.cnt, b.nbr, b.sizes, cap, nc};
+    RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc};
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
     k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x);
-    RoundOut o{b.x, b.xnext, b.tl, b.scal};
+    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.scal};
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
 }
 
@@ -1291,7 +1276,9 @@ struct BundleFix {
     const uint32_t* nodes;
     uint8_t* meta;
     const int32_t* newb;
+    uint8_t* tlc;
     uint8_t* tl;
+    uint32_t* chg;
     int32_t* xalt;
     long long* changed;
 };
@@ -1349,12 +1336,20 @@ __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __re
         if (o == 2) continue;
         long long cur = x[i];
         int b = (cur - o <= (long long)(pk >> 2)) ? 0 : 1;
-        uint32_t g = fx.nodes[i];
-        uint8_t t8 = fx.tl[g];
+        uint8_t t8 = fx.tlc[i];
         int spec_code = t8 & 0xF, prev = t8 >> 4;
         if (b + 1 != spec_code) {
-            fx.tl[g] = (uint8_t)((b + 1) | (prev << 4));
-            dch += (long long)(b + 1 != prev) - (long long)(spec_code != prev);
+            uint8_t nt = (uint8_t)((b + 1) | (prev << 4));
+            fx.tlc[i] = nt;
+            bool now = b + 1 != prev, was = spec_code != prev;
+            dch += (long long)now - (long long)was;
+            uint32_t g = fx.nodes[i];
+            if (now) {
+                fx.tl[g] = nt;
+                if (!was) atomicOr(&fx.chg[g >> 5], 1u << (g & 31));
+            } else if (was) {
+                atomicAnd(&fx.chg[g >> 5], ~(1u << (g & 31)));
+            }
         }
         uint8_t m = fx.meta[i];
         bool tie0 = (cur - o) <= (node_sl(m, fx.newb[i]) >> 1);
@@ -1385,7 +1380,7 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
     const long long* nbad = b.scal + 4;
     const long long* first_bad = b.scal + 6;
-    BundleFix fx{b.nodes, b.meta, b.newb, fix_decisions ? b.tl : nullptr, fix_decisions ? b.xnext : nullptr,
+    BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
                  fix_decisions ? b.scal + 1 : nullptr};
     k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
@@ -1408,59 +1403,28 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     if (fix_decisions) k_bundle_fix<<<grid_for(nc, 256), 256, 0, s>>>(bb.params, b.x, nc, L, nbad, first_bad, fx);
 }
 
-__global__ void k_decide(const uint32_t* __restrict__ nodes, int64_t nc, uint8_t* __restrict__ meta,
-                         const int32_t* __restrict__ newb, const int32_t* __restrict__ x, long long cap,
-                         uint8_t* __restrict__ tl, long long* changed) {
-    int ch = 0;
-    GRID_STRIDE(i, nc) {
-        uint8_t m = meta[i];
-        if (!meta_active(m)) continue;
-        long long lift = meta_old(m) != -1 ? 1 : 0;
-        NodeMap nm = node_map(m, (long long)newb[i] - lift, cap);
-        int b = ((long long)x[i] - nm.o <= nm.t) ? 0 : 1;
-        uint32_t g = nodes[i];
-        uint8_t t = tl[g];
-        int cur = t & 0xF;
-        int code = b + 1;
-        tl[g] = (uint8_t)(code | (cur << 4));
-        ch += (code != cur);
-        // next round's tie guess: the tie rule evaluated at this round's exact x
-        long long o = meta_old(m) == 0 ? 1 : 0;
-        bool tie0 = ((long long)x[i] - o) <= (((long long)newb[i] - lift) >> 1);
-        meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
-    }
-    for (int off = 16; off; off >>= 1) ch += __shfl_down_sync(0xffffffffu, ch, off);
-    if ((threadIdx.x & 31) == 0 && ch) atomicAdd((unsigned long long*)changed, (unsigned long long)ch);
-}
-
-void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s) {
-    k_decide<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.newb, b.x, cap, b.tl, b.scal + 1);
-}
 
 __global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const uint8_t* __restrict__ meta,
-                         unsigned long long* __restrict__ cnt, double2* __restrict__ nbr, int8_t* __restrict__ lab,
-                         const uint8_t* __restrict__ tl, uint8_t* __restrict__ flag, uint32_t* __restrict__ lab2) {
+                         const unsigned long long* __restrict__ cntc, const double2* __restrict__ nbrc,
+                         double2* __restrict__ nbr, int8_t* __restrict__ lab, const uint8_t* __restrict__ tlc,
+                         uint32_t* __restrict__ lab2) {
     GRID_STRIDE(i, nc) {
-        uint32_t g = nodes[i];
         uint8_t m = meta[i];
         if (meta_active(m)) {
-            double2 nb = make_double2(0.0, 0.0);
-            if (meta_old(m) != -1) nb = nbr[g];
+            uint32_t g = nodes[i];
             double a0, a1;
-            averaged(m, cnt[g], nb, a0, a1);
+            averaged(m, cntc[i], nbrc[i], a0, a1);
             nbr[g] = make_double2(a0, a1);
-            int code = tl[g] & 0xF;
+            int code = tlc[i] & 0xF;
             lab[g] = (int8_t)(code - 1);
             uint32_t diff = (uint32_t)((code ^ (m & M_OLD)) & 3);
             if (diff) atomicXor(&lab2[g >> 4], diff << ((g & 15) * 2));
         }
-        cnt[g] = 0ULL;
-        flag[g] = 0;
     }
 }
 
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
-    k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cnt, b.nbr, b.lab, b.tl, b.flag, b.lab2);
+    k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cntc, b.nbrc, b.nbr, b.lab, b.tlc, b.lab2);
 }
 
 __global__ void k_sizes_update(long long* sizes, const int32_t* x, int64_t nc, const long long* total_new) {

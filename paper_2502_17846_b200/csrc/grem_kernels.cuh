@@ -32,6 +32,12 @@ struct ChunkBufs {
     int32_t* xalt;      // exact x of the previous round (bundle window centre; read-only in a round)
     int32_t* xnext;     // exact x of this round (becomes xalt of the next round)
     uint8_t* bad;       // tie speculation inconsistent at i
+    // compact per-chunk-node round state (coalesced in every round)
+    unsigned long long* cntc;   // packed counts (c0 | c1 << 32) of chunk node i
+    double2* nbrc;              // running estimates of chunk node i (old nodes; 0 for new)
+    uint8_t* tlc;               // tentative label codes (cur | prev << 4) of chunk node i
+    int32_t* pos;               // n: chunk index of node g (valid for this chunk's nodes)
+    uint32_t* chg;              // n bits: tentative label changed in the last round (tl[g] valid)
     // per scan tile
     Clamp* tile_agg;
     long long* tile_x;
@@ -67,7 +73,6 @@ int num_sms();
 void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
 void launch_node_init(const ChunkBufs& b, int64_t nc, int refine, cudaStream_t s);
-void launch_prefs(const ChunkBufs& b, int64_t nc, int first_round, cudaStream_t s);
 void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t s);
 void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_walk(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
@@ -89,7 +94,6 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
 // fused round: preferences + clamp tile aggregates, top scan, x / tie check /
 // speculative decisions (node arrays padded to whole kScanTile tiles)
 void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s);
-void launch_decide(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 

@@ -119,6 +119,10 @@ struct grem_ctx {
     // per chunk node
     DBuf<uint32_t> nodes{"nodes"};
     DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
+    DBuf<unsigned long long> cntc{"cntc"};
+    DBuf<double2> nbrc{"nbrc"};
+    DBuf<uint8_t> tlc{"tlc"};
+    DBuf<uint32_t> chg{"chg"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
     DBuf<Clamp> tile_agg{"tile_agg"};
@@ -242,6 +246,7 @@ void ensure_nodes(grem_ctx* c, int64_t n) {
     c->cnt.ensure(n, c->s);
     c->nbr.ensure(n, c->s);
     c->rank.ensure(n, c->s);
+    c->chg.ensure(n / 32 + 2, c->s);
     c->scratch.ensure(2 * n + 2, c->s);
     c->newid.ensure(n + 1, c->s);
     ensure_temp(c, select_nodes_temp_bytes(n));
@@ -258,6 +263,9 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->x.ensure(padded, c->s);
     c->xalt.ensure(padded, c->s);
     c->xnext.ensure(padded, c->s);
+    c->cntc.ensure(padded, c->s);
+    c->nbrc.ensure(padded, c->s);
+    c->tlc.ensure(padded, c->s);
     int64_t nseg = (nc_cap + bundle_segment_len(nc_cap) - 1) / bundle_segment_len(nc_cap) + 2;
     c->bends.ensure(nseg * 192, c->s);
     c->bxin.ensure(nseg, c->s);
@@ -313,6 +321,11 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.xalt = c->xalt.p;
     b.xnext = c->xnext.p;
     b.bad = c->bad.p;
+    b.cntc = c->cntc.p;
+    b.nbrc = c->nbrc.p;
+    b.tlc = c->tlc.p;
+    b.pos = c->rank.p;   // the seed's rank array (chunk 0 only) doubles as the chunk index map
+    b.chg = c->chg.p;
     b.tile_agg = c->tile_agg.p;
     b.tile_x = c->tile_x.p;
     b.tile_bad = c->tile_bad.p;
@@ -581,6 +594,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         if (r > 1) {
             PhaseScope ps(c, PH_COUNT);
             launch_count_delta(e, mc, b, s);
+            CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));   // consumed
             c->stats.count_bytes += 9 * mc;   // 8 B edge read + 1 B tentative-label gather
             c->kernels++;
         }
@@ -729,6 +743,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     ensure_chunk(c, nc_cap, 0);
     CK(cudaMemsetAsync(c->lab.p, 0xFF, a.n, s));
     CK(cudaMemsetAsync(c->lab2.p, 0, sizeof(uint32_t) * (a.n / 16 + 2), s));
+    CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));
     CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
     CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
     CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
