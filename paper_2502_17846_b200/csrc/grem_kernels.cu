@@ -2303,27 +2303,6 @@ __device__ __forceinline__ uint32_t side_newid(const uint32_t* __restrict__ bits
     uint32_t r1 = side_rank1(bits, pre, g);
     return side ? r1 : g - r1;
 }
-struct SideBitPred {
-    const uint32_t* bits;
-    uint32_t side;
-    __device__ __forceinline__ bool operator()(const uint2& ed) const {
-        return ((bits[ed.x >> 5] >> (ed.x & 31)) & 1u) == side && ((bits[ed.y >> 5] >> (ed.y & 31)) & 1u) == side;
-    }
-};
-size_t extract_bits_temp_bytes(int64_t m) {
-    size_t bytes = 0;
-    cub::DeviceSelect::If(nullptr, bytes, (const uint2*)nullptr, (uint2*)nullptr, (long long*)nullptr, (int)m,
-                          SideBitPred{nullptr, 0});
-    return bytes;
-}
-__global__ void k_remap_bits(uint2* e, const long long* cnt, const uint32_t* __restrict__ bits,
-                             const uint32_t* __restrict__ pre, int side) {
-    int64_t m = *cnt;
-    GRID_STRIDE(i, m) {
-        uint2 ed = e[i];
-        e[i] = make_uint2(side_newid(bits, pre, ed.x, side), side_newid(bits, pre, ed.y, side));
-    }
-}
 __global__ void k_sub_orig_bits(const int8_t* __restrict__ lab, int64_t n, int side, const uint32_t* __restrict__ bits,
                                 const uint32_t* __restrict__ pre, const int32_t* __restrict__ orig,
                                 int32_t* __restrict__ sub) {
@@ -2335,11 +2314,142 @@ void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wp
     k_side_bits<<<grid_for(nw, 256), 256, 0, s>>>(lab, n, bits, wpop, nw);
     cub::DeviceScan::ExclusiveSum(temp, temp_bytes, wpop, pre, (int)(nw + 1), s);
 }
-void launch_extract_bits(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int side, uint2* out,
-                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s) {
-    cub::DeviceSelect::If(temp, temp_bytes, e, out, d_count, (int)m, SideBitPred{bits, (uint32_t)side}, s);
-    k_remap_bits<<<grid_for(m, 256, 8), 256, 0, s>>>(out, d_count, bits, pre, side);
+// Both induced subgraphs (grem.py:255-274) in ONE pass over the edges:
+// per edge two 8-byte gathers of {side bits, rank prefix} words (L2-resident),
+// the edge goes to side 0, side 1 or is cut; order within a side stays the
+// file order through a tile-local ballot ranking plus a decoupled look-back
+// across tiles (dynamic tile ids, so waiting only ever targets started tiles).
+constexpr int kSplitT = 256;
+constexpr int kSplitI = 8;
+constexpr int kSplitTile = kSplitT * kSplitI;
+constexpr unsigned long long kLbAgg = 1ULL << 62, kLbInc = 2ULL << 62, kLbVal = (1ULL << 62) - 1;
+
+__global__ void k_word_info(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ pre, int64_t nw,
+                            uint2* __restrict__ wi) {
+    GRID_STRIDE(w, nw) wi[w] = make_uint2(bits[w], pre[w]);
 }
+
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+// warp-cooperative look-back: exclusive prefix of tile t's value
+__device__ unsigned long long lb_prefix(unsigned long long* status, int64_t t) {
+    int lane = threadIdx.x & 31;
+    unsigned long long acc = 0;
+    int64_t j = t - 1;
+    while (j >= 0) {
+        int64_t q = j - lane;
+        unsigned long long st = 0;
+        if (q >= 0) {
+            do { st = lb_load(status + q); } while ((st >> 62) == 0);
+        } else {
+            st = kLbInc;   // before tile 0: an inclusive zero
+        }
+        unsigned inc = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        int stop = inc ? __ffs(inc) - 1 : 32;
+        unsigned long long v = lane <= stop ? (st & kLbVal) : 0;
+        for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        acc += __shfl_sync(0xffffffffu, v, 0);
+        if (inc) break;
+        j -= 32;
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kSplitT) k_split_edges(const uint2* __restrict__ e, int64_t m,
+                                                         const uint2* __restrict__ wi, uint2* __restrict__ out0,
+                                                         uint2* __restrict__ out1, unsigned long long* status0,
+                                                         unsigned long long* status1, unsigned int* ticket,
+                                                         long long* counts, int64_t ntiles) {
+    __shared__ int64_t s_tile;
+    __shared__ uint32_t s_c[2][kSplitI][kSplitT / 32];
+    __shared__ unsigned long long s_pre[2];
+    constexpr int NW = kSplitT / 32;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    int64_t t = s_tile;
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t base = t * kSplitTile;
+    uint2 ed[kSplitI];
+    int side[kSplitI];
+    uint32_t rank[kSplitI];
+#pragma unroll
+    for (int k = 0; k < kSplitI; ++k) {
+        int64_t i = base + (int64_t)k * kSplitT + threadIdx.x;   // warp-striped: coalesced loads
+        side[k] = 2;
+        if (i < m) {
+            uint2 d = e[i];
+            uint2 a = wi[d.x >> 5], b = wi[d.y >> 5];
+            uint32_t su = (a.x >> (d.x & 31)) & 1u, sv = (b.x >> (d.y & 31)) & 1u;
+            if (su == sv) {
+                uint32_t r1u = a.y + __popc(a.x & ((1u << (d.x & 31)) - 1u));
+                uint32_t r1v = b.y + __popc(b.x & ((1u << (d.y & 31)) - 1u));
+                side[k] = (int)su;
+                ed[k] = su ? make_uint2(r1u, r1v) : make_uint2(d.x - r1u, d.y - r1v);
+            }
+        }
+        unsigned b0 = __ballot_sync(0xffffffffu, side[k] == 0), b1 = __ballot_sync(0xffffffffu, side[k] == 1);
+        unsigned lt = (1u << lane) - 1u;
+        rank[k] = side[k] == 0 ? __popc(b0 & lt) : __popc(b1 & lt);
+        if (lane == 0) {
+            s_c[0][k][wid] = __popc(b0);
+            s_c[1][k][wid] = __popc(b1);
+        }
+    }
+    __syncthreads();
+    // exclusive prefix over (k, warp) in edge order, per side; warps 0/1 own sides 0/1
+    if (wid < 2) {
+        int sd = wid;
+        constexpr int NE = kSplitI * NW;   // 64 entries
+        uint32_t v0 = s_c[sd][(2 * lane) / NW][(2 * lane) % NW];
+        uint32_t v1 = s_c[sd][(2 * lane + 1) / NW][(2 * lane + 1) % NW];
+        uint32_t pair = v0 + v1, incl = pair;
+        for (int off = 1; off < 32; off <<= 1) {
+            uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        uint32_t excl = incl - pair;
+        static_assert(NE == 64, "two entries per lane");
+        __syncwarp();
+        s_c[sd][(2 * lane) / NW][(2 * lane) % NW] = excl;
+        s_c[sd][(2 * lane + 1) / NW][(2 * lane + 1) % NW] = excl + v0;
+        uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long* status = sd ? status1 : status0;
+        unsigned long long prefix = 0;
+        if (t == 0) {
+            if (lane == 0) atomicExch(status, kLbInc | total);
+        } else {
+            if (lane == 0) atomicExch(status + t, kLbAgg | total);
+            prefix = lb_prefix(status, t);
+            if (lane == 0) atomicExch(status + t, kLbInc | (prefix + total));
+        }
+        if (lane == 0) {
+            s_pre[sd] = prefix;
+            if (t == ntiles - 1) counts[sd] = (long long)(prefix + total);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSplitI; ++k) {
+        if (side[k] == 2) continue;
+        unsigned long long p = s_pre[side[k]] + s_c[side[k]][k][wid] + rank[k];
+        (side[k] ? out1 : out0)[p] = ed[k];
+    }
+}
+size_t split_edges_tiles(int64_t m) { return (size_t)((m + kSplitTile - 1) / kSplitTile); }
+void launch_split_edges(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int64_t nw, uint2* wi,
+                        uint2* out0, uint2* out1, unsigned long long* status, unsigned int* ticket, long long* counts,
+                        cudaStream_t s) {
+    int64_t ntiles = (int64_t)split_edges_tiles(m);
+    k_word_info<<<grid_for(nw, 256), 256, 0, s>>>(bits, pre, nw, wi);
+    cudaMemsetAsync(counts, 0, 2 * sizeof(long long), s);
+    if (ntiles == 0) return;
+    cudaMemsetAsync(status, 0, sizeof(unsigned long long) * 2 * ntiles, s);
+    cudaMemsetAsync(ticket, 0, sizeof(unsigned int), s);
+    k_split_edges<<<(unsigned)ntiles, kSplitT, 0, s>>>(e, m, wi, out0, out1, status, status + ntiles, ticket, counts,
+                                                       ntiles);
+}
+
 void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t* bits, const uint32_t* pre,
                           const int32_t* orig, int32_t* sub, cudaStream_t s) {
     k_sub_orig_bits<<<grid_for(n, 256), 256, 0, s>>>(lab, n, side, bits, pre, orig, sub);

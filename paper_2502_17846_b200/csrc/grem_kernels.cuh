@@ -211,9 +211,10 @@ void launch_iota(int32_t* a, int64_t n, cudaStream_t s);
 // succinct side maps for the recursion (preferred path)
 void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wpop, uint32_t* pre, void* temp,
                       size_t temp_bytes, cudaStream_t s);
-size_t extract_bits_temp_bytes(int64_t m);
-void launch_extract_bits(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int side, uint2* out,
-                         long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s);
+size_t split_edges_tiles(int64_t m);
+void launch_split_edges(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int64_t nw, uint2* wi,
+                        uint2* out0, uint2* out1, unsigned long long* status, unsigned int* ticket, long long* counts,
+                        cudaStream_t s);
 void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t* bits, const uint32_t* pre,
                           const int32_t* orig, int32_t* sub, cudaStream_t s);
 // cut count with labels packed to 2^lb bits (d_neg gets bit 1 on negative labels)

@@ -156,7 +156,10 @@ struct grem_ctx {
     DBuf<int32_t> lab32;
     DBuf<uint32_t> packed_lab{"packed_lab"}, side_bits{"side_bits"}, side_pop{"side_pop"}, side_pre{"side_pre"};
     // recursion arena: per-level induced-subgraph buffers (reused across calls)
-    DBuf<uint2> rec_e[40];
+    DBuf<uint2> rec_e[40], rec_e1[40];
+    DBuf<uint2> word_info{"word_info"};
+    DBuf<unsigned long long> lb_status{"lb_status"};
+    DBuf<unsigned int> lb_ticket{"lb_ticket"};
     DBuf<int32_t> rec_o[40];
     DBuf<int32_t> part_fin{"part_fin"}, part_orig{"part_orig"};
     // live state for hooks
@@ -1090,42 +1093,43 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         c->kernels++;
         return;
     }
-    // extract both sides
+    // extract both sides: one pass over the edges writes both induced subgraphs
     c->rec_e[level].ensure(m > 0 ? m : 1, s);
+    c->rec_e1[level].ensure(m > 0 ? m : 1, s);
     c->rec_o[level].ensure(n, s);
-    uint2* sub_e = c->rec_e[level].p;
+    uint2* side_e[2] = {c->rec_e[level].p, c->rec_e1[level].p};
     int32_t* sub_o = c->rec_o[level].p;
     int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
-    ensure_temp(c, extract_bits_temp_bytes(m > 0 ? m : 1));
     int64_t nw = (n + 31) / 32;
     c->side_bits.ensure(nw + 2, s);
     c->side_pop.ensure(nw + 2, s);
     c->side_pre.ensure(nw + 2, s);
+    c->word_info.ensure(nw + 2, s);
+    c->lb_status.ensure(2 * (int64_t)split_edges_tiles(m) + 2, s);
+    c->lb_ticket.ensure(4, s);
     ensure_temp(c, scan_temp_bytes(nw + 2));
     {
         PhaseScope ps(c, PH_EXTRACT);
         CK(cudaMemsetAsync(c->side_pop.p + nw, 0, sizeof(uint32_t), s));
         launch_side_bits(c->lab.p, n, c->side_bits.p, c->side_pop.p, c->side_pre.p, c->temp.p, c->temp.cap, s);
+        launch_split_edges(e, m, c->side_bits.p, c->side_pre.p, nw, c->word_info.p, side_e[0], side_e[1],
+                           c->lb_status.p, c->lb_ticket.p, c->d_scal + 6, s);
         CK(cudaMemcpyAsync(&c->h_pin[0], c->side_pre.p + nw, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&c->h_pin[1], c->d_scal + 6, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        c->kernels += 2;
+        c->kernels += 5;
     }
     uint32_t ones;
     memcpy(&ones, &c->h_pin[0], sizeof(uint32_t));
     n_off[1] = n - (int64_t)ones;
     n_off[2] = n;
-    for (int side = 0; side < 2; ++side) {
+    e_off[1] = c->h_pin[1];
+    e_off[2] = e_off[1] + c->h_pin[2];
+    {
         PhaseScope ps(c, PH_EXTRACT);
-        launch_sub_orig_bits(c->lab.p, n, side, c->side_bits.p, c->side_pre.p, orig, sub_o + n_off[side], s);
-        int64_t kept = 0;
-        if (m > 0) {
-            launch_extract_bits(e, m, c->side_bits.p, c->side_pre.p, side, sub_e + e_off[side], c->d_scal + 7,
-                                c->temp.p, c->temp.cap, s);
-            scal_read(c, c->d_scal + 7, 1);
-            kept = c->h_pin[0];
-        }
-        c->kernels += 3;
-        e_off[side + 1] = e_off[side] + kept;
+        for (int side = 0; side < 2; ++side)
+            launch_sub_orig_bits(c->lab.p, n, side, c->side_bits.p, c->side_pre.p, orig, sub_o + n_off[side], s);
+        c->kernels += 2;
     }
     c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
     // split the owning ranks between the sides in proportion to their edges
@@ -1145,7 +1149,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         if (k == 0) return;   // grem.py:308-309
         if (pc.shard_rank < sr0[side] || pc.shard_rank >= sr1[side]) return;   // another rank's subtree
         int64_t base = leaf_base + side * (p_level / 2);
-        recurse(cc, pc, sub_e + e_off[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
+        recurse(cc, pc, side_e[side], e_off[side + 1] - e_off[side], k, sub_o + n_off[side], p_level / 2,
                 level + 1, base, sr0[side], sr1[side]);
     };
     (void)split;
@@ -1160,13 +1164,14 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, s));
-        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + p_level / 2));
+        int big = (e_off[1] - e_off[0]) >= (e_off[2] - e_off[1]) ? 0 : 1;   // stays on this context
+        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
         std::exception_ptr err = nullptr;
         std::thread th([&] {
             try {
                 CK(cudaSetDevice(ch->device));
                 CK(cudaStreamWaitEvent(ch->s, ready, 0));
-                side_call(ch, 1);
+                side_call(ch, 1 - big);
                 CK(cudaStreamSynchronize(ch->s));
             } catch (...) {
                 err = std::current_exception();
@@ -1175,7 +1180,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         });
         std::exception_ptr err0 = nullptr;
         try {
-            side_call(c, 0);
+            side_call(c, big);
         } catch (...) {
             err0 = std::current_exception();
         }
@@ -1310,6 +1315,7 @@ void grem_destroy(grem_ctx* c) {
     c->side_pre.release();
     for (int l = 0; l < 40; ++l) {
         c->rec_e[l].release();
+        c->rec_e1[l].release();
         c->rec_o[l].release();
     }
     c->part_fin.release();

@@ -14,7 +14,7 @@ for r in rows:
     name = d["Kernel Name"].split("(")[0].split("<")[0]
     v = float(d["Metric Value"].replace(",", ""))
     unit = d.get("Metric Unit", "nsecond")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1e-3)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}[unit]
     agg[name][0] += 1
     agg[name][1] += v * scale
 tot = sum(v[1] for v in agg.values())
