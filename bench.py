@@ -250,17 +250,32 @@ def main():
                "h2d_bytes_per_step": E * 8, "d2h_bytes_per_step": n * 4}
         del host
 
-    # roofline of the dominant streaming kernel (edge-count pass) and of the path
+    # roofline of the dominant HBM-streaming kernel, k_count_delta (one pass
+    # over a chunk's edges per fixpoint round; 9 algorithmic B/edge: 8 B edge
+    # read + 1 B label of the lower endpoint).  Its launches are timed with CUDA
+    # events on the library stream in a level-0 bisection (k=2: one stream, no
+    # concurrent sibling subtrees), right after the timed steps.
     peak, peak_kind = measured_peak()
-    cnt_ms, cnt_n = phases.get("count", (0.0, 0))
-    count_bytes = st.get("count_bytes", 0)
+    top = {kk: v for kk, v in phases.items() if "." not in kk}
     roof = None
-    if cnt_ms > 0:
-        per_step_count_bytes = count_bytes
-        achieved = per_step_count_bytes / (cnt_ms / args.steps / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": "k_count_init/k_count_delta (edge pass)", "achieved": achieved,
-                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
-                "share_of_step": cnt_ms / sum(v[0] for kk, v in phases.items() if "." not in kk)}
+    grem.set_profiling(True)
+    grem.partition_edges(None, n, 2, cfg, on_device_ptr=dptr.value, num_edges=E)
+    st_l0, ph_l0 = grem.last_stats(), grem.phase_times()
+    grem.set_profiling(False)
+    d_ms, d_n = ph_l0.get("count_delta", (0.0, 0))
+    if d_ms > 0 and d_n > 0:
+        achieved = st_l0["delta_bytes"] / (d_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["k_count_delta"]
+            traffic = tr["dram_bytes_per_launch"]
+        except Exception:  # noqa: BLE001
+            pass
+        roof = {"bound": "hbm", "kernel": "k_count_delta", "achieved": achieved, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": st_l0["delta_bytes"] / d_n, "launches_timed": d_n,
+                "avg_launch_ms": d_ms / d_n, "timed_in": f"{args.workload} level-0 bisection (k=2), CUDA events",
+                "share_of_step": top.get("count_delta", (0.0, 0))[0] / max(1e-9, sum(v[0] for v in top.values()))}
     path_bytes = st.get("path_bytes")
     roof_path = None
     if path_bytes:

@@ -93,6 +93,7 @@ typedef struct {
     double ms_total;         /* device time of the call (CUDA events) */
     int64_t count_bytes;     /* algorithmic bytes of the edge count passes (10 B/edge init, 9 B/edge delta) */
     int64_t path_bytes;      /* algorithmic bytes of the whole call, SURVEY.md 8(d) formula */
+    int64_t delta_bytes;     /* the k_count_delta share of count_bytes (9 B/edge per launch) */
 } grem_stats;
 
 /* ------------------------------------------------------------------ life */

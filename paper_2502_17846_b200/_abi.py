@@ -46,7 +46,8 @@ class GremHooksC(ctypes.Structure):
 class GremStatsC(ctypes.Structure):
     _fields_ = [("chunks", c_i64), ("rounds", c_i64), ("max_rounds", c_i64), ("visits", c_i64),
                 ("walk_steps", c_i64), ("seed_bfs_levels", c_i64), ("bisections", c_i64),
-                ("kernels", c_i64), ("ms_total", c_dbl), ("count_bytes", c_i64), ("path_bytes", c_i64)]
+                ("kernels", c_i64), ("ms_total", c_dbl), ("count_bytes", c_i64), ("path_bytes", c_i64),
+                ("delta_bytes", c_i64)]
 
 
 # every exported symbol of include/grem_b200.h (tests check they all resolve)

@@ -547,11 +547,24 @@ __global__ void __launch_bounds__(256) k_bin_apply(const uint32_t* __restrict__ 
         __syncthreads();
         if (base >= total) break;
         int64_t end = base + kApplyItem < total ? base + kApplyItem : total;
-        for (int64_t i = base + threadIdx.x; i < end; i += blockDim.x) {
-            uint32_t r = recs[i];
-            uint32_t node = r >> 2, c = r & 3u;
-            if (c == 1) atomicAdd(&cnt[node], 1ULL);
-            else if (c == 2) atomicAdd(&cnt[node], 1ULL << 32);
+        // 8 records per thread from two 16-byte loads (all loads in flight
+        // before the REDs), items are 16-byte aligned
+        int64_t i0 = base + (int64_t)threadIdx.x * 8;
+        uint32_t r[8];
+        if (i0 + 8 <= end) {
+            uint4 a = *reinterpret_cast<const uint4*>(recs + i0), b = *reinterpret_cast<const uint4*>(recs + i0 + 4);
+            r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = i0 + j < end ? recs[i0 + j] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (r[j] == 0xFFFFFFFFu) continue;
+            uint32_t node = r[j] >> 2, c = r[j] & 3u;
+            // 32-bit REDs on the halves of the packed counter (c0 low, c1 high word)
+            if (c == 1) atomicAdd(reinterpret_cast<unsigned int*>(cnt + node), 1u);
+            else if (c == 2) atomicAdd(reinterpret_cast<unsigned int*>(cnt + node) + 1, 1u);
             else flag[node] = 1;
         }
     }
@@ -2259,6 +2272,25 @@ __global__ void k_max_id(const uint2* __restrict__ e, int64_t m, uint32_t* mx) {
     }
     for (int off = 16; off; off >>= 1) v = max(v, __shfl_down_sync(0xffffffffu, v, off));
     if ((threadIdx.x & 31) == 0) atomicMax(mx, v);
+}
+// ingest piece check (edgefile.py:63-65): endpoints >= n are recorded (max)
+// and replaced by 0 so that kernels that run before the host sees the error
+// stay in bounds; the call then fails with the reference's FormatError.
+__global__ void k_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max) {
+    uint32_t v = 0;
+    bool any = false;
+    GRID_STRIDE(i, m) {
+        uint2 ed = e[i];
+        if (ed.x >= n || ed.y >= n) {
+            v = max(v, max(ed.x, ed.y));
+            any = true;
+            e[i] = make_uint2(ed.x >= n ? 0u : ed.x, ed.y >= n ? 0u : ed.y);
+        }
+    }
+    if (any) atomicMax(bad_max, v + 1);   // 0 = no bad endpoint
+}
+void launch_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max, cudaStream_t s) {
+    if (m > 0) k_check_piece<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, n, bad_max);
 }
 void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_t s) {
     if (m > 0) k_max_id<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, d_max_id);

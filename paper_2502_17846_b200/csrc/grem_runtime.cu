@@ -83,12 +83,12 @@ struct DBuf {
 // (enabled per call by grem_set_profiling); elapsed times are folded in after
 // the call's final synchronisation.
 enum Phase {
-    PH_COUNT = 0, PH_SELECT, PH_NODE, PH_PREFS, PH_SCAN, PH_BUNDLE, PH_DECIDE, PH_COMMIT,
+    PH_COUNT = 0, PH_SELECT, PH_NODE, PH_DELTA, PH_SCAN, PH_BUNDLE, PH_COMMIT,
     PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_HUBS,
     PH_SEED_CSR, PH_SEED_CC, PH_SEED_BFS, PH_SEED_REFINE, PH_SEED_COMMIT,   // inside "seed"
     PH_N
 };
-static const char* kPhaseNames[PH_N] = {"count", "select", "node_init", "prefs", "scan", "bundle", "decide",
+static const char* kPhaseNames[PH_N] = {"count_init", "select", "node_init", "count_delta", "scan", "bundle",
                                         "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs",
                                         "seed.csr", "seed.cc", "seed.bfs", "seed.refine", "seed.commit"};
 
@@ -143,6 +143,18 @@ struct grem_ctx {
     long long* d_sizes = nullptr;   // [2]
     long long* d_scal = nullptr;    // [8]
     long long* d_sscal = nullptr;   // [16] seed scalars
+    // overlapped ingest of a page-locked host edge list: pieces copied on
+    // copy_s, each checked and marked with an event; consumers wait only for
+    // the pieces covering the edges they read
+    cudaStream_t copy_s = nullptr;
+    struct IngestMark {
+        int64_t end;
+        cudaEvent_t ev;
+    };
+    std::vector<IngestMark> ingest;
+    const uint2* ingest_base = nullptr;
+    int64_t ingest_m = 0, ingest_n = 0;
+    uint32_t* d_bad = nullptr;
     long long* h_pin = nullptr;     // [32] pinned mirror
     // cub temp
     DBuf<unsigned char> temp{"temp"};
@@ -309,6 +321,9 @@ void ensure_seed(grem_ctx* c, int64_t nc, int64_t entries) {
     ensure_temp(c, sort_temp_bytes(nc));
     ensure_temp(c, scan_temp_bytes(nc + 1));
 }
+
+void ingest_wait(grem_ctx* c, const uint2* end);
+void ingest_wait_all(grem_ctx* c);
 
 ChunkBufs chunk_bufs(grem_ctx* c) {
     ChunkBufs b;
@@ -595,10 +610,11 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     for (int r = 1;; ++r) {
         rounds++;
         if (r > 1) {
-            PhaseScope ps(c, PH_COUNT);
+            PhaseScope ps(c, PH_DELTA);
             launch_count_delta(e, mc, b, s);
             CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));   // consumed
             c->stats.count_bytes += 9 * mc;   // 8 B edge read + 1 B tentative-label gather
+            c->stats.delta_bytes += 9 * mc;
             c->kernels++;
         }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
@@ -678,6 +694,7 @@ void detect_hubs(grem_ctx* c, const BisectArgs& a) {
     cudaStream_t s = c->s;
     PhaseScope ps(c, PH_HUBS);
     int64_t S = a.m < (1LL << 22) ? a.m : (1LL << 22);
+    ingest_wait(c, a.e + S);
     CK(cudaMemsetAsync(c->scratch.p, 0, sizeof(int32_t) * a.n, s));
     launch_sample_degrees(a.e, S, c->scratch.p, s);
     c->hub_ids.ensure(1 << 20, c->s);
@@ -761,6 +778,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
             int64_t mc = a.m - lo < a.chunk ? a.m - lo : a.chunk;
             meter.on_chunk(mc);
             const uint2* e = a.e + lo;
+            ingest_wait(c, e + mc);
             if (pass == 0 && ci == 0) {
                 PhaseScope ps(c, PH_SEED);
                 seed_chunk(c, a, e, mc);
@@ -806,6 +824,7 @@ void validate_cfg(const grem_config* cfg) {
 // count_cuts on device edges / int32 device labels
 void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, int64_t n, grem_report* rep) {
     cudaStream_t s = c->s;
+    ingest_wait_all(c);
     int64_t cap = rep && rep->sizes_cap > 0 ? rep->sizes_cap : 2;
     if (cap < 2) cap = 2;
     c->cc_sizes.ensure(cap + 4, c->s);
@@ -888,7 +907,44 @@ void staged_upload(grem_ctx* c, void* dst, uint64_t total, Fill fill) {
     CK(cudaStreamSynchronize(c->s));
 }
 
-const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device) {
+// make c->s wait until the ingested edges [base, end) are resident and checked
+void ingest_wait(grem_ctx* c, const uint2* end) {
+    if (c->ingest.empty() || end <= c->ingest_base || end > c->ingest_base + c->ingest_m) return;
+    int64_t idx = end - c->ingest_base;
+    for (auto& mk : c->ingest)
+        if (mk.end >= idx) {
+            CK(cudaStreamWaitEvent(c->s, mk.ev, 0));
+            return;
+        }
+}
+void ingest_wait_all(grem_ctx* c) {
+    if (!c->ingest.empty()) CK(cudaStreamWaitEvent(c->s, c->ingest.back().ev, 0));
+}
+// end of a call: every piece consumed; raise the reference's FormatError if an
+// endpoint was out of range (edgefile.py:63-65)
+void ingest_finish(grem_ctx* c) {
+    if (c->ingest.empty()) return;
+    ingest_wait_all(c);
+    uint32_t bad = 0;
+    CK(cudaMemcpyAsync(&c->h_pin[0], c->d_bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    memcpy(&bad, &c->h_pin[0], sizeof(uint32_t));
+    for (auto& mk : c->ingest) cudaEventDestroy(mk.ev);
+    c->ingest.clear();
+    int64_t n = c->ingest_n;
+    c->ingest_base = nullptr;
+    if (bad)
+        fail(GREM_E_FORMAT, "edge endpoint " + std::to_string((int64_t)bad - 1) + " >= num_nodes " + std::to_string(n));
+}
+void ingest_abort(grem_ctx* c) {
+    if (c->copy_s) cudaStreamSynchronize(c->copy_s);
+    for (auto& mk : c->ingest) cudaEventDestroy(mk.ev);
+    c->ingest.clear();
+    c->ingest_base = nullptr;
+}
+
+const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device,
+                         bool overlap = false) {
     if (n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
     if (n >= (1LL << 31)) fail(GREM_E_FORMAT, "num_nodes >= 2^31 is not supported by the GPU path");
     const uint2* d;
@@ -899,7 +955,31 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
         cudaPointerAttributes at{};
         bool pinned = cudaPointerGetAttributes(&at, edges) == cudaSuccess && at.type == cudaMemoryTypeHost;
         cudaGetLastError();
-        if (pinned) {   // page-locked source: DMA straight into HBM
+        if (pinned && overlap) {   // page-locked source: DMA pieces overlapped with the first bisection
+            if (!c->copy_s) CK(cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking));
+            if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(uint32_t)));
+            cudaEvent_t ready;
+            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(ready, c->s));   // the buffer's stream-ordered allocation
+            CK(cudaStreamWaitEvent(c->copy_s, ready, 0));
+            cudaEventDestroy(ready);
+            CK(cudaMemsetAsync(c->d_bad, 0, sizeof(uint32_t), c->copy_s));
+            const int64_t piece = 1LL << 24;   // 128 MB of edges per DMA
+            uint2* dst = c->edges_owned.p;
+            for (int64_t off = 0; off < m; off += piece) {
+                int64_t cnt = m - off < piece ? m - off : piece;
+                CK(cudaMemcpyAsync(dst + off, edges + 2 * off, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->copy_s));
+                launch_check_piece(dst + off, cnt, (uint32_t)n, c->d_bad, c->copy_s);
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, c->copy_s));
+                c->ingest.push_back({off + cnt, ev});
+            }
+            c->ingest_base = dst;
+            c->ingest_m = m;
+            c->ingest_n = n;
+            return dst;
+        } else if (pinned) {   // page-locked source: DMA straight into HBM
             PhaseScope ps(c, PH_INGEST);
             CK(cudaMemcpyAsync(c->edges_owned.p, edges, (size_t)m * 8, cudaMemcpyHostToDevice, c->s));
             CK(cudaStreamSynchronize(c->s));
@@ -1047,6 +1127,7 @@ void ctx_release(grem_ctx* parent, grem_ctx* ch) {
     parent->stats.seed_bfs_levels += ch->stats.seed_bfs_levels;
     parent->stats.bisections += ch->stats.bisections;
     parent->stats.count_bytes += ch->stats.count_bytes;
+    parent->stats.delta_bytes += ch->stats.delta_bytes;
     parent->stats.path_bytes += ch->stats.path_bytes;
     parent->kernels += ch->kernels;
     for (int k = 0; k < PH_N; ++k) {
@@ -1093,6 +1174,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         c->kernels++;
         return;
     }
+    ingest_wait_all(c);
     // extract both sides: one pass over the edges writes both induced subgraphs
     c->rec_e[level].ensure(m > 0 ? m : 1, s);
     c->rec_e1[level].ensure(m > 0 ? m : 1, s);
@@ -1242,6 +1324,7 @@ int guarded(grem_ctx* c, F f) {
         }
         f();
         if (c) {
+            ingest_finish(c);
             CK(cudaEventRecord(c->ev1, c->s));
             CK(cudaEventSynchronize(c->ev1));
             float ms = 0;
@@ -1253,10 +1336,14 @@ int guarded(grem_ctx* c, F f) {
         return GREM_OK;
     } catch (const GremError& e) {
         g_err = e.msg;
-        if (c) cudaStreamSynchronize(c->s);
+        if (c) {
+            cudaStreamSynchronize(c->s);
+            ingest_abort(c);
+        }
         return e.code;
     } catch (const std::exception& e) {
         g_err = e.what();
+        if (c) ingest_abort(c);
         return GREM_E_NOMEM;
     }
 }
@@ -1332,6 +1419,8 @@ void grem_destroy(grem_ctx* c) {
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->s) cudaStreamDestroy(c->s);
+    if (c->copy_s) cudaStreamDestroy(c->copy_s);
+    if (c->d_bad) cudaFree(c->d_bad);
     delete c;
 }
 
@@ -1362,7 +1451,7 @@ int grem_bisect_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, in
                     int64_t capacity, const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
     if (!c || !cfg) return GREM_E_FORMAT;
     return guarded(c, [&] {
-        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        const uint2* d = stage_edges(c, edges, m, n, on_device, true);
         bisect_entry(c, d, m, n, cfg, capacity, hooks, labels_out, rep);
     });
 }
@@ -1373,7 +1462,7 @@ int grem_partition_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n,
     return guarded(c, [&] {
         if (p < 2 || (p & (p - 1)) != 0)
             fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
-        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        const uint2* d = stage_edges(c, edges, m, n, on_device, true);
         partition_entry(c, d, m, n, p, cfg, hooks, labels_out, rep);
     });
 }
@@ -1384,7 +1473,7 @@ int grem_partition_shard_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int6
     return guarded(c, [&] {
         if (p < 2 || (p & (p - 1)) != 0)
             fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
-        const uint2* d = stage_edges(c, edges, m, n, on_device);
+        const uint2* d = stage_edges(c, edges, m, n, on_device, true);
         partition_entry(c, d, m, n, p, cfg, nullptr, labels_out, nullptr, rank, world);
     });
 }

@@ -279,15 +279,17 @@ print("poison ok")
     assert r.returncode == 0 and "poison ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_papers100m_k16_golden(golden_dir):
-    """papers100M-shaped 111M nodes / 1.6B edges, k=16, edges generated on the
-    device (bit-identical to the host generator): labels sha256 and report
-    pinned by the C oracle (51 min single-thread run, tests/golden)."""
+@pytest.mark.parametrize("key", ["papers100m_k16", "friendster_k16"])
+def test_big_shapes_k16_golden(golden_dir, key):
+    """papers100M-shaped 111M nodes / 1.6B edges and Friendster-shaped 65.6M
+    nodes / 1.8B edges, k=16, edges generated on the device (bit-identical to
+    the host generator): labels sha256 and report pinned by the C oracle
+    (51 / 53 min single-thread runs, tests/golden)."""
     import ctypes
     import hashlib
     from paper_2502_17846_b200 import _abi
-    gs = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))["papers100m_k16"]
-    s = synth.SHAPES["papers100m"]
+    gs = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))[key]
+    s = synth.SHAPES[gs["shape"]]
     L = _abi.lib()
     ctx = grem.context()
     ptr = ctypes.c_void_p()
@@ -300,3 +302,26 @@ def test_papers100m_k16_golden(golden_dir):
         L.grem_device_free(ctx, ptr)
     assert hashlib.sha256(lab.astype("<i4").tobytes()).hexdigest() == gs["labels_sha256"]
     assert rep.cut_edges == gs["cut_edges"] and list(rep.partition_sizes) == gs["partition_sizes"]
+
+
+def test_pinned_host_edges_overlapped_ingest():
+    """Page-locked host edges are uploaded in pieces overlapped with the first
+    bisection: same labels as device-resident edges, and an out-of-range
+    endpoint still raises the reference's FormatError (edgefile.py:63-65)."""
+    import torch
+    s = synth.SHAPES["arxiv"]
+    e = np.ascontiguousarray(synth.shape_edges(s).astype(np.uint32))
+    ref, rep = grem.partition_edges(e, s.num_nodes, 8, GremConfig(chunk_frac=0.1))
+    pinned = torch.empty(e.shape, dtype=torch.int32, pin_memory=True)
+    pv = pinned.numpy().view(np.uint32)
+    pv[:] = e
+    lab, rep2 = grem.partition_edges(pv, s.num_nodes, 8, GremConfig(chunk_frac=0.1))
+    assert np.array_equal(lab, ref) and rep2.cut_edges == rep.cut_edges
+    lab_b, _ = grem.bisect_edges(pv, s.num_nodes, GremConfig(chunk_frac=0.05))
+    assert np.array_equal(lab_b, grem.bisect_edges(e, s.num_nodes, GremConfig(chunk_frac=0.05))[0])
+    pv[len(pv) // 2, 1] = s.num_nodes + 7
+    with pytest.raises(FormatError, match=str(s.num_nodes + 7)):
+        grem.partition_edges(pv, s.num_nodes, 8, GremConfig(chunk_frac=0.1))
+    pv[len(pv) // 2, 1] = 0
+    lab3, _ = grem.partition_edges(e, s.num_nodes, 8, GremConfig(chunk_frac=0.1))   # context still healthy
+    assert np.array_equal(lab3, ref)
