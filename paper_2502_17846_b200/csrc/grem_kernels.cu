@@ -1324,10 +1324,33 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
             e = hi;
             cur = xin[seg];
         }
-        for (int64_t i = a; i < e; ++i) {
-            x[i] = (int32_t)cur;
-            if (xalt) xalt[i] = (int32_t)cur;
-            cur = bundle_step(cur, bp[i]);
+        if (e - a == kCkpt) {
+            // a full interval (256-byte aligned): all 64 params in flight at
+            // once, the chain in registers, 16-byte stores
+            static_assert(kCkpt == 64, "interval = 16 x int4");
+            int32_t xs[kCkpt];
+#pragma unroll
+            for (int q = 0; q < kCkpt / 4; ++q) {
+                int4 p4 = __ldg(reinterpret_cast<const int4*>(bp + a) + q);
+                int32_t pk[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    xs[q * 4 + j] = (int32_t)cur;
+                    cur = bundle_step(cur, pk[j]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kCkpt / 4; ++q) {
+                int4 v = make_int4(xs[4 * q], xs[4 * q + 1], xs[4 * q + 2], xs[4 * q + 3]);
+                reinterpret_cast<int4*>(x + a)[q] = v;
+                if (xalt) reinterpret_cast<int4*>(xalt + a)[q] = v;
+            }
+        } else {
+            for (int64_t i = a; i < e; ++i) {
+                x[i] = (int32_t)cur;
+                if (xalt) xalt[i] = (int32_t)cur;
+                cur = bundle_step(cur, bp[i]);
+            }
         }
         if (e == nc) {
             x[nc] = (int32_t)cur;
