@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
                                                               const uint32_t* __restrict__ chg,
                                                               const int32_t* __restrict__ pos,
                                                               unsigned long long* __restrict__ cntc,
-                                                              const uint32_t* __restrict__ hub_keys) {
+                                                              const uint32_t* __restrict__ hub_keys,
+                                                              const long long* __restrict__ gate) {
+    if (gate && *gate == 0) return;   // previous round changed nothing (converged)
     __shared__ uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
     hub_load(s_keys, hub_keys);
@@ -378,7 +380,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys);
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate);
 }
 
 // -------------------------------------------------- binned round-1 counting
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_bin_count(const uint2* __restr
     __shared__ uint32_t s_keys[kHubSlots];
     __shared__ unsigned int s_hist[kMaxBins];
     hub_load(s_keys, hub_keys);
-    for (int k = threadIdx.x; k < kMaxBins; k += blockDim.x) s_hist[k] = 0;
+    for (int k = threadIdx.x; k < nbins; k += blockDim.x) s_hist[k] = 0;
     __syncthreads();
     int64_t lo, hi;
     cta_range(m, lo, hi);
@@ -406,185 +408,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_bin_count(const uint2* __restr
         if (s_hist[k]) atomicAdd(&bin_count[k], s_hist[k]);
 }
 
-__global__ void k_bin_offsets(unsigned int* bin_count, unsigned int* bin_cur, int nbins) {
-    if (threadIdx.x == 0) {
-        unsigned int acc = 0;
-        for (int b = 0; b < nbins; ++b) {
-            unsigned int c = bin_count[b];
-            bin_cur[b] = acc;
-            acc += c;
-        }
-        bin_count[kMaxBins] = acc;   // total records
-    }
-}
-
-constexpr int kBinBatch = 4096;                  // edges per CTA batch (<= 2 records each)
-constexpr size_t kBinSmem = (size_t)kHubSlots * (4 + 8 + 1) + (size_t)kMaxBins * 4 * 4 + (size_t)2 * kBinBatch * 4 * 2 + 16;
-
-__global__ void __launch_bounds__(kEdgeThreads) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
-                                                              const uint32_t* __restrict__ lab2,
-                                                              const uint32_t* __restrict__ hub_keys, int shift,
-                                                              int nbins, unsigned int* __restrict__ bin_cur,
-                                                              uint32_t* __restrict__ recs,
-                                                              unsigned long long* __restrict__ cnt,
-                                                              uint8_t* __restrict__ flag) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(smem_raw);
-    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_cnt + kHubSlots);
-    unsigned int* s_hist = s_keys + kHubSlots;
-    unsigned int* s_start = s_hist + kMaxBins;
-    unsigned int* s_fill = s_start + kMaxBins;
-    unsigned int* s_base = s_fill + kMaxBins;
-    uint32_t* s_rec = s_base + kMaxBins;
-    uint32_t* s_out = s_rec + 2 * kBinBatch;
-    unsigned int* s_n = s_out + 2 * kBinBatch;
-    uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_n + 4);
-    hub_load(s_keys, hub_keys);
-    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
-        s_cnt[k] = 0ULL;
-        s_flag[k] = 0;
-    }
-    int64_t lo, hi;
-    cta_range(m, lo, hi);
-    for (int64_t b0 = lo; b0 < hi; b0 += kBinBatch) {
-        int64_t b1 = b0 + kBinBatch < hi ? b0 + kBinBatch : hi;
-        for (int k = threadIdx.x; k < nbins; k += blockDim.x) {
-            s_hist[k] = 0;
-            s_fill[k] = 0;
-        }
-        if (threadIdx.x == 0) *s_n = 0;
-        __syncthreads();
-        // records: node << 2 | code (1: +c0, 2: +c1, 0: unassigned neighbour, 3: self-loop)
-        for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-            uint2 ed = e[i];
-            uint32_t u = ed.x, v = ed.y;
-            int hu = hub_find(s_keys, u);
-            if (u == v) {
-                if (hu >= 0) s_flag[hu] = 1;
-                else {
-                    unsigned int p = atomicAdd(s_n, 1u);
-                    s_rec[p] = (u << 2) | 3u;
-                    atomicAdd(&s_hist[u >> shift], 1u);
-                }
-                continue;
-            }
-            int hv = hub_find(s_keys, v);
-            uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
-            if (hu >= 0) {
-                if (cv) atomicAdd(&s_cnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
-                else s_flag[hu] = 1;
-            } else {
-                unsigned int p = atomicAdd(s_n, 1u);
-                s_rec[p] = (u << 2) | cv;
-                atomicAdd(&s_hist[u >> shift], 1u);
-            }
-            if (hv >= 0) {
-                if (cu) atomicAdd(&s_cnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
-                else s_flag[hv] = 1;
-            } else {
-                unsigned int p = atomicAdd(s_n, 1u);
-                s_rec[p] = (v << 2) | cu;
-                atomicAdd(&s_hist[v >> shift], 1u);
-            }
-        }
-        __syncthreads();
-        // block counting sort by bin: starts (exclusive scan) and global reservations
-        if (threadIdx.x < 32) {
-            unsigned int carry = 0;
-            for (int c0 = 0; c0 < nbins; c0 += 32) {
-                int k = c0 + threadIdx.x;
-                unsigned int v = k < nbins ? s_hist[k] : 0u;
-                unsigned int incl = v;
-                for (int off = 1; off < 32; off <<= 1) {
-                    unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
-                    if ((int)threadIdx.x >= off) incl += o;
-                }
-                if (k < nbins) {
-                    s_start[k] = carry + incl - v;
-                    s_base[k] = v ? atomicAdd(&bin_cur[k], v) : 0u;
-                }
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-        }
-        __syncthreads();
-        unsigned int nrec = *s_n;
-        for (unsigned int k = threadIdx.x; k < nrec; k += blockDim.x) {
-            uint32_t r = s_rec[k];
-            unsigned int bb = (r >> 2) >> shift;
-            s_out[s_start[bb] + atomicAdd(&s_fill[bb], 1u)] = r;
-        }
-        __syncthreads();
-        for (unsigned int k = threadIdx.x; k < nrec; k += blockDim.x) {   // runs of a bin are contiguous
-            uint32_t r = s_out[k];
-            unsigned int bb = (r >> 2) >> shift;
-            recs[s_base[bb] + (k - s_start[bb])] = r;
-        }
-        __syncthreads();
-    }
-    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
-        uint32_t key = s_keys[k];
-        if (key == kHubEmpty) continue;
-        if (s_cnt[k]) atomicAdd(&cnt[key], s_cnt[k]);
-        if (s_flag[k]) flag[key] = 1;
-    }
-}
-
-// apply records bin by bin: work items are handed out in array order from a
-// global counter, so the whole GPU stays within ~one bin at a time and that
-// bin's counter slice is L2-hot (a grid-stride loop lets warps drift apart
-// across many bins and the REDs miss L2).
-constexpr int kApplyItem = 2048;
-__global__ void __launch_bounds__(256) k_bin_apply(const uint32_t* __restrict__ recs,
-                                                   const unsigned int* __restrict__ bin_count,
-                                                   unsigned long long* __restrict__ cnt, uint8_t* __restrict__ flag,
-                                                   unsigned int* __restrict__ work) {
-    __shared__ unsigned int s_item;
-    int64_t total = bin_count[kMaxBins];
-    while (true) {
-        if (threadIdx.x == 0) s_item = atomicAdd(work, 1u);
-        __syncthreads();
-        int64_t base = (int64_t)s_item * kApplyItem;
-        __syncthreads();
-        if (base >= total) break;
-        int64_t end = base + kApplyItem < total ? base + kApplyItem : total;
-        // 8 records per thread from two 16-byte loads (all loads in flight
-        // before the REDs), items are 16-byte aligned
-        int64_t i0 = base + (int64_t)threadIdx.x * 8;
-        uint32_t r[8];
-        if (i0 + 8 <= end) {
-            uint4 a = *reinterpret_cast<const uint4*>(recs + i0), b = *reinterpret_cast<const uint4*>(recs + i0 + 4);
-            r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = i0 + j < end ? recs[i0 + j] : 0xFFFFFFFFu;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (r[j] == 0xFFFFFFFFu) continue;
-            uint32_t node = r[j] >> 2, c = r[j] & 3u;
-            // 32-bit REDs on the halves of the packed counter (c0 low, c1 high word)
-            if (c == 1) atomicAdd(reinterpret_cast<unsigned int*>(cnt + node), 1u);
-            else if (c == 2) atomicAdd(reinterpret_cast<unsigned int*>(cnt + node) + 1, 1u);
-            else flag[node] = 1;
-        }
-    }
-}
-
-void launch_count_init_binned(const uint2* e, int64_t m, const ChunkBufs& b, const BinBufs& bb, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBinSmem);
-        attr = true;
-    }
-    cudaMemsetAsync(bb.bin_count, 0, sizeof(unsigned int) * (kMaxBins + 2), s);   // counts, total, apply cursor
-    k_bin_count<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.bin_count);
-    k_bin_offsets<<<1, 32, 0, s>>>(bb.bin_count, bb.bin_cur, bb.nbins);
-    unsigned grid = (unsigned)(num_sms() * 2);
-    k_bin_scatter<<<grid, kEdgeThreads, kBinSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.bin_cur,
-                                                     bb.recs, b.cnt, b.flag);
-    k_bin_apply<<<(unsigned)(num_sms() * 8), 256, 0, s>>>(bb.recs, bb.bin_count, b.cnt, b.flag,
-                                                        bb.bin_count + kMaxBins + 1);
-}
+// (bin offsets, scatter and the fused apply/compact are at the end of the file)
 
 // hub detection: endpoint histogram of a sample, candidates, top-K
 __global__ void k_sample_deg(const uint2* __restrict__ e, int64_t sample, int32_t* sdeg) {
@@ -832,6 +656,7 @@ struct RoundArgs {
     const long long* sizes;
     long long cap;
     int64_t nc;
+    const long long* gate;   // nullptr or the previous round's changed count (0: converged, skip)
 };
 
 __device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t* v) {
@@ -865,6 +690,7 @@ __device__ __forceinline__ long long node_sl(uint8_t m, int32_t nb) {
 }
 
 __global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_agg, int first_round) {
+    if (a.gate && *a.gate == 0) return;
     __shared__ Clamp smem[kRT / 32];
     __shared__ Clamp stotal;
     int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
@@ -910,6 +736,7 @@ struct RoundOut {
 };
 
 __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
+    if (a.gate && *a.gate == 0) return;
     __shared__ Clamp smem[kRT / 32];
     __shared__ long long sbad;
     if (threadIdx.x == 0) sbad = kInf;
@@ -974,11 +801,13 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     if (threadIdx.x == 0 && sbad != kInf) atomicMin(out.scal + 6, sbad);
 }
 
+__global__ void k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p, long long* tile_x,
+                                 const long long* gate);
 void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s) {
-    RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc};
+    RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc, first_round ? nullptr : b.gate};
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
-    k_scan_top<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x);
+    k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
     RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.scal};
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
 }
@@ -1037,7 +866,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce_gated(Src src, int
 }
 __global__ void __launch_bounds__(1024) k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p,
                                                          long long* tile_x, const long long* gate) {
-    if (*gate == 0) return;
+    if (gate && *gate == 0) return;
     __shared__ Clamp smem[32];
     int64_t per = (ntiles + 1023) / 1024;
     int64_t lo = (int64_t)threadIdx.x * per;
@@ -1462,6 +1291,14 @@ __global__ void k_commit(const uint32_t* __restrict__ nodes, int64_t nc, const u
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
     k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cntc, b.nbrc, b.nbr, b.lab, b.tlc, b.lab2);
 }
+
+// end of a round: the next round runs only if this one changed a label;
+// scal[8] counts the rounds that actually ran
+__global__ void k_round_gate(long long* scal) {
+    if (scal[7]) scal[8] += 1;
+    scal[7] = scal[1];
+}
+void launch_round_gate(const ChunkBufs& b, cudaStream_t s) { k_round_gate<<<1, 1, 0, s>>>(b.scal); }
 
 __global__ void k_sizes_update(long long* sizes, const int32_t* x, int64_t nc, const long long* total_new) {
     long long s0 = sizes[0] + sizes[1];
@@ -2661,5 +2498,332 @@ void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, ui
     p.perm_bits = perm_bits;
     k_gen<<<grid_for((int64_t)count, 256, 32), 256, 0, s>>>(p, e0, count, out);
 }
+
+
+// ===================================================== binned round-1 counts
+// Round 1 of a large chunk (cnt_nbrs with pre-sweep labels, grem.py:82-97,
+// plus the chunk node set np.unique, model.py:59) in three passes:
+//   k_bin_count    records per coarse bin (2^shift node ids);
+//   k_bin_scatter  per 8192-edge batch a block counting sort by coarse bin
+//                  (rank = smem atomic return), coalesced record runs out;
+//   k_bin_compact  one CTA per 2^kSubShift-node tile, in node order: smem
+//                  counters (smem atomics run ~12x faster than L2 REDs),
+//                  hub counts merged, chunk membership, block scan and a
+//                  decoupled look-back give the chunk index, and the compact
+//                  round state is written directly (no n-sized counters, no
+//                  select, no separate node init or scan).
+// Records: node << 2 | code (1: +c0, 2: +c1, 0: unassigned neighbour, 3: self-loop).
+
+__global__ void __launch_bounds__(1024) k_bin_offsets(const unsigned int* __restrict__ bin_count,
+                                                      unsigned int* __restrict__ bin_cur, int nbins) {
+    __shared__ unsigned int s_w[32];
+    int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    unsigned int v0 = 2 * t < nbins ? bin_count[2 * t] : 0u, v1 = 2 * t + 1 < nbins ? bin_count[2 * t + 1] : 0u;
+    unsigned int pr = v0 + v1, incl = pr;
+    for (int off = 1; off < 32; off <<= 1) {
+        unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned int w = s_w[lane], wi = w;
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += o;
+        }
+        s_w[lane] = wi - w;
+    }
+    __syncthreads();
+    unsigned int ex = s_w[wid] + incl - pr;
+    if (2 * t < nbins) bin_cur[2 * t] = ex;
+    if (2 * t + 1 < nbins) bin_cur[2 * t + 1] = ex + v0;
+}
+
+constexpr int kScatT = 1024;
+constexpr int kScatIPT = 8;
+constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
+constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * 3 + (size_t)2 * kScatBatch * 4 + 64 * 4;
+
+__global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
+                                                        const uint32_t* __restrict__ lab2,
+                                                        const uint32_t* __restrict__ hub_keys, int shift, int nbins,
+                                                        unsigned int* __restrict__ bin_cur,
+                                                        uint32_t* __restrict__ recs,
+                                                        unsigned long long* __restrict__ hub_cnt,
+                                                        uint32_t* __restrict__ hub_flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* s_hcnt = reinterpret_cast<unsigned long long*>(smem_raw);
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_hcnt + kHubSlots);
+    uint32_t* s_hflag = s_keys + kHubSlots;
+    unsigned int* s_hist = s_hflag + kHubSlots;
+    unsigned int* s_start = s_hist + kMaxBins;
+    unsigned int* s_base = s_start + kMaxBins;
+    uint32_t* s_out = s_base + kMaxBins;
+    unsigned int* s_w = s_out + 2 * kScatBatch;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    hub_load(s_keys, hub_keys);
+    for (int k = t; k < kHubSlots; k += kScatT) {
+        s_hcnt[k] = 0ULL;
+        s_hflag[k] = 0u;
+    }
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t b0 = lo; b0 < hi; b0 += kScatBatch) {
+        for (int k = t; k < nbins; k += kScatT) s_hist[k] = 0u;
+        __syncthreads();
+        uint32_t rec[2 * kScatIPT], rk[2 * kScatIPT];
+#pragma unroll
+        for (int k = 0; k < kScatIPT; ++k) {
+            int64_t i = b0 + (int64_t)k * kScatT + t;
+            rec[2 * k] = 0xFFFFFFFFu;
+            rec[2 * k + 1] = 0xFFFFFFFFu;
+            if (i < hi) {
+                uint2 ed = e[i];
+                uint32_t u = ed.x, v = ed.y;
+                int hu = hub_find(s_keys, u);
+                if (u == v) {   // self-loop: u is a chunk node, no count (model.py:53-55)
+                    if (hu >= 0) s_hflag[hu] = 1u;
+                    else rec[2 * k] = (u << 2) | 3u;
+                } else {
+                    int hv = hub_find(s_keys, v);
+                    uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
+                    if (hu >= 0) {
+                        if (cv) atomicAdd(&s_hcnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
+                        else s_hflag[hu] = 1u;
+                    } else {
+                        rec[2 * k] = (u << 2) | cv;
+                    }
+                    if (hv >= 0) {
+                        if (cu) atomicAdd(&s_hcnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
+                        else s_hflag[hv] = 1u;
+                    } else {
+                        rec[2 * k + 1] = (v << 2) | cu;
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (rec[2 * k + h] != 0xFFFFFFFFu) rk[2 * k + h] = atomicAdd(&s_hist[(rec[2 * k + h] >> 2) >> shift], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the bin histogram (nbins <= 2 * kScatT), global reservations
+        {
+            unsigned int v0 = 2 * t < nbins ? s_hist[2 * t] : 0u, v1 = 2 * t + 1 < nbins ? s_hist[2 * t + 1] : 0u;
+            unsigned int pr = v0 + v1, incl = pr;
+            for (int off = 1; off < 32; off <<= 1) {
+                unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += o;
+            }
+            if (lane == 31) s_w[wid] = incl;
+            __syncthreads();
+            if (wid == 0) {
+                unsigned int w = s_w[lane], wi = w;
+                for (int off = 1; off < 32; off <<= 1) {
+                    unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
+                    if (lane >= off) wi += o;
+                }
+                s_w[lane] = wi - w;
+                if (lane == 31) s_w[32] = wi;
+            }
+            __syncthreads();
+            unsigned int ex = s_w[wid] + incl - pr;
+            if (2 * t < nbins) {
+                s_start[2 * t] = ex;
+                s_base[2 * t] = v0 ? atomicAdd(&bin_cur[2 * t], v0) : 0u;
+            }
+            if (2 * t + 1 < nbins) {
+                s_start[2 * t + 1] = ex + v0;
+                s_base[2 * t + 1] = v1 ? atomicAdd(&bin_cur[2 * t + 1], v1) : 0u;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 2 * kScatIPT; ++k)
+            if (rec[k] != 0xFFFFFFFFu) s_out[s_start[(rec[k] >> 2) >> shift] + rk[k]] = rec[k];
+        __syncthreads();
+        unsigned int nrec = s_w[32];
+        for (unsigned int k = t; k < nrec; k += kScatT) {   // runs of a bin are contiguous
+            uint32_t r = s_out[k];
+            unsigned int bb = (r >> 2) >> shift;
+            recs[s_base[bb] + (k - s_start[bb])] = r;
+        }
+        __syncthreads();
+    }
+    for (int k = t; k < kHubSlots; k += kScatT) {
+        if (s_keys[k] == kHubEmpty) continue;
+        if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
+        if (s_hflag[k]) hub_flag[k] = 1u;
+    }
+}
+
+constexpr int kCmpT = 1024;
+constexpr int kCmpSub = 1 << kSubShift;              // nodes per tile
+constexpr int kCmpIPT = kCmpSub / kCmpT;             // 16 consecutive nodes per thread
+constexpr size_t kCmpSmem = (size_t)kCmpSub * 8 + (size_t)kCmpSub / 8 + 64 * 8;
+static_assert(kCmpIPT == 16, "16 nodes per thread (one 16-byte label load)");
+
+__global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restrict__ recs,
+                                                       const unsigned int* __restrict__ bin_count,
+                                                       const unsigned int* __restrict__ bin_end, int shift,
+                                                       int64_t n, const uint32_t* __restrict__ hub_keys,
+                                                       const unsigned long long* __restrict__ hub_cnt,
+                                                       const uint32_t* __restrict__ hub_flag, int refine,
+                                                       ChunkBufs b, unsigned long long* status,
+                                                       unsigned int* ticket, int64_t ntiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(smem_raw);
+    uint32_t* s_pres = reinterpret_cast<uint32_t*>(s_cnt + kCmpSub);
+    unsigned long long* s_w = reinterpret_cast<unsigned long long*>(s_pres + kCmpSub / 32);
+    __shared__ int64_t s_tile;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int k = t; k < kCmpSub; k += kCmpT) s_cnt[k] = 0ULL;
+    for (int k = t; k < kCmpSub / 32; k += kCmpT) s_pres[k] = 0u;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t g0 = tile << kSubShift;
+    const int cb = (int)(g0 >> shift);
+    const int64_t rend = bin_end[cb], rbeg = rend - bin_count[cb];
+    // records of the coarse bin that fall in this tile; 16-byte loads on the aligned body
+    auto apply = [&](uint32_t r) {
+        uint32_t node = r >> 2;
+        if ((int64_t)(node >> kSubShift) != tile) return;
+        uint32_t l = node & (kCmpSub - 1), c = r & 3u;
+        if (c == 1) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + l), 1u);
+        else if (c == 2) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + l) + 1, 1u);
+        else atomicOr(&s_pres[l >> 5], 1u << (l & 31));
+    };
+    int64_t abeg = (rbeg + 3) & ~3LL, aend = rend & ~3LL;
+    if (abeg > aend) abeg = aend = rbeg;
+    for (int64_t k = rbeg + t; k < abeg && k < rend; k += kCmpT) apply(recs[k]);
+    for (int64_t k = abeg + 4 * (int64_t)t; k < aend; k += 4 * (int64_t)kCmpT) {
+        uint4 q = *reinterpret_cast<const uint4*>(recs + k);
+        apply(q.x);
+        apply(q.y);
+        apply(q.z);
+        apply(q.w);
+    }
+    for (int64_t k = (aend > abeg ? aend : abeg) + t; k < rend; k += kCmpT) apply(recs[k]);
+    if (hub_keys) {   // hubs never emit records: their counts come from the slot table
+        for (int k = t; k < kHubSlots; k += kCmpT) {
+            uint32_t key = hub_keys[k];
+            if (key == kHubEmpty || (int64_t)(key >> kSubShift) != tile) continue;
+            uint32_t l = key & (kCmpSub - 1);
+            unsigned long long c = hub_cnt[k];
+            if (c) s_cnt[l] = c;
+            if (hub_flag[k]) atomicOr(&s_pres[l >> 5], 1u << (l & 31));
+        }
+    }
+    __syncthreads();
+    // this thread's 16 consecutive nodes: membership, old labels, new flags
+    const int l0 = t * kCmpIPT;
+    const int64_t gt = g0 + l0;
+    int8_t lab16[kCmpIPT];
+    if (gt + kCmpIPT <= n) {
+        uint4 q = *reinterpret_cast<const uint4*>(b.lab + gt);
+        const int8_t* qb = reinterpret_cast<const int8_t*>(&q);
+#pragma unroll
+        for (int j = 0; j < kCmpIPT; ++j) lab16[j] = qb[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCmpIPT; ++j) lab16[j] = gt + j < n ? b.lab[gt + j] : (int8_t)-1;
+    }
+    uint32_t pw = (s_pres[l0 >> 5] >> (l0 & 31)) & 0xFFFFu;
+    uint32_t pmask = 0, nmask = 0;
+#pragma unroll
+    for (int j = 0; j < kCmpIPT; ++j) {
+        bool pres = (gt + j < n) && (((pw >> j) & 1u) || s_cnt[l0 + j] != 0ULL);
+        if (pres) {
+            pmask |= 1u << j;
+            if (lab16[j] == -1) nmask |= 1u << j;
+        }
+    }
+    // block scan of (members, new members) packed as p | nw << 31
+    unsigned long long mine = (unsigned long long)__popc(pmask) | ((unsigned long long)__popc(nmask) << 31);
+    unsigned long long incl = mine;
+    for (int off = 1; off < 32; off <<= 1) {
+        unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long w = s_w[lane], wi = w;
+        for (int off = 1; off < 32; off <<= 1) {
+            unsigned long long o = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += o;
+        }
+        s_w[lane] = wi - w;
+        unsigned long long total = __shfl_sync(0xffffffffu, wi, 31);
+        unsigned long long prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(status, kLbInc | total);
+        } else {
+            if (lane == 0) atomicExch(status + tile, kLbAgg | total);
+            prefix = lb_prefix(status, tile);
+            if (lane == 0) atomicExch(status + tile, kLbInc | (prefix + total));
+        }
+        if (lane == 0) {
+            s_w[32] = prefix;
+            if (tile == ntiles - 1) {
+                unsigned long long all = prefix + total;
+                b.scal[0] = (long long)(all & 0x7FFFFFFFULL);
+                b.scal[2] = (long long)(all >> 31);
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long ex = s_w[32] + s_w[wid] + incl - mine;
+    int64_t i = (int64_t)(ex & 0x7FFFFFFFULL);
+    long long nb = b.sizes[0] + b.sizes[1] + (long long)(ex >> 31);
+#pragma unroll
+    for (int j = 0; j < kCmpIPT; ++j) {
+        if (!((pmask >> j) & 1u)) continue;
+        uint32_t g = (uint32_t)(gt + j);
+        int old = lab16[j];
+        int code = old + 1;
+        bool isnew = old == -1;
+        bool active = isnew || refine;
+        b.nodes[i] = g;
+        b.meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
+        b.tlc[i] = (uint8_t)(code | (code << 4));
+        b.pos[g] = (int32_t)i;
+        b.cntc[i] = s_cnt[l0 + j];
+        b.nbrc[i] = isnew ? make_double2(0.0, 0.0) : b.nbr[g];
+        b.newb[i] = (int32_t)nb;   // s0 + active new nodes before i (new nodes are always active)
+        nb += isnew ? 1 : 0;
+        ++i;
+    }
+}
+
+void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
+                              const BinBufs& bb, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatSmem);
+        cudaFuncSetAttribute(k_bin_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCmpSmem);
+        attr = true;
+    }
+    int64_t ntiles = (n + kCmpSub - 1) >> kSubShift;
+    cudaMemsetAsync(bb.bin_count, 0, sizeof(unsigned int) * (kMaxBins + 2), s);
+    cudaMemsetAsync(bb.hub_cnt, 0, sizeof(unsigned long long) * kHubSlots, s);
+    cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
+    cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
+    cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
+    k_bin_count<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.bin_count);
+    k_bin_offsets<<<1, 1024, 0, s>>>(bb.bin_count, bb.bin_cur, bb.nbins);
+    k_bin_scatter<<<(unsigned)num_sms(), kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins,
+                                                                bb.bin_cur, bb.recs, bb.hub_cnt, bb.hub_flag);
+    k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.bin_count, bb.bin_cur, bb.shift, n,
+                                                           b.hub_keys, bb.hub_cnt, bb.hub_flag, refine, b,
+                                                           bb.status, bb.ticket, ntiles);
+}
+int binned_shift(int64_t n) {
+    int shift = kSubShift;
+    while (((n + (1LL << shift) - 1) >> shift) > kMaxBins) ++shift;
+    return shift;
+}
+int64_t binned_tiles(int64_t n) { return (n + kCmpSub - 1) >> kSubShift; }
 
 }  // namespace grem

@@ -44,24 +44,35 @@ struct ChunkBufs {
     long long* tile_bad;
     // device scalars
     long long* sizes;   // [2] live sizes (read-only during a chunk)
-    long long* scal;    // [8] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0,
-                        //     6 first mis-speculated tie
+    long long* scal;    // [16] scratch scalars: 0 n_c, 1 changed, 2 total_new, 3 bundle misses, 4 nbad, 5 2*x0,
+                        //     6 first mis-speculated tie, 7 round gate, 8 rounds run
     const uint32_t* hub_keys;   // kHubSlots table or nullptr (no hubs)
     uint32_t* lab2;             // 2-bit mirror of lab (code = label + 1), L2-resident gathers
+    const long long* gate;      // scal + 7: changed count of the previous round (round kernels skip on 0)
 };
 
-// Propagation blocking for the round-1 counts: edges emit (node, label code)
-// records binned by node-id range (coalesced writes through a per-CTA counting
-// sort), then the records are applied bin by bin so each bin's counter slice
-// stays in L2.  kMaxBins bins of 2^shift node ids.
-constexpr int kMaxBins = 256;
+// Round-1 counts of large chunks (propagation blocking): edges emit
+// (node, label code) records binned by coarse node range (2^shift ids,
+// <= kMaxBins bins); one CTA per 2^kSubShift-node tile then accumulates its
+// records in shared memory and writes the compact chunk state directly.
+constexpr int kMaxBins = 2048;
+constexpr int kSubShift = 14;
 struct BinBufs {
     uint32_t* recs;          // >= 2 * edges of the chunk
-    unsigned int* bin_count; // kMaxBins + 1
-    unsigned int* bin_cur;   // kMaxBins
+    unsigned int* bin_count; // kMaxBins + 2
+    unsigned int* bin_cur;   // kMaxBins (after the scatter: end of each bin's records)
+    unsigned long long* hub_cnt;   // kHubSlots
+    uint32_t* hub_flag;            // kHubSlots
+    unsigned long long* status;    // binned_tiles(n) look-back words
+    unsigned int* ticket;          // 1
     int shift, nbins;
 };
-void launch_count_init_binned(const uint2* e, int64_t m, const ChunkBufs& b, const BinBufs& bb, cudaStream_t s);
+int binned_shift(int64_t n);
+int64_t binned_tiles(int64_t n);
+// writes nodes, meta, tlc, pos, cntc, nbrc, newb (incl. s0) for the chunk;
+// scal[0] = N_c, scal[2] = new nodes
+void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
+                              const BinBufs& bb, cudaStream_t s);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
@@ -95,6 +106,7 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
 // speculative decisions (node arrays padded to whole kScanTile tiles)
 void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
+void launch_round_gate(const ChunkBufs& b, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 
 // --- chunk membership ---

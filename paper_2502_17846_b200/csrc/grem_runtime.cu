@@ -111,7 +111,9 @@ struct grem_ctx {
     // per node
     DBuf<int8_t> lab{"lab"};
     DBuf<uint32_t> lab2{"lab2"}, bin_recs{"bin_recs"};
-    DBuf<unsigned int> bin_count{"bin_count"}, bin_cur{"bin_cur"};
+    DBuf<unsigned int> bin_count{"bin_count"}, bin_cur{"bin_cur"}, bin_ticket{"bin_ticket"};
+    DBuf<unsigned long long> bin_hcnt{"bin_hcnt"}, bin_status{"bin_status"};
+    DBuf<uint32_t> bin_hflag{"bin_hflag"};
     DBuf<uint8_t> tl{"tl"}, flag{"flag"};
     DBuf<unsigned long long> cnt{"cnt"};
     DBuf<double2> nbr{"nbr"};
@@ -351,6 +353,7 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.scal = c->d_scal;
     b.hub_keys = c->hubs_on ? c->hub_table.p : nullptr;
     b.lab2 = c->lab2.p;
+    b.gate = nullptr;
     return b;
 }
 
@@ -568,53 +571,65 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
 void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     cudaStream_t s = c->s;
     ChunkBufs b = chunk_bufs(c);
-    CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 8, s));
+    CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 16, s));
+    CK(cudaMemsetAsync(c->d_scal + 7, 1, 1, s));   // round gate open
+    b.gate = c->d_scal + 7;
+    bool binned = false;
     {
         PhaseScope ps(c, PH_COUNT);
         // propagation blocking when the per-node counters do not fit in L2
         const char* nb_env = getenv("GREM_NO_BINNING");
         const char* fb_env = getenv("GREM_FORCE_BINNING");   // tests: exercise the binned path on small graphs
-        if (!nb_env && (fb_env || (a.n * 9 > (48LL << 20) && mc >= (1 << 20)))) {
-            int shift = 0;
-            while (((a.n + (1LL << shift) - 1) >> shift) > kMaxBins) ++shift;
+        binned = !nb_env && (fb_env || (a.n * 9 > (48LL << 20) && mc >= (1 << 20)));
+        if (binned) {
+            int shift = binned_shift(a.n);
             int nbins = (int)((a.n + (1LL << shift) - 1) >> shift);
+            int64_t ntiles = binned_tiles(a.n);
             c->bin_recs.ensure(2 * mc + 16, s);
             c->bin_count.ensure(kMaxBins + 2, s);
             c->bin_cur.ensure(kMaxBins, s);
-            BinBufs bb{c->bin_recs.p, c->bin_count.p, c->bin_cur.p, shift, nbins};
-            launch_count_init_binned(e, mc, b, bb, s);
-            c->kernels += 4;
+            c->bin_hcnt.ensure(kHubSlots, s);
+            c->bin_hflag.ensure(kHubSlots, s);
+            c->bin_status.ensure(ntiles + 1, s);
+            c->bin_ticket.ensure(4, s);
+            BinBufs bb{c->bin_recs.p, c->bin_count.p, c->bin_cur.p, c->bin_hcnt.p, c->bin_hflag.p, c->bin_status.p,
+                       c->bin_ticket.p, shift, nbins};
+            launch_count_init_binned(e, mc, a.n, a.refine, b, bb, s);
+            c->kernels += 9;
         } else {
             launch_count_init(e, mc, b, s);
         }
     }
     c->stats.count_bytes += 10 * mc;   // 8 B edge read + 2 x 1 B label gather
-    { PhaseScope ps(c, PH_SELECT); launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s); }
-    c->kernels += 2;
+    if (!binned) {
+        PhaseScope ps(c, PH_SELECT);
+        launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
+        c->kernels += 2;
+    }
     scal_read(c, c->d_scal, 1);
     int64_t nc = c->h_pin[0];
     c->stats.visits += nc;
-    {
+    if (!binned) {   // (the binned path wrote the compact state and newb already)
         PhaseScope ps(c, PH_NODE);
         launch_node_init(b, nc, a.refine, s);
         exclusive_sum_i32(c->x.p, c->newb.p, nc, c->temp.p, c->temp.cap, s);
         launch_add_base(c->newb.p, nc, c->d_sizes, s);
+        c->kernels += 3;
     }
-    c->kernels += 3;
     // identity padding up to whole round tiles (inactive nodes, meta 0)
     {
         int64_t padded = (nc + 1 + kScanTile - 1) / kScanTile * kScanTile;
         CK(cudaMemsetAsync(c->meta.p + nc, 0, padded - nc, s));
     }
-    int64_t rounds = 0;
+    // Rounds are launched in batches without a host round trip: every round
+    // kernel is gated on the device by the previous round's changed count, so
+    // rounds after the fixpoint are no-ops; the host checks once per batch.
+    static const int batch = getenv("GREM_ROUND_BATCH") ? std::max(1, atoi(getenv("GREM_ROUND_BATCH"))) : 2;
     for (int r = 1;; ++r) {
-        rounds++;
         if (r > 1) {
             PhaseScope ps(c, PH_DELTA);
             launch_count_delta(e, mc, b, s);
             CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));   // consumed
-            c->stats.count_bytes += 9 * mc;   // 8 B edge read + 1 B tentative-label gather
-            c->stats.delta_bytes += 9 * mc;
             c->kernels++;
         }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
@@ -639,19 +654,28 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
             c->kernels += 5;
         }
+        launch_round_gate(b, s);
+        c->kernels++;
         if (getenv("GREM_DEBUG_BUNDLE")) {
             scal_read(c, c->d_scal + 1, 4);
             fprintf(stderr, "[bundle] round %d nc %lld changed %lld nbad %lld misses(cum) %lld\n", r, (long long)nc,
                     c->h_pin[0], c->h_pin[3], c->h_pin[2]);
         }
         // this round's exact x becomes the next round's second window centre
+        // (after the fixpoint the swaps are harmless: nothing reads xalt)
         std::swap(c->xalt.p, c->xnext.p);
         b.xalt = c->xalt.p;
         b.xnext = c->xnext.p;
-        scal_read(c, c->d_scal + 1, 1);
-        if (c->h_pin[0] == 0) break;
-        if (r > nc + 2) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
+        if (r % batch == 0) {
+            scal_read(c, c->d_scal + 7, 1);
+            if (c->h_pin[0] == 0) break;
+        }
+        if (r > nc + 2 + batch) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
     }
+    scal_read(c, c->d_scal + 8, 1);
+    int64_t rounds = c->h_pin[0];
+    c->stats.count_bytes += 9 * mc * (rounds - 1);   // rounds >= 2: 8 B edge read + 1 B tentative-label gather
+    c->stats.delta_bytes += 9 * mc * (rounds - 1);
     {
         PhaseScope ps(c, PH_COMMIT);
         launch_commit(b, nc, s);
@@ -717,6 +741,8 @@ void detect_hubs(grem_ctx* c, const BisectArgs& a) {
     c->hubs_on = true;
 }
 
+cudaEvent_t g_dbg_t0 = nullptr;   // GREM_DEBUG_LEVELS timeline origin
+
 // bisect (grem.py:192-224) on device-resident edges; leaves labels in c->lab
 void bisect_core(grem_ctx* c, const BisectArgs& a) {
     cudaStream_t s = c->s;
@@ -734,10 +760,14 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
             if (!a) return;
             cudaEventRecord(b, c->s);
             cudaEventSynchronize(b);
-            float ms = 0;
+            float ms = 0, t0 = -1, t1 = -1;
             cudaEventElapsedTime(&ms, a, b);
-            fprintf(stderr, "[level] n %lld m %lld cap %lld chunk %lld: %.2f ms rounds %lld visits %lld misses %lld\n",
-                    (long long)args.n, (long long)args.m, args.cap, (long long)args.chunk, ms,
+            if (g_dbg_t0) {   // timeline relative to the start of partition()
+                cudaEventElapsedTime(&t0, g_dbg_t0, a);
+                cudaEventElapsedTime(&t1, g_dbg_t0, b);
+            }
+            fprintf(stderr, "[level] [%7.1f, %7.1f] n %lld m %lld cap %lld chunk %lld: %.2f ms rounds %lld visits %lld misses %lld\n",
+                    t0, t1, (long long)args.n, (long long)args.m, args.cap, (long long)args.chunk, ms,
                     (long long)(c->stats.rounds - r0), (long long)(c->stats.visits - v0),
                     (long long)(c->stats.walk_steps - b0));
             cudaEventDestroy(a);
@@ -1073,14 +1103,21 @@ void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_
     CK(cudaStreamSynchronize(c->s));
 }
 
-void init_ctx(grem_ctx* c, int device) {
+// Stream priorities: the root context carries the dense chain of the
+// recursion (the larger side always stays on it), child contexts the smaller
+// subtrees.  GREM_PRIO: 0 = none, 1 = root high, 2 = children high.
+void init_ctx(grem_ctx* c, int device, bool child = false) {
     c->device = device;
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    static const int prio_mode = getenv("GREM_PRIO") ? atoi(getenv("GREM_PRIO")) : 2;
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    bool high = (prio_mode == 1 && !child) || (prio_mode == 2 && child);
+    CK(cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, (prio_mode && high) ? hi : lo));
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaMalloc(&c->d_sizes, sizeof(long long) * 2));
-    CK(cudaMalloc(&c->d_scal, sizeof(long long) * 8));
+    CK(cudaMalloc(&c->d_scal, sizeof(long long) * 16));
     CK(cudaMalloc(&c->d_sscal, sizeof(long long) * 16));
     CK(cudaHostAlloc(&c->h_pin, sizeof(long long) * 32, cudaHostAllocDefault));
     ensure_temp(c, 1 << 20);
@@ -1097,7 +1134,7 @@ grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
         if (!ch) {
             ch = new grem_ctx();
             ch->root = root;
-            init_ctx(ch, root->device);
+            init_ctx(ch, root->device, true);
             root->pool_all.push_back(ch);
             root->pool_keyed.push_back({key, ch});
         }
@@ -1290,6 +1327,10 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
     int32_t* orig = c->part_orig.p;
     CK(cudaMemsetAsync(fin, 0xFF, sizeof(int32_t) * n, s));
     launch_iota(orig, n, s);
+    if (getenv("GREM_DEBUG_LEVELS")) {
+        if (!g_dbg_t0) CK(cudaEventCreate(&g_dbg_t0));
+        CK(cudaEventRecord(g_dbg_t0, s));
+    }
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
     try {
         recurse(c, pc, d, m, n, orig, p, 0, 0, 0, shard_world);
@@ -1385,7 +1426,8 @@ void grem_destroy(grem_ctx* c) {
     c->lab2.release();
     c->bin_recs.release();
     c->bin_count.release();
-    c->bin_cur.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
+    c->bin_cur.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
+    c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
     c->rank.release(); c->scratch.release(); c->newid.release();
     c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
     c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
