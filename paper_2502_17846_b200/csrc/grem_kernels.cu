@@ -248,18 +248,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down_plain(Src src, int64
 // ------------------------------------------------------------- counting
 
 // ------------------------------------------------------------- hub table
-__device__ __forceinline__ uint32_t hub_hash(uint32_t u) { return (u * 0x9E3779B1u) >> (32 - 11); }   // 2048 slots
-
+// Hub table: bucketised 2-choice cuckoo hashing (kHubSlots / 2 buckets of two
+// slots; built on the host, hub_table_build).  A lookup is two 8-byte shared
+// loads and four compares: no probe loop, so no warp divergence.
 __device__ __forceinline__ int hub_find(const uint32_t* s_keys, uint32_t u) {
-    uint32_t h = hub_hash(u);
-    while (true) {
-        uint32_t k = s_keys[h];
-        if (k == u) return (int)h;
-        if (k == kHubEmpty) return -1;
-        h = (h + 1) & (kHubSlots - 1);
-    }
+    uint32_t b1 = hub_bucket1(u), b2 = hub_bucket2(u);
+    uint2 p = reinterpret_cast<const uint2*>(s_keys)[b1];
+    uint2 q = reinterpret_cast<const uint2*>(s_keys)[b2];
+    int r = -1;
+    r = p.x == u ? (int)(2 * b1) : r;
+    r = p.y == u ? (int)(2 * b1 + 1) : r;
+    r = q.x == u ? (int)(2 * b2) : r;
+    r = q.y == u ? (int)(2 * b2 + 1) : r;
+    return r;
 }
-
 __device__ __forceinline__ void hub_load(uint32_t* s_keys, const uint32_t* hub_keys) {
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_keys[k] = hub_keys ? hub_keys[k] : kHubEmpty;
 }
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
                                                              unsigned long long* __restrict__ cnt,
                                                              uint8_t* __restrict__ flag,
                                                              const uint32_t* __restrict__ hub_keys) {
-    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
     __shared__ uint8_t s_flag[kHubSlots];
     hub_load(s_keys, hub_keys);
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
                                                               const uint32_t* __restrict__ hub_keys,
                                                               const long long* __restrict__ gate) {
     if (gate && *gate == 0) return;   // previous round changed nothing (converged)
-    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
     hub_load(s_keys, hub_keys);
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = 0ULL;
@@ -388,26 +390,6 @@ __device__ __forceinline__ uint32_t lab2_code(const uint32_t* __restrict__ lab2,
     return (lab2[u >> 4] >> ((u & 15) * 2)) & 3u;
 }
 
-__global__ void __launch_bounds__(kEdgeThreads) k_bin_count(const uint2* __restrict__ e, int64_t m,
-                                                            const uint32_t* __restrict__ hub_keys, int shift,
-                                                            int nbins, unsigned int* __restrict__ bin_count) {
-    __shared__ uint32_t s_keys[kHubSlots];
-    __shared__ unsigned int s_hist[kMaxBins];
-    hub_load(s_keys, hub_keys);
-    for (int k = threadIdx.x; k < nbins; k += blockDim.x) s_hist[k] = 0;
-    __syncthreads();
-    int64_t lo, hi;
-    cta_range(m, lo, hi);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        uint2 ed = e[i];
-        if (hub_find(s_keys, ed.x) < 0) atomicAdd(&s_hist[ed.x >> shift], 1u);
-        if (ed.x != ed.y && hub_find(s_keys, ed.y) < 0) atomicAdd(&s_hist[ed.y >> shift], 1u);
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < nbins; k += blockDim.x)
-        if (s_hist[k]) atomicAdd(&bin_count[k], s_hist[k]);
-}
-
 // (bin offsets, scatter and the fused apply/compact are at the end of the file)
 
 // hub detection: endpoint histogram of a sample, candidates, top-K
@@ -442,18 +424,6 @@ __global__ void k_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg
 }
 void launch_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg, unsigned long long* keys, cudaStream_t s) {
     k_hub_keys<<<grid_for(cnt, 256), 256, 0, s>>>(ids, cnt, sdeg, keys);
-}
-__global__ void k_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table) {
-    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) table[k] = kHubEmpty;
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < nhubs; j += blockDim.x) {
-        uint32_t u = (uint32_t)(sorted_desc[j] & 0xFFFFFFFFULL);
-        uint32_t h = hub_hash(u);
-        while (atomicCAS(&table[h], kHubEmpty, u) != kHubEmpty) h = (h + 1) & (kHubSlots - 1);
-    }
-}
-void launch_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table, cudaStream_t s) {
-    k_build_hub_table<<<1, 1024, 0, s>>>(sorted_desc, nhubs, table);
 }
 
 __global__ void k_mark_all(const uint2* __restrict__ e, int64_t m, uint8_t* __restrict__ flag) {
@@ -1322,7 +1292,7 @@ void launch_set_rank(const uint32_t* nodes, int64_t nc, int32_t* rank, cudaStrea
 __global__ void __launch_bounds__(kEdgeThreads) k_degrees(const uint2* __restrict__ e, int64_t m,
                                                           const int32_t* __restrict__ rank, int32_t* __restrict__ deg,
                                                           const uint32_t* __restrict__ hub_keys) {
-    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ uint32_t s_deg[kHubSlots];
     hub_load(s_keys, hub_keys);
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_deg[k] = 0;
@@ -1356,7 +1326,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_fill_csr(const uint2* __restri
                                                            int32_t* __restrict__ cursor, uint32_t* __restrict__ adj,
                                                            uint32_t* __restrict__ row_of,
                                                            const uint32_t* __restrict__ hub_keys) {
-    __shared__ uint32_t s_keys[kHubSlots];
+    __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ int32_t s_pos[kHubSlots];
     hub_load(s_keys, hub_keys);
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_pos[k] = 0;
@@ -2503,7 +2473,8 @@ void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, ui
 // ===================================================== binned round-1 counts
 // Round 1 of a large chunk (cnt_nbrs with pre-sweep labels, grem.py:82-97,
 // plus the chunk node set np.unique, model.py:59) in three passes:
-//   k_bin_count    records per coarse bin (2^shift node ids);
+//   k_bin_hist     records per (coarse bin of 2^shift node ids, scatter CTA),
+//                  scanned into private per-CTA cursors;
 //   k_bin_scatter  per 8192-edge batch a block counting sort by coarse bin
 //                  (rank = smem atomic return), coalesced record runs out;
 //   k_bin_compact  one CTA per 2^kSubShift-node tile, in node order: smem
@@ -2514,33 +2485,36 @@ void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, ui
 //                  select, no separate node init or scan).
 // Records: node << 2 | code (1: +c0, 2: +c1, 0: unassigned neighbour, 3: self-loop).
 
-__global__ void __launch_bounds__(1024) k_bin_offsets(const unsigned int* __restrict__ bin_count,
-                                                      unsigned int* __restrict__ bin_cur, int nbins) {
-    __shared__ unsigned int s_w[32];
-    int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    unsigned int v0 = 2 * t < nbins ? bin_count[2 * t] : 0u, v1 = 2 * t + 1 < nbins ? bin_count[2 * t + 1] : 0u;
-    unsigned int pr = v0 + v1, incl = pr;
-    for (int off = 1; off < 32; off <<= 1) {
-        unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += o;
-    }
-    if (lane == 31) s_w[wid] = incl;
+// Per-CTA record histogram (the scatter CTA c covers the same contiguous
+// edge range): hist[bin * G + c]; its exclusive scan gives every CTA a private,
+// deterministic cursor per bin (no global atomics in the scatter).
+constexpr int kScatT = 1024;
+__global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e, int64_t m,
+                                                     const uint32_t* __restrict__ hub_keys, int shift, int nbins,
+                                                     int32_t* __restrict__ hist) {
+    __shared__ __align__(8) uint32_t s_keys[kHubSlots];
+    __shared__ unsigned int s_hist[kMaxBins];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < nbins; k += kScatT) s_hist[k] = 0;
     __syncthreads();
-    if (wid == 0) {
-        unsigned int w = s_w[lane], wi = w;
-        for (int off = 1; off < 32; off <<= 1) {
-            unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= off) wi += o;
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += 4 * kScatT) {
+        uint2 ed[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ed[j] = i + j * kScatT < hi ? __ldcs(e + i + j * kScatT) : make_uint2(kHubEmpty, kHubEmpty);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (ed[j].x == kHubEmpty) continue;
+            if (hub_find(s_keys, ed[j].x) < 0) atomicAdd(&s_hist[ed[j].x >> shift], 1u);
+            if (ed[j].x != ed[j].y && hub_find(s_keys, ed[j].y) < 0) atomicAdd(&s_hist[ed[j].y >> shift], 1u);
         }
-        s_w[lane] = wi - w;
     }
     __syncthreads();
-    unsigned int ex = s_w[wid] + incl - pr;
-    if (2 * t < nbins) bin_cur[2 * t] = ex;
-    if (2 * t + 1 < nbins) bin_cur[2 * t + 1] = ex + v0;
+    for (int k = threadIdx.x; k <= nbins; k += kScatT)
+        hist[(int64_t)k * gridDim.x + blockIdx.x] = k < nbins ? (int32_t)s_hist[k] : 0;   // row nbins: total
 }
 
-constexpr int kScatT = 1024;
 constexpr int kScatIPT = 8;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
 constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * 3 + (size_t)2 * kScatBatch * 4 + 64 * 4;
@@ -2548,7 +2522,7 @@ constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins 
 __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
                                                         const uint32_t* __restrict__ hub_keys, int shift, int nbins,
-                                                        unsigned int* __restrict__ bin_cur,
+                                                        const int32_t* __restrict__ offs,
                                                         uint32_t* __restrict__ recs,
                                                         unsigned long long* __restrict__ hub_cnt,
                                                         uint32_t* __restrict__ hub_flag) {
@@ -2558,8 +2532,8 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
     uint32_t* s_hflag = s_keys + kHubSlots;
     unsigned int* s_hist = s_hflag + kHubSlots;
     unsigned int* s_start = s_hist + kMaxBins;
-    unsigned int* s_base = s_start + kMaxBins;
-    uint32_t* s_out = s_base + kMaxBins;
+    unsigned int* s_cur = s_start + kMaxBins;
+    uint32_t* s_out = s_cur + kMaxBins;
     unsigned int* s_w = s_out + 2 * kScatBatch;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     hub_load(s_keys, hub_keys);
@@ -2567,20 +2541,25 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         s_hcnt[k] = 0ULL;
         s_hflag[k] = 0u;
     }
+    for (int k = t; k < nbins; k += kScatT) s_cur[k] = (unsigned int)offs[(int64_t)k * gridDim.x + blockIdx.x];
     int64_t lo, hi;
     cta_range(m, lo, hi);
     for (int64_t b0 = lo; b0 < hi; b0 += kScatBatch) {
         for (int k = t; k < nbins; k += kScatT) s_hist[k] = 0u;
+        uint2 ed[kScatIPT];
+#pragma unroll
+        for (int k = 0; k < kScatIPT; ++k) {
+            int64_t i = b0 + (int64_t)k * kScatT + t;
+            ed[k] = i < hi ? __ldcs(e + i) : make_uint2(kHubEmpty, kHubEmpty);   // streaming: keep L2 for the record runs
+        }
         __syncthreads();
         uint32_t rec[2 * kScatIPT], rk[2 * kScatIPT];
 #pragma unroll
         for (int k = 0; k < kScatIPT; ++k) {
-            int64_t i = b0 + (int64_t)k * kScatT + t;
             rec[2 * k] = 0xFFFFFFFFu;
             rec[2 * k + 1] = 0xFFFFFFFFu;
-            if (i < hi) {
-                uint2 ed = e[i];
-                uint32_t u = ed.x, v = ed.y;
+            uint32_t u = ed[k].x, v = ed[k].y;
+            if (u != kHubEmpty) {
                 int hu = hub_find(s_keys, u);
                 if (u == v) {   // self-loop: u is a chunk node, no count (model.py:53-55)
                     if (hu >= 0) s_hflag[hu] = 1u;
@@ -2607,9 +2586,9 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
                 if (rec[2 * k + h] != 0xFFFFFFFFu) rk[2 * k + h] = atomicAdd(&s_hist[(rec[2 * k + h] >> 2) >> shift], 1u);
         }
         __syncthreads();
-        // exclusive scan of the bin histogram (nbins <= 2 * kScatT), global reservations
+        // exclusive scan of the batch's bin histogram (nbins <= 2 * kScatT)
+        unsigned int v0 = 2 * t < nbins ? s_hist[2 * t] : 0u, v1 = 2 * t + 1 < nbins ? s_hist[2 * t + 1] : 0u;
         {
-            unsigned int v0 = 2 * t < nbins ? s_hist[2 * t] : 0u, v1 = 2 * t + 1 < nbins ? s_hist[2 * t + 1] : 0u;
             unsigned int pr = v0 + v1, incl = pr;
             for (int off = 1; off < 32; off <<= 1) {
                 unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
@@ -2628,14 +2607,8 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
             }
             __syncthreads();
             unsigned int ex = s_w[wid] + incl - pr;
-            if (2 * t < nbins) {
-                s_start[2 * t] = ex;
-                s_base[2 * t] = v0 ? atomicAdd(&bin_cur[2 * t], v0) : 0u;
-            }
-            if (2 * t + 1 < nbins) {
-                s_start[2 * t + 1] = ex + v0;
-                s_base[2 * t + 1] = v1 ? atomicAdd(&bin_cur[2 * t + 1], v1) : 0u;
-            }
+            if (2 * t < nbins) s_start[2 * t] = ex;
+            if (2 * t + 1 < nbins) s_start[2 * t + 1] = ex + v0;
         }
         __syncthreads();
 #pragma unroll
@@ -2646,10 +2619,13 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         for (unsigned int k = t; k < nrec; k += kScatT) {   // runs of a bin are contiguous
             uint32_t r = s_out[k];
             unsigned int bb = (r >> 2) >> shift;
-            recs[s_base[bb] + (k - s_start[bb])] = r;
+            recs[s_cur[bb] + (k - s_start[bb])] = r;
         }
         __syncthreads();
+        if (2 * t < nbins) s_cur[2 * t] += v0;
+        if (2 * t + 1 < nbins) s_cur[2 * t + 1] += v1;
     }
+    __syncthreads();
     for (int k = t; k < kHubSlots; k += kScatT) {
         if (s_keys[k] == kHubEmpty) continue;
         if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
@@ -2660,12 +2636,11 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
 constexpr int kCmpT = 1024;
 constexpr int kCmpSub = 1 << kSubShift;              // nodes per tile
 constexpr int kCmpIPT = kCmpSub / kCmpT;             // 16 consecutive nodes per thread
-constexpr size_t kCmpSmem = (size_t)kCmpSub * 8 + (size_t)kCmpSub / 8 + 64 * 8;
+constexpr size_t kCmpSmem = (size_t)kCmpSub * (8 + 2 + 2) + (size_t)kCmpSub / 8 + 64 * 8;
 static_assert(kCmpIPT == 16, "16 nodes per thread (one 16-byte label load)");
 
 __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restrict__ recs,
-                                                       const unsigned int* __restrict__ bin_count,
-                                                       const unsigned int* __restrict__ bin_end, int shift,
+                                                       const int32_t* __restrict__ offs, int G, int shift,
                                                        int64_t n, const uint32_t* __restrict__ hub_keys,
                                                        const unsigned long long* __restrict__ hub_cnt,
                                                        const uint32_t* __restrict__ hub_flag, int refine,
@@ -2673,8 +2648,10 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
                                                        unsigned int* ticket, int64_t ntiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(smem_raw);
-    uint32_t* s_pres = reinterpret_cast<uint32_t*>(s_cnt + kCmpSub);
-    unsigned long long* s_w = reinterpret_cast<unsigned long long*>(s_pres + kCmpSub / 32);
+    unsigned long long* s_w = s_cnt + kCmpSub;
+    uint32_t* s_pres = reinterpret_cast<uint32_t*>(s_w + 64);
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_pres + kCmpSub / 32);   // member k: local id | old code << 14
+    uint16_t* s_nwx = s_idx + kCmpSub;                                       // member k: new members before k
     __shared__ int64_t s_tile;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     if (t == 0) s_tile = atomicAdd(ticket, 1u);
@@ -2683,9 +2660,9 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
     __syncthreads();
     const int64_t tile = s_tile;
     const int64_t g0 = tile << kSubShift;
-    const int cb = (int)(g0 >> shift);
-    const int64_t rend = bin_end[cb], rbeg = rend - bin_count[cb];
-    // records of the coarse bin that fall in this tile; 16-byte loads on the aligned body
+    const int64_t cb = g0 >> shift;
+    const int64_t rbeg = offs[cb * G], rend = offs[(cb + 1) * G];
+    // records of the coarse bin that fall in this tile (16-byte loads, 4 in flight)
     auto apply = [&](uint32_t r) {
         uint32_t node = r >> 2;
         if ((int64_t)(node >> kSubShift) != tile) return;
@@ -2695,16 +2672,26 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         else atomicOr(&s_pres[l >> 5], 1u << (l & 31));
     };
     int64_t abeg = (rbeg + 3) & ~3LL, aend = rend & ~3LL;
-    if (abeg > aend) abeg = aend = rbeg;
-    for (int64_t k = rbeg + t; k < abeg && k < rend; k += kCmpT) apply(recs[k]);
-    for (int64_t k = abeg + 4 * (int64_t)t; k < aend; k += 4 * (int64_t)kCmpT) {
-        uint4 q = *reinterpret_cast<const uint4*>(recs + k);
-        apply(q.x);
-        apply(q.y);
-        apply(q.z);
-        apply(q.w);
+    if (abeg >= aend) {
+        for (int64_t k = rbeg + t; k < rend; k += kCmpT) apply(recs[k]);
+    } else {
+        if (rbeg + t < abeg) apply(recs[rbeg + t]);
+        if (aend + t < rend) apply(recs[aend + t]);
+        const uint4* q4 = reinterpret_cast<const uint4*>(recs + abeg);
+        int64_t nq = (aend - abeg) >> 2;
+        for (int64_t k = t; k < nq; k += 4 * kCmpT) {
+            uint4 q[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[j] = k + j * kCmpT < nq ? q4[k + j * kCmpT] : make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                apply(q[j].x);
+                apply(q[j].y);
+                apply(q[j].z);
+                apply(q[j].w);
+            }
+        }
     }
-    for (int64_t k = (aend > abeg ? aend : abeg) + t; k < rend; k += kCmpT) apply(recs[k]);
     if (hub_keys) {   // hubs never emit records: their counts come from the slot table
         for (int k = t; k < kHubSlots; k += kCmpT) {
             uint32_t key = hub_keys[k];
@@ -2766,6 +2753,7 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         }
         if (lane == 0) {
             s_w[32] = prefix;
+            s_w[33] = total;
             if (tile == ntiles - 1) {
                 unsigned long long all = prefix + total;
                 b.scal[0] = (long long)(all & 0x7FFFFFFFULL);
@@ -2774,31 +2762,44 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         }
     }
     __syncthreads();
-    unsigned long long ex = s_w[32] + s_w[wid] + incl - mine;
-    int64_t i = (int64_t)(ex & 0x7FFFFFFFULL);
-    long long nb = b.sizes[0] + b.sizes[1] + (long long)(ex >> 31);
+    {   // members of this thread in tile order
+        unsigned long long ex = s_w[wid] + incl - mine;
+        int k = (int)(ex & 0x7FFFFFFFULL), nw = (int)(ex >> 31);
 #pragma unroll
-    for (int j = 0; j < kCmpIPT; ++j) {
-        if (!((pmask >> j) & 1u)) continue;
-        uint32_t g = (uint32_t)(gt + j);
-        int old = lab16[j];
-        int code = old + 1;
-        bool isnew = old == -1;
+        for (int j = 0; j < kCmpIPT; ++j) {
+            if (!((pmask >> j) & 1u)) continue;
+            s_idx[k] = (uint16_t)((l0 + j) | ((lab16[j] + 1) << 14));
+            s_nwx[k] = (uint16_t)nw;
+            nw += (nmask >> j) & 1u;
+            ++k;
+        }
+    }
+    __syncthreads();
+    // outputs, one member per thread (coalesced chunk-index writes)
+    const unsigned long long pre = s_w[32];
+    const int64_t i0 = (int64_t)(pre & 0x7FFFFFFFULL);
+    const long long nb0 = b.sizes[0] + b.sizes[1] + (long long)(pre >> 31);
+    const int cnt = (int)(s_w[33] & 0x7FFFFFFFULL);
+    for (int k = t; k < cnt; k += kCmpT) {
+        uint32_t v = s_idx[k];
+        uint32_t l = v & (kCmpSub - 1);
+        int code = (int)(v >> 14);
+        uint32_t g = (uint32_t)(g0 + l);
+        bool isnew = code == 0;
         bool active = isnew || refine;
+        int64_t i = i0 + k;
         b.nodes[i] = g;
         b.meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
         b.tlc[i] = (uint8_t)(code | (code << 4));
         b.pos[g] = (int32_t)i;
-        b.cntc[i] = s_cnt[l0 + j];
+        b.cntc[i] = s_cnt[l];
         b.nbrc[i] = isnew ? make_double2(0.0, 0.0) : b.nbr[g];
-        b.newb[i] = (int32_t)nb;   // s0 + active new nodes before i (new nodes are always active)
-        nb += isnew ? 1 : 0;
-        ++i;
+        b.newb[i] = (int32_t)(nb0 + s_nwx[k]);   // s0 + active new nodes before i (new nodes are always active)
     }
 }
 
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
-                              const BinBufs& bb, cudaStream_t s) {
+                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatSmem);
@@ -2806,19 +2807,20 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
         attr = true;
     }
     int64_t ntiles = (n + kCmpSub - 1) >> kSubShift;
-    cudaMemsetAsync(bb.bin_count, 0, sizeof(unsigned int) * (kMaxBins + 2), s);
+    const int G = num_sms();
     cudaMemsetAsync(bb.hub_cnt, 0, sizeof(unsigned long long) * kHubSlots, s);
     cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
     cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
     cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
-    k_bin_count<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.bin_count);
-    k_bin_offsets<<<1, 1024, 0, s>>>(bb.bin_count, bb.bin_cur, bb.nbins);
-    k_bin_scatter<<<(unsigned)num_sms(), kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins,
-                                                                bb.bin_cur, bb.recs, bb.hub_cnt, bb.hub_flag);
-    k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.bin_count, bb.bin_cur, bb.shift, n,
-                                                           b.hub_keys, bb.hub_cnt, bb.hub_flag, refine, b,
-                                                           bb.status, bb.ticket, ntiles);
+    k_bin_hist<<<G, kScatT, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
+    exclusive_sum_i32(bb.hist, bb.offs, (int64_t)(bb.nbins + 1) * G, temp, temp_bytes, s);
+    k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
+                                               bb.hub_cnt, bb.hub_flag);
+    k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.offs, G, bb.shift, n, b.hub_keys,
+                                                           bb.hub_cnt, bb.hub_flag, refine, b, bb.status,
+                                                           bb.ticket, ntiles);
 }
+int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * num_sms(); }
 int binned_shift(int64_t n) {
     int shift = kSubShift;
     while (((n + (1LL << shift) - 1) >> shift) > kMaxBins) ++shift;

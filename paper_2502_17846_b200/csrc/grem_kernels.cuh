@@ -16,6 +16,13 @@ namespace grem {
 constexpr int kHubSlots = 2048;
 constexpr int kMaxHubs = 1024;
 constexpr uint32_t kHubEmpty = 0xFFFFFFFFu;
+// the two candidate buckets (of kHubSlots / 2) of a key
+__host__ __device__ __forceinline__ uint32_t hub_bucket1(uint32_t u) { return (u * 0x9E3779B1u) >> 22; }
+__host__ __device__ __forceinline__ uint32_t hub_bucket2(uint32_t u) { return ((u ^ (u >> 15)) * 0x85EBCA77u) >> 22; }
+static_assert(kHubSlots == 2048, "hub buckets are 10-bit hashes");
+// host: cuckoo insertion of ids (most important first) into table[kHubSlots];
+// ids that cannot be placed are simply not hubs.  Returns the number placed.
+int hub_table_build(const uint32_t* ids, int count, uint32_t* table);
 
 struct ChunkBufs {
     // global per-node state (n)
@@ -59,8 +66,8 @@ constexpr int kMaxBins = 2048;
 constexpr int kSubShift = 14;
 struct BinBufs {
     uint32_t* recs;          // >= 2 * edges of the chunk
-    unsigned int* bin_count; // kMaxBins + 2
-    unsigned int* bin_cur;   // kMaxBins (after the scatter: end of each bin's records)
+    int32_t* hist;           // binned_hist_entries(nbins): records per (bin, scatter CTA)
+    int32_t* offs;           // its exclusive scan: record cursor per (bin, CTA); row nbins = end
     unsigned long long* hub_cnt;   // kHubSlots
     uint32_t* hub_flag;            // kHubSlots
     unsigned long long* status;    // binned_tiles(n) look-back words
@@ -69,10 +76,11 @@ struct BinBufs {
 };
 int binned_shift(int64_t n);
 int64_t binned_tiles(int64_t n);
+int64_t binned_hist_entries(int nbins);
 // writes nodes, meta, tlc, pos, cntc, nbrc, newb (incl. s0) for the chunk;
 // scal[0] = N_c, scal[2] = new nodes
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
-                              const BinBufs& bb, cudaStream_t s);
+                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
@@ -161,7 +169,6 @@ void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entri
 void launch_sample_degrees(const uint2* e, int64_t sample, int32_t* sdeg, cudaStream_t s);
 void launch_hub_keys(const uint32_t* ids, int64_t cnt, const int32_t* sdeg, unsigned long long* keys,
                      cudaStream_t s);
-void launch_build_hub_table(const unsigned long long* sorted_desc, int64_t nhubs, uint32_t* table, cudaStream_t s);
 size_t hub_select_temp_bytes(int64_t n);
 void launch_hub_select(const int32_t* sdeg, int64_t n, int32_t min_deg, uint32_t* ids, long long* d_count, void* temp,
                        size_t temp_bytes, cudaStream_t s);

@@ -111,7 +111,8 @@ struct grem_ctx {
     // per node
     DBuf<int8_t> lab{"lab"};
     DBuf<uint32_t> lab2{"lab2"}, bin_recs{"bin_recs"};
-    DBuf<unsigned int> bin_count{"bin_count"}, bin_cur{"bin_cur"}, bin_ticket{"bin_ticket"};
+    DBuf<unsigned int> bin_ticket{"bin_ticket"};
+    DBuf<int32_t> bin_hist{"bin_hist"}, bin_offs{"bin_offs"};
     DBuf<unsigned long long> bin_hcnt{"bin_hcnt"}, bin_status{"bin_status"};
     DBuf<uint32_t> bin_hflag{"bin_hflag"};
     DBuf<uint8_t> tl{"tl"}, flag{"flag"};
@@ -141,6 +142,7 @@ struct grem_ctx {
     DBuf<uint32_t> hub_table{"hub_table"}, hub_ids{"hub_ids"};
     DBuf<unsigned long long> hub_k1{"hub_k1"}, hub_k2{"hub_k2"};
     bool hubs_on = false;
+    uint32_t hub_host[kHubSlots];
     // scalars
     long long* d_sizes = nullptr;   // [2]
     long long* d_scal = nullptr;    // [8]
@@ -586,15 +588,17 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             int nbins = (int)((a.n + (1LL << shift) - 1) >> shift);
             int64_t ntiles = binned_tiles(a.n);
             c->bin_recs.ensure(2 * mc + 16, s);
-            c->bin_count.ensure(kMaxBins + 2, s);
-            c->bin_cur.ensure(kMaxBins, s);
+            int64_t hent = binned_hist_entries(nbins);
+            c->bin_hist.ensure(hent, s);
+            c->bin_offs.ensure(hent, s);
+            ensure_temp(c, scan_temp_bytes(hent));
             c->bin_hcnt.ensure(kHubSlots, s);
             c->bin_hflag.ensure(kHubSlots, s);
             c->bin_status.ensure(ntiles + 1, s);
             c->bin_ticket.ensure(4, s);
-            BinBufs bb{c->bin_recs.p, c->bin_count.p, c->bin_cur.p, c->bin_hcnt.p, c->bin_hflag.p, c->bin_status.p,
+            BinBufs bb{c->bin_recs.p, c->bin_hist.p, c->bin_offs.p, c->bin_hcnt.p, c->bin_hflag.p, c->bin_status.p,
                        c->bin_ticket.p, shift, nbins};
-            launch_count_init_binned(e, mc, a.n, a.refine, b, bb, s);
+            launch_count_init_binned(e, mc, a.n, a.refine, b, bb, c->temp.p, c->temp.cap, s);
             c->kernels += 9;
         } else {
             launch_count_init(e, mc, b, s);
@@ -706,6 +710,43 @@ struct Meter {
     }
 };
 
+}  // namespace
+
+// Bucketised cuckoo insertion (2 buckets x 2 slots per key); a key that is
+// still homeless after the displacement budget drops out of the hub set
+// (hubs only change performance, never results).
+int grem::hub_table_build(const uint32_t* ids, int count, uint32_t* table) {
+    for (int k = 0; k < kHubSlots; ++k) table[k] = kHubEmpty;
+    int placed = 0;
+    uint32_t rng = 0x12345u;
+    for (int i = 0; i < count; ++i) {
+        uint32_t key = ids[i];
+        bool dup = false;
+        for (uint32_t bk : {hub_bucket1(key), hub_bucket2(key)})
+            for (int s2 = 0; s2 < 2; ++s2) dup |= table[2 * bk + s2] == key;
+        if (dup) continue;
+        bool ok = false;
+        for (int kick = 0; kick < 256 && !ok; ++kick) {
+            uint32_t b1 = hub_bucket1(key), b2 = hub_bucket2(key);
+            for (uint32_t bk : {b1, b2})
+                for (int s2 = 0; s2 < 2 && !ok; ++s2)
+                    if (table[2 * bk + s2] == kHubEmpty) {
+                        table[2 * bk + s2] = key;
+                        ok = true;
+                    }
+            if (ok) break;
+            rng = rng * 1664525u + 1013904223u;
+            uint32_t bk = (rng >> 16) & 1 ? b1 : b2;
+            int s2 = (rng >> 17) & 1;
+            std::swap(key, table[2 * bk + s2]);   // evict and re-home the victim
+        }
+        if (ok) ++placed;   // else `key` (the original or a victim) is dropped
+    }
+    return placed;
+}
+
+namespace {
+
 // Hubs of this bisection: top-kMaxHubs endpoints of a 4M-edge sample of the
 // level's edge list (edges are in random order, so the sample ranks degrees);
 // only worthwhile for large chunks.  Performance only: results never depend
@@ -736,7 +777,15 @@ void detect_hubs(grem_ctx* c, const BisectArgs& a) {
     ensure_temp(c, sort_temp_bytes(cnt));
     launch_hub_keys(c->hub_ids.p, cnt, c->scratch.p, c->hub_k1.p, s);
     sort_keys_u64_desc(c->hub_k1.p, c->hub_k2.p, cnt, c->temp.p, c->temp.cap, s);
-    launch_build_hub_table(c->hub_k2.p, cnt < kMaxHubs ? cnt : kMaxHubs, c->hub_table.p, s);
+    int nh = (int)(cnt < kMaxHubs ? cnt : kMaxHubs);
+    std::vector<unsigned long long> top(nh);
+    CK(cudaMemcpyAsync(top.data(), c->hub_k2.p, sizeof(unsigned long long) * nh, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<uint32_t> ids(nh);
+    for (int k = 0; k < nh; ++k) ids[k] = (uint32_t)(top[k] & 0xFFFFFFFFULL);
+    hub_table_build(ids.data(), nh, c->hub_host);
+    CK(cudaMemcpyAsync(c->hub_table.p, c->hub_host, sizeof(uint32_t) * kHubSlots, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
     c->kernels += 4;
     c->hubs_on = true;
 }
@@ -1109,7 +1158,7 @@ void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_
 void init_ctx(grem_ctx* c, int device, bool child = false) {
     c->device = device;
     CK(cudaSetDevice(device));
-    static const int prio_mode = getenv("GREM_PRIO") ? atoi(getenv("GREM_PRIO")) : 2;
+    static const int prio_mode = getenv("GREM_PRIO") ? atoi(getenv("GREM_PRIO")) : 1;
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     bool high = (prio_mode == 1 && !child) || (prio_mode == 2 && child);
@@ -1425,8 +1474,8 @@ void grem_destroy(grem_ctx* c) {
     c->lab.release();
     c->lab2.release();
     c->bin_recs.release();
-    c->bin_count.release();
-    c->bin_cur.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
+    c->bin_hist.release();
+    c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
     c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
     c->rank.release(); c->scratch.release(); c->newid.release();
     c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
