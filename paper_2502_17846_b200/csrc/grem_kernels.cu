@@ -342,7 +342,8 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
                                                               const int32_t* __restrict__ pos,
                                                               unsigned long long* __restrict__ cntc,
                                                               const uint32_t* __restrict__ hub_keys,
-                                                              const long long* __restrict__ gate) {
+                                                              const long long* __restrict__ gate,
+                                                              uint8_t* __restrict__ dirty) {
     if (gate && *gate == 0) return;   // previous round changed nothing (converged)
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
@@ -361,13 +362,22 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
         int cur = t & 0xF, prev = t >> 4;
         unsigned long long d = enc_label(cur) - enc_label(prev);
         int hb = hub_find(s_keys, b);
-        if (hb >= 0) atomicAdd(&s_cnt[hb], d);
-        else atomicAdd(&cntc[pos[b]], d);
+        if (hb >= 0) {
+            atomicAdd(&s_cnt[hb], d);
+        } else {
+            int32_t pb = pos[b];
+            atomicAdd(&cntc[pb], d);
+            dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
+        }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
         uint32_t key = s_keys[k];
-        if (key != kHubEmpty && s_cnt[k]) atomicAdd(&cntc[pos[key]], s_cnt[k]);
+        if (key != kHubEmpty && s_cnt[k]) {
+            int32_t pk = pos[key];
+            atomicAdd(&cntc[pk], s_cnt[k]);
+            dirty[pk / kRTileC] = 1;
+        }
     }
 }
 
@@ -382,7 +392,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate);
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur);
 }
 
 // -------------------------------------------------- binned round-1 counting
@@ -616,6 +626,7 @@ constexpr int kRT = 512;             // threads per tile
 constexpr int kRI = 8;               // nodes per thread
 constexpr int kRTile = kRT * kRI;    // == kScanTile
 static_assert(kRTile == kScanTile, "round tiles reuse the scan tile buffers");
+static_assert(kRTile == kRTileC, "dirty-tile granularity");
 
 struct RoundArgs {
     const uint32_t* nodes;
@@ -627,6 +638,9 @@ struct RoundArgs {
     long long cap;
     int64_t nc;
     const long long* gate;   // nullptr or the previous round's changed count (0: converged, skip)
+    const uint8_t* dcur;     // incremental rounds: tiles whose inputs changed since the last round
+    uint8_t* dnext;          // tiles whose tie guesses changed (dirty in the next round)
+    int incremental;         // skip clean tiles (round >= 3)
 };
 
 __device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t* v) {
@@ -661,6 +675,9 @@ __device__ __forceinline__ long long node_sl(uint8_t m, int32_t nb) {
 
 __global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_agg, int first_round) {
     if (a.gate && *a.gate == 0) return;
+    // a clean tile (no count change, no tie-guess change) keeps its preferences
+    // and its aggregate from the previous round
+    if (a.incremental && !a.dcur[blockIdx.x]) return;
     __shared__ Clamp smem[kRT / 32];
     __shared__ Clamp stotal;
     int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
@@ -708,9 +725,23 @@ struct RoundOut {
 __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
     if (a.gate && *a.gate == 0) return;
     __shared__ Clamp smem[kRT / 32];
-    __shared__ long long sbad;
-    if (threadIdx.x == 0) sbad = kInf;
+    __shared__ long long sbad, sfirst;
+    __shared__ int sspec;
+    if (threadIdx.x == 0) {
+        sbad = sfirst = kInf;
+        sspec = 0;
+    }
     int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
+    if (a.incremental && !a.dcur[blockIdx.x] && (long long)out.x[(int64_t)blockIdx.x * kRTile] == tile_x[blockIdx.x]) {
+        // clean tile entered with last round's exact x: every decision, tie
+        // guess and x is what the last round computed; only the second window
+        // centre (this round's exact x) needs the copy
+        int32_t xs[kRI];
+        load8_32(out.x + base, xs);
+        store8_32(out.xalt + base, xs);
+        if (base + kRI > a.nc && base <= a.nc) out.xalt[a.nc] = out.x[a.nc];
+        return;
+    }
     uint8_t m[kRI];
     int32_t nb[kRI];
     uint32_t g[kRI];
@@ -726,7 +757,7 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     load8_u8(out.tlc + base, tc);
     int32_t xs[kRI];
     int nbad = 0, ch = 0;
-    long long mybad = kInf;
+    long long mybad = kInf, mybad_ch = kInf;
 #pragma unroll
     for (int j = 0; j < kRI; ++j) {
         xs[j] = (int32_t)x;
@@ -744,12 +775,14 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
             tc[j] = (uint8_t)(code | (cur << 4));
             if (code != cur) {
                 ch++;
+                if (base + j < mybad_ch) mybad_ch = base + j;
                 out.tl[g[j]] = tc[j];
                 atomicOr(&out.chg[g[j] >> 5], 1u << (g[j] & 31));
             }
             // next round's tie guess: the tie rule at this x
             bool tie0 = (x - nm.o) <= (sl >> 1);
             m[j] = (uint8_t)(tie0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
+            if (meta_pref(mm) == 2 && m[j] != mm) sspec = 1;   // a tie's map changes next round
             x = clamp_apply(nm.f, x);
         }
     }
@@ -763,18 +796,23 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
         ch += __shfl_down_sync(0xffffffffu, ch, off);
     }
     if (mybad != kInf) atomicMin(&sbad, mybad);
+    if (mybad_ch != kInf) atomicMin(&sfirst, mybad_ch);
     if ((threadIdx.x & 31) == 0) {
         if (nbad) atomicAdd((unsigned long long*)(out.scal + 4), (unsigned long long)nbad);
         if (ch) atomicAdd((unsigned long long*)(out.scal + 1), (unsigned long long)ch);
     }
     __syncthreads();
     if (threadIdx.x == 0 && sbad != kInf) atomicMin(out.scal + 6, sbad);
+    if (threadIdx.x == 0 && sfirst != kInf) atomicMin(out.scal + 9, sfirst);   // first changed decision
+    if (threadIdx.x == 0 && sspec) a.dnext[blockIdx.x] = 1;
 }
 
 __global__ void k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p, long long* tile_x,
                                  const long long* gate);
-void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s) {
-    RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc, first_round ? nullptr : b.gate};
+void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, int incremental,
+                       cudaStream_t s) {
+    RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc, first_round ? nullptr : b.gate,
+                b.dcur, b.dnext, incremental};
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
     k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
@@ -1093,6 +1131,7 @@ struct BundleFix {
     uint32_t* chg;
     int32_t* xalt;
     long long* changed;
+    uint8_t* dnext;   // tie-guess changes make the tile dirty next round
 };
 
 template <int NWIN>
@@ -1188,7 +1227,9 @@ __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __re
         }
         uint8_t m = fx.meta[i];
         bool tie0 = (cur - o) <= (node_sl(m, fx.newb[i]) >> 1);
-        fx.meta[i] = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
+        uint8_t m2 = (uint8_t)(tie0 ? (m & ~M_SPEC) : (m | M_SPEC));
+        fx.meta[i] = m2;
+        if (m2 != m && meta_pref(m) == 2) fx.dnext[i / kRTile] = 1;
     }
     for (int off = 16; off; off >>= 1) dch += __shfl_down_sync(0xffffffffu, dch, off);
     if ((threadIdx.x & 31) == 0 && dch) atomicAdd((unsigned long long*)fx.changed, (unsigned long long)dch);
@@ -1216,7 +1257,7 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     const long long* nbad = b.scal + 4;
     const long long* first_bad = b.scal + 6;
     BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
-                 fix_decisions ? b.scal + 1 : nullptr};
+                 fix_decisions ? b.scal + 1 : nullptr, b.dnext};
     k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
     int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;

@@ -56,7 +56,10 @@ struct ChunkBufs {
     const uint32_t* hub_keys;   // kHubSlots table or nullptr (no hubs)
     uint32_t* lab2;             // 2-bit mirror of lab (code = label + 1), L2-resident gathers
     const long long* gate;      // scal + 7: changed count of the previous round (round kernels skip on 0)
+    uint8_t* dcur;              // per round tile: inputs changed since the last round (incremental rounds)
+    uint8_t* dnext;             // per round tile: dirty in the next round
 };
+constexpr int kRTileC = 4096;   // nodes per round tile (kRT * kRI in grem_kernels.cu)
 
 // Round-1 counts of large chunks (propagation blocking): edges emit
 // (node, label code) records binned by coarse node range (2^shift ids,
@@ -112,7 +115,8 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
                    cudaStream_t s, bool fix_decisions);
 // fused round: preferences + clamp tile aggregates, top scan, x / tie check /
 // speculative decisions (node arrays padded to whole kScanTile tiles)
-void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, cudaStream_t s);
+void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, int incremental,
+                       cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 void launch_round_gate(const ChunkBufs& b, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);

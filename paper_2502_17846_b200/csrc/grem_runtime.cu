@@ -126,6 +126,7 @@ struct grem_ctx {
     DBuf<double2> nbrc{"nbrc"};
     DBuf<uint8_t> tlc{"tlc"};
     DBuf<uint32_t> chg{"chg"};
+    DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
     DBuf<Clamp> tile_agg{"tile_agg"};
@@ -356,6 +357,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.hub_keys = c->hubs_on ? c->hub_table.p : nullptr;
     b.lab2 = c->lab2.p;
     b.gate = nullptr;
+    b.dcur = c->dirty0.p;
+    b.dnext = c->dirty1.p;
     return b;
 }
 
@@ -629,7 +632,19 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     // kernel is gated on the device by the previous round's changed count, so
     // rounds after the fixpoint are no-ops; the host checks once per batch.
     static const int batch = getenv("GREM_ROUND_BATCH") ? std::max(1, atoi(getenv("GREM_ROUND_BATCH"))) : 2;
+    // Incremental rounds (r >= 3): a round tile whose counts and tie guesses
+    // did not change and whose incoming x equals last round's exact x is
+    // skipped (its decisions are already the fixpoint's for that input).
+    static const bool incr_on = !getenv("GREM_NO_INCREMENTAL");
+    int64_t rtiles = (nc + 1 + kRTileC - 1) / kRTileC;
+    c->dirty0.ensure(rtiles + 1, s);
+    c->dirty1.ensure(rtiles + 1, s);
+    uint8_t* dbuf[2] = {c->dirty0.p, c->dirty1.p};
     for (int r = 1;; ++r) {
+        b.dcur = dbuf[r & 1];
+        b.dnext = dbuf[(r + 1) & 1];
+        CK(cudaMemsetAsync(b.dnext, 0, rtiles + 1, s));
+        if (r == 1) CK(cudaMemsetAsync(b.dcur, 1, rtiles + 1, s));
         if (r > 1) {
             PhaseScope ps(c, PH_DELTA);
             launch_count_delta(e, mc, b, s);
@@ -639,9 +654,10 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
         CK(cudaMemsetAsync(c->d_scal + 6, 0x7F, sizeof(long long), s));   // first bad = +large
+        CK(cudaMemsetAsync(c->d_scal + 9, 0x7F, sizeof(long long), s));   // first changed = +large
         {
             PhaseScope ps(c, PH_SCAN);
-            launch_round_scan(b, nc, a.cap, r == 1, s);
+            launch_round_scan(b, nc, a.cap, r == 1, incr_on && r >= 3, s);
             c->kernels += 3;
         }
         {
@@ -661,9 +677,10 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         launch_round_gate(b, s);
         c->kernels++;
         if (getenv("GREM_DEBUG_BUNDLE")) {
-            scal_read(c, c->d_scal + 1, 4);
-            fprintf(stderr, "[bundle] round %d nc %lld changed %lld nbad %lld misses(cum) %lld\n", r, (long long)nc,
-                    c->h_pin[0], c->h_pin[3], c->h_pin[2]);
+            scal_read(c, c->d_scal + 1, 9);
+            fprintf(stderr, "[bundle] n %lld round %d nc %lld changed %lld first %lld nbad %lld misses(cum) %lld\n",
+                    (long long)a.n, r, (long long)nc, c->h_pin[0], c->h_pin[8] > nc ? -1LL : c->h_pin[8], c->h_pin[3],
+                    c->h_pin[2]);
         }
         // this round's exact x becomes the next round's second window centre
         // (after the fixpoint the swaps are harmless: nothing reads xalt)
