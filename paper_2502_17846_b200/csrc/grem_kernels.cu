@@ -2107,15 +2107,47 @@ __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long
     for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) sh[j] = 0;
     __syncthreads();
     int lm = -1, anyneg = 0;
-    GRID_STRIDE(i, n) {
-        int l = lab[i];
-        if (l < 0) {
-            anyneg = 1;
-            continue;
+    const int lane = threadIdx.x & 31;
+    if (nb <= 32 && ((uintptr_t)lab & 15) == 0) {
+        // few parts: warp ballots per part instead of same-address atomics;
+        // lane b keeps the count of part b
+        unsigned long long mine = 0;
+        int64_t nw4 = n / 4;
+        const int4* l4 = reinterpret_cast<const int4*>(lab);
+        for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; w < nw4;
+             w += (int64_t)gridDim.x * blockDim.x) {
+            int4 q = w + lane < nw4 ? l4[w + lane] : make_int4(-2, -2, -2, -2);
+            int v[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                anyneg |= v[j] == -1 || (v[j] < -2);
+                lm = v[j] > lm ? v[j] : lm;
+                for (int b = 0; b < nb; ++b) {
+                    unsigned bal = __ballot_sync(0xffffffffu, v[j] == b);
+                    if (lane == b) mine += __popc(bal);
+                }
+            }
         }
-        lm = l > lm ? l : lm;
-        if (l < nb) atomicAdd(&sh[l], 1ULL);
-        else if (l < cap) atomicAdd(&sizes[l], 1ULL);
+        if (blockIdx.x == 0 && threadIdx.x < 32) {   // tail
+            for (int64_t i = nw4 * 4 + threadIdx.x; i < n; i += 32) {
+                int l = lab[i];
+                if (l < 0) { anyneg = 1; continue; }
+                lm = l > lm ? l : lm;
+                if (l < nb) atomicAdd(&sh[l], 1ULL);
+            }
+        }
+        if (lane < nb && mine) atomicAdd(&sh[lane], mine);
+    } else {
+        GRID_STRIDE(i, n) {
+            int l = lab[i];
+            if (l < 0) {
+                anyneg = 1;
+                continue;
+            }
+            lm = l > lm ? l : lm;
+            if (l < nb) atomicAdd(&sh[l], 1ULL);
+            else if (l < cap) atomicAdd(&sizes[l], 1ULL);
+        }
     }
     for (int off = 16; off; off >>= 1) {
         int o = __shfl_down_sync(0xffffffffu, lm, off);
@@ -2276,13 +2308,25 @@ __global__ void __launch_bounds__(kSplitT) k_split_edges(const uint2* __restrict
     uint2 ed[kSplitI];
     int side[kSplitI];
     uint32_t rank[kSplitI];
+    // all edge loads, then all side-map gathers, in flight before any use
+    uint2 dd[kSplitI], wa[kSplitI], wb[kSplitI];
 #pragma unroll
     for (int k = 0; k < kSplitI; ++k) {
         int64_t i = base + (int64_t)k * kSplitT + threadIdx.x;   // warp-striped: coalesced loads
+        dd[k] = i < m ? __ldcs(e + i) : make_uint2(0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < kSplitI; ++k) {
+        wa[k] = wi[dd[k].x >> 5];
+        wb[k] = wi[dd[k].y >> 5];
+    }
+#pragma unroll
+    for (int k = 0; k < kSplitI; ++k) {
+        int64_t i = base + (int64_t)k * kSplitT + threadIdx.x;
         side[k] = 2;
         if (i < m) {
-            uint2 d = e[i];
-            uint2 a = wi[d.x >> 5], b = wi[d.y >> 5];
+            uint2 d = dd[k];
+            uint2 a = wa[k], b = wb[k];
             uint32_t su = (a.x >> (d.x & 31)) & 1u, sv = (b.x >> (d.y & 31)) & 1u;
             if (su == sv) {
                 uint32_t r1u = a.y + __popc(a.x & ((1u << (d.x & 31)) - 1u));
