@@ -11,7 +11,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgrem_b200.so")
+# GREM_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("GREM_LIB") or os.path.join(_HERE, "libgrem_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 _lib = None
 

@@ -2602,7 +2602,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
 
 constexpr int kScatIPT = 8;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
-constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * 3 + (size_t)2 * kScatBatch * 4 + 64 * 4;
+constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8) + (size_t)2 * kScatBatch * 4 + 64 * 4;
 
 __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
@@ -2618,7 +2618,9 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
     unsigned int* s_hist = s_hflag + kHubSlots;
     unsigned int* s_start = s_hist + kMaxBins;
     unsigned int* s_cur = s_start + kMaxBins;
-    uint32_t* s_out = s_cur + kMaxBins;
+    unsigned int* s_beg = s_cur + kMaxBins;       // first record slot of this CTA's region per bin
+    uint32_t* s_carry = s_beg + kMaxBins;         // per bin: the open (incomplete) 32-byte sector
+    uint32_t* s_out = s_carry + 8 * kMaxBins;
     unsigned int* s_w = s_out + 2 * kScatBatch;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     hub_load(s_keys, hub_keys);
@@ -2626,7 +2628,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         s_hcnt[k] = 0ULL;
         s_hflag[k] = 0u;
     }
-    for (int k = t; k < nbins; k += kScatT) s_cur[k] = (unsigned int)offs[(int64_t)k * gridDim.x + blockIdx.x];
+    for (int k = t; k < nbins; k += kScatT) s_beg[k] = s_cur[k] = (unsigned int)offs[(int64_t)k * gridDim.x + blockIdx.x];
     int64_t lo, hi;
     cta_range(m, lo, hi);
     for (int64_t b0 = lo; b0 < hi; b0 += kScatBatch) {
@@ -2699,18 +2701,42 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
 #pragma unroll
         for (int k = 0; k < 2 * kScatIPT; ++k)
             if (rec[k] != 0xFFFFFFFFu) s_out[s_start[(rec[k] >> 2) >> shift] + rk[k]] = rec[k];
+        // Records leave in whole 32-byte sectors: a bin's open sector waits in
+        // shared memory until this CTA's next run of that bin completes it
+        // (partial sectors would cost a DRAM read-modify-write).
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {   // flush open sectors this batch completes
+            int k = 2 * t + h;
+            unsigned int v = h ? v1 : v0;
+            if (k < nbins && v) {
+                unsigned int cur = s_cur[k], sec = cur & ~7u;
+                if ((cur & 7u) && cur + v >= sec + 8) {
+                    unsigned int lo = s_beg[k] > sec ? s_beg[k] : sec;
+                    for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[8 * k + (p & 7u)];
+                }
+            }
+        }
         __syncthreads();
         unsigned int nrec = s_w[32];
         for (unsigned int k = t; k < nrec; k += kScatT) {   // runs of a bin are contiguous
             uint32_t r = s_out[k];
             unsigned int bb = (r >> 2) >> shift;
-            recs[s_cur[bb] + (k - s_start[bb])] = r;
+            unsigned int p = s_cur[bb] + (k - s_start[bb]);
+            if (p < ((s_cur[bb] + s_hist[bb]) & ~7u)) recs[p] = r;
+            else s_carry[8 * bb + (p & 7u)] = r;
         }
         __syncthreads();
         if (2 * t < nbins) s_cur[2 * t] += v0;
         if (2 * t + 1 < nbins) s_cur[2 * t + 1] += v1;
     }
     __syncthreads();
+    for (int k = t; k < nbins; k += kScatT) {   // the last open sectors
+        unsigned int cur = s_cur[k], sec = cur & ~7u;
+        if (cur & 7u) {
+            unsigned int lo = s_beg[k] > sec ? s_beg[k] : sec;
+            for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[8 * k + (p & 7u)];
+        }
+    }
     for (int k = t; k < kHubSlots; k += kScatT) {
         if (s_keys[k] == kHubEmpty) continue;
         if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
@@ -2718,8 +2744,8 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
     }
 }
 
-constexpr int kCmpT = 1024;
 constexpr int kCmpSub = 1 << kSubShift;              // nodes per tile
+constexpr int kCmpT = kCmpSub / 16;
 constexpr int kCmpIPT = kCmpSub / kCmpT;             // 16 consecutive nodes per thread
 constexpr size_t kCmpSmem = (size_t)kCmpSub * (8 + 2 + 2) + (size_t)kCmpSub / 8 + 64 * 8;
 static_assert(kCmpIPT == 16, "16 nodes per thread (one 16-byte label load)");
@@ -2821,7 +2847,7 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
     if (lane == 31) s_w[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-        unsigned long long w = s_w[lane], wi = w;
+        unsigned long long w = lane < kCmpT / 32 ? s_w[lane] : 0ULL, wi = w;
         for (int off = 1; off < 32; off <<= 1) {
             unsigned long long o = __shfl_up_sync(0xffffffffu, wi, off);
             if (lane >= off) wi += o;

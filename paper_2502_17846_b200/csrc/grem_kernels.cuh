@@ -66,7 +66,10 @@ constexpr int kRTileC = 4096;   // nodes per round tile (kRT * kRI in grem_kerne
 // <= kMaxBins bins); one CTA per 2^kSubShift-node tile then accumulates its
 // records in shared memory and writes the compact chunk state directly.
 constexpr int kMaxBins = 2048;
-constexpr int kSubShift = 14;
+#ifndef GREM_SUB_SHIFT
+#define GREM_SUB_SHIFT 14
+#endif
+constexpr int kSubShift = GREM_SUB_SHIFT;   // nodes per compact tile = 2^kSubShift (16 per thread)
 struct BinBufs {
     uint32_t* recs;          // >= 2 * edges of the chunk
     int32_t* hist;           // binned_hist_entries(nbins): records per (bin, scatter CTA)

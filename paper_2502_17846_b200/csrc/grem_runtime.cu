@@ -820,12 +820,27 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
         cudaEventCreate(&lv1);
         cudaEventRecord(lv0, s);
     }
+    double ph0[PH_N];
+    if (dbg_levels && c->profiling) {   // per-bisection phase split (debug): fold the open events first
+        cudaStreamSynchronize(s);
+        prof_collect(c);
+        for (int k = 0; k < PH_N; ++k) ph0[k] = c->phase_ms[k];
+    }
     struct LevelLog {
-        grem_ctx* c; cudaEvent_t a, b; const BisectArgs& args; int64_t r0, v0, b0;
+        grem_ctx* c; cudaEvent_t a, b; const BisectArgs& args; int64_t r0, v0, b0; const double* ph0;
         ~LevelLog() {
             if (!a) return;
             cudaEventRecord(b, c->s);
             cudaEventSynchronize(b);
+            if (c->profiling) {
+                prof_collect(c);
+                std::string line;
+                for (int k = 0; k < PH_N; ++k) {
+                    double d = c->phase_ms[k] - ph0[k];
+                    if (d >= 0.05) line += std::string(" ") + kPhaseNames[k] + "=" + std::to_string(d).substr(0, 6);
+                }
+                fprintf(stderr, "[phases] n %lld m %lld:%s\n", (long long)args.n, (long long)args.m, line.c_str());
+            }
             float ms = 0, t0 = -1, t1 = -1;
             cudaEventElapsedTime(&ms, a, b);
             if (g_dbg_t0) {   // timeline relative to the start of partition()
@@ -839,7 +854,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
             cudaEventDestroy(a);
             cudaEventDestroy(b);
         }
-    } level_log{c, lv0, lv1, a, r0, v0, b0};
+    } level_log{c, lv0, lv1, a, r0, v0, b0, ph0};
     if (a.n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
     // bundle tables pack a threshold and a lift into one int32 (t * 4 + o)
     if (a.n >= (1LL << 29)) fail(GREM_E_FORMAT, "bisections over 2^29 or more nodes are not supported");
