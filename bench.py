@@ -267,7 +267,7 @@ def main():
         achieved = st_l0["delta_bytes"] / (d_ms / 1e3) / 1e9
         traffic = None
         try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["k_count_delta"]
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r01b_traffic.json")))["k_count_delta"]
             traffic = tr["dram_bytes_per_launch"]
         except Exception:  # noqa: BLE001
             pass
