@@ -74,12 +74,23 @@ __host__ __device__ __forceinline__ NodeMap node_map(uint8_t m, long long s_l, l
     } else if (pref == 1) {   // wants side 1: b=0 iff side 1 is full
         r.f = Clamp{-o, s_l - cap + 1, kInf};
         r.t = s_l - cap;
-    } else {                  // tie: smaller side, ties to 0 (speculated in f)
-        long long spec1 = (m & M_SPEC) ? 1 : 0;
-        r.f = Clamp{1 - spec1 - o, -kInf, kInf};
+    } else {
+        // tie: smaller side, ties to 0.  The exact map x -> x - o + [x - o <= t]
+        // is not a clamp; it is speculated as the clamp of the guessed side,
+        // which is exact on a one-step-wider region and, like the true map,
+        // absorbs a +-1 shift of x at the threshold (so a trajectory perturbed
+        // upstream re-merges instead of mis-speculating every later tie):
+        //   guess 0: min(x + 1 - o, t + 1), exact iff x - o <= t + 1
+        //   guess 1: max(x - o, t + 1),     exact iff x - o >= t
         r.t = s_l >> 1;
+        if (m & M_SPEC) r.f = Clamp{-o, r.t + 1, kInf};
+        else r.f = Clamp{1 - o, -kInf, r.t + 1};
     }
     return r;
+}
+// the speculated clamp of a tie was not exact at input x (repair needed)
+__host__ __device__ __forceinline__ bool tie_misspeculated(uint8_t m, long long x, const NodeMap& nm) {
+    return (m & M_SPEC) ? (x - nm.o < nm.t) : (x - nm.o > nm.t + 1);
 }
 
 __device__ __forceinline__ unsigned long long enc_label(int code) {

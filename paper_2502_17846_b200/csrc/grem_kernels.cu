@@ -203,9 +203,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down_chunk(Src src, int64
         uint8_t m = out.meta[i];
         uint8_t isbad = 0;
         if (meta_active(m) && meta_pref(m) == 2) {
-            int b = (x - nm.o <= nm.t) ? 0 : 1;
-            int spec = (m & M_SPEC) ? 1 : 0;
-            if (b != spec) {
+            if (tie_misspeculated(m, x, nm)) {
                 isbad = 1;
                 if (i < mybad) mybad = i;
                 nb++;
@@ -766,7 +764,7 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
             long long sl = node_sl(mm, nb[j]);
             NodeMap nm = node_map(mm, sl, a.cap);
             int b = (x - nm.o <= nm.t) ? 0 : 1;
-            if (meta_pref(mm) == 2 && b != ((mm & M_SPEC) ? 1 : 0)) {   // mis-speculated tie
+            if (meta_pref(mm) == 2 && tie_misspeculated(mm, x, nm)) {   // mis-speculated tie
                 nbad++;
                 if (base + j < mybad) mybad = base + j;
             }

@@ -160,5 +160,12 @@ def test_node_maps_match_assign_exhaustive():
                         elif pref == 1:
                             f = (-o, sl - cap + 1, INF)
                         else:
-                            f = (1 - o - b, -INF, INF)   # tie with a correct speculation
+                            # tie speculated as the clamp of the guessed side
+                            # (grem_core.cuh node_map): exact on its region
+                            for guess in (0, 1):
+                                f = (1 - o, -INF, t + 1) if guess == 0 else (-o, t + 1, INF)
+                                exact = (x - o <= t + 1) if guess == 0 else (x - o >= t)
+                                if exact:
+                                    assert apply(f, x) == xn
+                            continue
                         assert apply(f, x) == xn
