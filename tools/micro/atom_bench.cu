@@ -17,6 +17,36 @@ __global__ void k_smem(int iters, unsigned long long* out) {
     __syncthreads();
     if (threadIdx.x == 0) atomicAdd(out, c[0]);
 }
+// same, but the old value is used (rank-style ATOMS with return)
+template <int NODES>
+__global__ void k_smem_ret(int iters, unsigned long long* out) {
+    extern __shared__ uint32_t c[];
+    for (int i = threadIdx.x; i < 2 * NODES; i += blockDim.x) c[i] = 0;
+    __syncthreads();
+    uint32_t s = hsh(blockIdx.x * 1024 + threadIdx.x), acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        s = hsh(s);
+        acc += atomicAdd(&c[s & (2 * NODES - 1)], 1u);
+    }
+    __syncthreads();
+    if (acc == 0xFFFFFFFFu) atomicAdd(out, acc);
+}
+// 8 independent ATOMS with return in flight per thread (the scatter's pattern)
+__global__ void k_smem_ret8(int iters, unsigned long long* out, int mask) {
+    extern __shared__ uint32_t c[];
+    for (int i = threadIdx.x; i <= mask; i += blockDim.x) c[i] = 0;
+    __syncthreads();
+    uint32_t s = hsh(blockIdx.x * 1024 + threadIdx.x), acc = 0;
+    for (int i = 0; i < iters; i += 8) {
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { s = hsh(s); r[j] = atomicAdd(&c[s & mask], 1u); }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += r[j];
+    }
+    __syncthreads();
+    if (acc == 0xFFFFFFFFu) atomicAdd(out, acc);
+}
 __global__ void k_glob(int iters, uint32_t* c, uint32_t mask) {
     uint32_t s = hsh(blockIdx.x * 1024 + threadIdx.x);
     for (int i = 0; i < iters; ++i) {
@@ -50,6 +80,25 @@ int main() {
             cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
             double ops = 5.0 * grid * threads * iters;
             printf("smem atomics 128KB table, %d thr x %d CTAs: %.1f G atom/s\n", threads, grid, ops / ms / 1e6);
+        }
+    }
+    {
+        constexpr int NODES = 16384;
+        size_t sm = 2 * NODES * 4;
+        cudaFuncSetAttribute(k_smem_ret<NODES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_smem_ret8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        int threads = 1024, grid = sms;
+        k_smem_ret<NODES><<<grid, threads, sm>>>(iters, out);
+        cudaEventRecord(a);
+        for (int r = 0; r < 5; ++r) k_smem_ret<NODES><<<grid, threads, sm>>>(iters, out);
+        cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+        printf("smem atomics WITH return (dependent use), 1024 thr: %.1f G atom/s\n", 5.0 * grid * threads * iters / ms / 1e6);
+        for (int mask : {2047, 32767}) {
+            k_smem_ret8<<<grid, threads, sm>>>(iters, out, mask);
+            cudaEventRecord(a);
+            for (int r = 0; r < 5; ++r) k_smem_ret8<<<grid, threads, sm>>>(iters, out, mask);
+            cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+            printf("smem atomics WITH return, 8 in flight, %d addrs: %.1f G atom/s\n", mask + 1, 5.0 * grid * threads * iters / ms / 1e6);
         }
     }
     uint32_t* c; size_t big = 1ull << 30; cudaMalloc(&c, big * 4); cudaMemset(c, 0, big * 4);
