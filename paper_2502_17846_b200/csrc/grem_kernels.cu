@@ -332,6 +332,12 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
     }
 }
 
+__device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, uint32_t g) {
+    uint32_t c = g >> shift;
+    uint32_t bit = 1u << (c & 31);
+    if (!(((volatile uint32_t*)chgc)[c >> 5] & bit)) atomicOr(&chgc[c >> 5], bit);   // mostly set already
+}
+
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
 __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __restrict__ e, int64_t m,
@@ -341,12 +347,15 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
                                                               unsigned long long* __restrict__ cntc,
                                                               const uint32_t* __restrict__ hub_keys,
                                                               const long long* __restrict__ gate,
-                                                              uint8_t* __restrict__ dirty) {
+                                                              uint8_t* __restrict__ dirty,
+                                                              const uint32_t* __restrict__ chgc, int cshift) {
     if (gate && *gate == 0) return;   // previous round changed nothing (converged)
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
+    __shared__ uint32_t s_chgc[kChgCoarseBits / 32];
     hub_load(s_keys, hub_keys);
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = 0ULL;
+    for (int k = threadIdx.x; k < kChgCoarseBits / 32; k += blockDim.x) s_chgc[k] = chgc[k];
     __syncthreads();
     int64_t lo, hi;
     cta_range(m, lo, hi);
@@ -355,6 +364,8 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
         uint32_t u = ed.x, v = ed.y;
         if (u == v) continue;
         uint32_t a = u < v ? u : v, b = u < v ? v : u;
+        uint32_t ca = a >> cshift;
+        if (!((s_chgc[ca >> 5] >> (ca & 31)) & 1u)) continue;   // coarse filter in shared memory
         if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
         uint8_t t = tl[a];
         int cur = t & 0xF, prev = t >> 4;
@@ -390,7 +401,8 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur);
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
+                                                              b.chgc, b.chg_shift);
 }
 
 // -------------------------------------------------- binned round-1 counting
@@ -717,6 +729,8 @@ struct RoundOut {
     uint8_t* tlc;      // compact codes (cur | prev << 4)
     uint8_t* tl;       // id-indexed codes, written for changed nodes only
     uint32_t* chg;     // id-indexed changed bits
+    uint32_t* chgc;    // coarse changed filter
+    int chg_shift;
     long long* scal;   // [1] changed, [4] nbad, [6] first bad
 };
 
@@ -776,6 +790,7 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
                 if (base + j < mybad_ch) mybad_ch = base + j;
                 out.tl[g[j]] = tc[j];
                 atomicOr(&out.chg[g[j] >> 5], 1u << (g[j] & 31));
+                mark_changed_coarse(out.chgc, out.chg_shift, g[j]);
             }
             // next round's tie guess: the tie rule at this x
             bool tie0 = (x - nm.o) <= (sl >> 1);
@@ -814,7 +829,7 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
     k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
-    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.scal};
+    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.chgc, b.chg_shift, b.scal};
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
 }
 
@@ -1130,6 +1145,8 @@ struct BundleFix {
     int32_t* xalt;
     long long* changed;
     uint8_t* dnext;   // tie-guess changes make the tile dirty next round
+    uint32_t* chgc;
+    int chg_shift;
 };
 
 template <int NWIN>
@@ -1218,7 +1235,10 @@ __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __re
             uint32_t g = fx.nodes[i];
             if (now) {
                 fx.tl[g] = nt;
-                if (!was) atomicOr(&fx.chg[g >> 5], 1u << (g & 31));
+                if (!was) {
+                    atomicOr(&fx.chg[g >> 5], 1u << (g & 31));
+                    mark_changed_coarse(fx.chgc, fx.chg_shift, g);
+                }
             } else if (was) {
                 atomicAnd(&fx.chg[g >> 5], ~(1u << (g & 31)));
             }
@@ -1255,7 +1275,7 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     const long long* nbad = b.scal + 4;
     const long long* first_bad = b.scal + 6;
     BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
-                 fix_decisions ? b.scal + 1 : nullptr, b.dnext};
+                 fix_decisions ? b.scal + 1 : nullptr, b.dnext, b.chgc, b.chg_shift};
     k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
     int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;
@@ -1668,32 +1688,54 @@ void launch_frontier_degrees(const SeedBufs& sb, int64_t fsize, cudaStream_t s) 
 // level expansion: every (frontier node, neighbour) pair, balanced over
 // entries; a candidate keeps its minimum discoverer rank (FIFO order of
 // _bfs_grow: queue order, then ascending neighbour id).
-__global__ void k_bfs_expand(const uint32_t* __restrict__ frontier, int64_t fsize, long long rbase,
-                             const int64_t* __restrict__ fpre, int64_t total, const int32_t* __restrict__ start,
-                             const uint32_t* __restrict__ adj, const int8_t* __restrict__ slab,
-                             uint32_t* __restrict__ disc, unsigned long long* __restrict__ cand, long long* ncand) {
-    GRID_STRIDE(k, total) {
-        // j = last index with fpre[j] <= k
-        int64_t lo = 0, hi = fsize - 1;
-        while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
-            if (fpre[mid] <= k) lo = mid; else hi = mid - 1;
+__global__ void __launch_bounds__(256) k_bfs_expand(const uint32_t* __restrict__ frontier, int64_t fsize,
+                                                    long long rbase, const int64_t* __restrict__ fpre, int64_t total,
+                                                    const int32_t* __restrict__ start,
+                                                    const uint32_t* __restrict__ adj, const int8_t* __restrict__ slab,
+                                                    uint32_t* __restrict__ disc,
+                                                    unsigned long long* __restrict__ cand, long long* ncand) {
+    // each lane expands 4 consecutive frontier-adjacency slots (one binary
+    // search for the first); first discoveries are appended warp-aggregated
+    constexpr int Q = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t wb = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * (32 * Q); wb < total;
+         wb += nwarps * 32 * Q) {
+        int64_t k0 = wb + (int64_t)lane * Q;
+        int64_t lo = 0;
+        if (k0 < total) {   // j = last index with fpre[j] <= k0
+            int64_t hi = fsize - 1;
+            while (lo < hi) {
+                int64_t mid = (lo + hi + 1) >> 1;
+                if (fpre[mid] <= k0) lo = mid; else hi = mid - 1;
+            }
         }
-        uint32_t v = frontier[lo];
-        uint32_t w = adj[start[v] + (k - fpre[lo])];
-        if (slab[w] != 2) continue;
-        uint32_t r = (uint32_t)(rbase + lo);
-        if (r < ((volatile uint32_t*)disc)[w]) {
-            uint32_t old = atomicMin(&disc[w], r);
-            if (old == 0xFFFFFFFFu) {
-                unsigned long long idx = atomicAdd((unsigned long long*)ncand, 1ULL);
-                cand[idx] = w;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            int64_t k = k0 + q;
+            bool fresh = false;
+            uint32_t w = 0;
+            if (k < total) {
+                while (lo + 1 < fsize && fpre[lo + 1] <= k) ++lo;
+                uint32_t v = frontier[lo];
+                w = adj[start[v] + (k - fpre[lo])];
+                if (slab[w] == 2) {
+                    uint32_t r = (uint32_t)(rbase + lo);
+                    if (r < ((volatile uint32_t*)disc)[w]) fresh = atomicMin(&disc[w], r) == 0xFFFFFFFFu;
+                }
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, fresh);
+            if (bal) {
+                unsigned long long base = 0;
+                if (lane == __ffs(bal) - 1) base = atomicAdd((unsigned long long*)ncand, (unsigned long long)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+                if (fresh) cand[base + __popc(bal & ((1u << lane) - 1))] = w;
             }
         }
     }
 }
 void launch_bfs_expand(const SeedBufs& sb, int64_t fsize, long long rbase, int64_t total, cudaStream_t s) {
-    k_bfs_expand<<<grid_for(total, 256, 16), 256, 0, s>>>(sb.frontier, fsize, rbase, sb.cum, total, sb.start, sb.adj,
+    k_bfs_expand<<<grid_for(total / 4 + 1, 256, 16), 256, 0, s>>>(sb.frontier, fsize, rbase, sb.cum, total, sb.start, sb.adj,
                                                          sb.slab, sb.disc, sb.cand_keys, sb.scal + 4);
 }
 

@@ -45,6 +45,8 @@ struct ChunkBufs {
     uint8_t* tlc;               // tentative label codes (cur | prev << 4) of chunk node i
     int32_t* pos;               // n: chunk index of node g (valid for this chunk's nodes)
     uint32_t* chg;              // n bits: tentative label changed in the last round (tl[g] valid)
+    uint32_t* chgc;             // kChgCoarseBits bits: some node of the 2^chg_shift-id block changed
+    int chg_shift;
     // per scan tile
     Clamp* tile_agg;
     long long* tile_x;
@@ -59,6 +61,12 @@ struct ChunkBufs {
     uint8_t* dcur;              // per round tile: inputs changed since the last round (incremental rounds)
     uint8_t* dnext;             // per round tile: dirty in the next round
 };
+constexpr int kChgCoarseBits = 1 << 17;   // coarse changed-label filter (16 KB, staged in shared memory)
+__host__ __device__ __forceinline__ int chg_coarse_shift(int64_t n) {
+    int sh = 0;
+    while ((((n + (1LL << sh) - 1) >> sh)) > kChgCoarseBits) ++sh;
+    return sh;
+}
 constexpr int kRTileC = 4096;   // nodes per round tile (kRT * kRI in grem_kernels.cu)
 
 // Round-1 counts of large chunks (propagation blocking): edges emit

@@ -125,7 +125,7 @@ struct grem_ctx {
     DBuf<unsigned long long> cntc{"cntc"};
     DBuf<double2> nbrc{"nbrc"};
     DBuf<uint8_t> tlc{"tlc"};
-    DBuf<uint32_t> chg{"chg"};
+    DBuf<uint32_t> chg{"chg"}, chgc{"chgc"};
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
@@ -267,6 +267,7 @@ void ensure_nodes(grem_ctx* c, int64_t n) {
     c->nbr.ensure(n, c->s);
     c->rank.ensure(n, c->s);
     c->chg.ensure(n / 32 + 2, c->s);
+    c->chgc.ensure(kChgCoarseBits / 32, c->s);
     c->scratch.ensure(2 * n + 2, c->s);
     c->newid.ensure(n + 1, c->s);
     ensure_temp(c, select_nodes_temp_bytes(n));
@@ -349,6 +350,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.tlc = c->tlc.p;
     b.pos = c->rank.p;   // the seed's rank array (chunk 0 only) doubles as the chunk index map
     b.chg = c->chg.p;
+    b.chgc = c->chgc.p;
+    b.chg_shift = chg_coarse_shift(c->live_n);
     b.tile_agg = c->tile_agg.p;
     b.tile_x = c->tile_x.p;
     b.tile_bad = c->tile_bad.p;
@@ -649,6 +652,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             PhaseScope ps(c, PH_DELTA);
             launch_count_delta(e, mc, b, s);
             CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));   // consumed
+            CK(cudaMemsetAsync(c->chgc.p, 0, kChgCoarseBits / 8, s));
             c->kernels++;
         }
         CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
@@ -875,6 +879,7 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     CK(cudaMemsetAsync(c->lab.p, 0xFF, a.n, s));
     CK(cudaMemsetAsync(c->lab2.p, 0, sizeof(uint32_t) * (a.n / 16 + 2), s));
     CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));
+    CK(cudaMemsetAsync(c->chgc.p, 0, kChgCoarseBits / 8, s));
     CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
     CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
     CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
