@@ -132,6 +132,12 @@ int grem_partition_shard_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_e
                              int edges_on_device, int64_t p, const grem_config* cfg, int rank, int world,
                              int32_t* labels_out);
 
+/* Device copy of the host edge list staged by the last call on this context
+ * (edges_on_device = 0); valid until the next call.  Lets a sharded caller run
+ * grem_count_cuts_u32 on the merged labels without a second upload.
+ * *dev_edges = NULL when the last call used device edges. */
+int grem_staged_edges(grem_ctx* ctx, const uint32_t** dev_edges, int64_t* num_edges);
+
 /* count_cuts (grem.py:227-252).  labels_on_device as for edges. */
 int grem_count_cuts_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
                         int edges_on_device, const int32_t* labels, int labels_on_device,

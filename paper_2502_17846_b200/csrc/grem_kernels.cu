@@ -820,6 +820,182 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     if (threadIdx.x == 0 && sspec) a.dnext[blockIdx.x] = 1;
 }
 
+// ---- single-pass round (GREM_ROUND_FUSED=1; off by default: measured no faster): preferences, tile
+// aggregate, decoupled look-back over round tiles (taken in ticket order) for
+// the tile's incoming x, then decisions -- one launch and one read of the
+// node state instead of reduce / top / down.  Look-back payloads are clamps
+// (3 x 64 bit): written, fenced, then flagged (1: aggregate, 2: inclusive).
+__device__ __forceinline__ Clamp ld_clamp_cg(const Clamp* p) {
+    Clamp c;
+    c.d = __ldcg(&p->d);
+    c.L = __ldcg(&p->L);
+    c.U = __ldcg(&p->U);
+    return c;
+}
+__device__ Clamp clamp_lookback(const Clamp* agg, const Clamp* inc, const unsigned* flag, int64_t t) {
+    const int lane = threadIdx.x & 31;
+    Clamp acc = clamp_identity();   // composite of the tiles after the current window, up to t - 1
+    int64_t j = t - 1;
+    while (true) {
+        int64_t q = j - lane;   // lane 0: nearest predecessor
+        unsigned f = 2;
+        Clamp v = clamp_identity();
+        if (q >= 0) {
+            do { f = ((volatile const unsigned*)flag)[q]; } while (f == 0);
+            __threadfence();
+            v = f == 2 ? ld_clamp_cg(inc + q) : ld_clamp_cg(agg + q);
+        }
+        unsigned incm = __ballot_sync(0xffffffffu, f == 2);
+        int stop = incm ? __ffs(incm) - 1 : 31;
+        Clamp w = clamp_identity();
+        for (int l = stop; l >= 0; --l) w = clamp_then(w, shfl_clamp(v, l));   // tile order: lane stop first
+        acc = clamp_then(w, acc);
+        if (incm) break;
+        j -= 32;
+    }
+    return acc;
+}
+
+struct FusedBufs {
+    Clamp* tile_inc;
+    unsigned* tflag;
+    unsigned* ticket;
+};
+
+__global__ void __launch_bounds__(kRT, 2) k_round_fused(RoundArgs a, Clamp* tile_agg, FusedBufs fb, RoundOut out,
+                                                     int first_round) {
+    if (a.gate && *a.gate == 0) return;
+    __shared__ int64_t s_tile;
+    __shared__ Clamp smem[kRT / 32];
+    __shared__ Clamp stotal, sprefix;
+    __shared__ long long sbad, sfirst;
+    __shared__ int sspec;
+    if (threadIdx.x == 0) {
+        s_tile = atomicAdd(fb.ticket, 1u);
+        sbad = sfirst = kInf;
+        sspec = 0;
+    }
+    __syncthreads();
+    const int64_t t = s_tile;
+    const int64_t base = t * kRTile + (int64_t)threadIdx.x * kRI;
+    const bool clean = a.incremental && !a.dcur[t];
+    uint8_t m[kRI];
+    int32_t nb[kRI];
+    load8_u8(a.meta + base, m);
+    load8_32(a.newb + base, nb);
+    const long long x0 = a.sizes[0];
+    Clamp acc = clamp_identity();
+    if (!clean) {
+#pragma unroll
+        for (int j = 0; j < kRI; ++j) {
+            uint8_t mm = m[j];
+            if (meta_active(mm)) {   // preferences: assign() inputs (grem.py:138-150)
+                unsigned long long c = a.cnt[base + j];
+                double2 nbv = make_double2(0.0, 0.0);
+                if (meta_old(mm) != -1) nbv = a.nbr[base + j];
+                double a0, a1;
+                averaged(mm, c, nbv, a0, a1);
+                int pref = a0 < a1 ? 1 : (a1 < a0 ? 0 : 2);
+                mm = (uint8_t)((mm & ~M_PREF) | (pref << M_PREF_SHIFT));
+                if (first_round) {
+                    long long o = meta_old(mm) == 0 ? 1 : 0;
+                    bool side0 = (x0 - o) <= (node_sl(mm, nb[j]) >> 1);
+                    mm = (uint8_t)(side0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
+                }
+                m[j] = mm;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) acc = clamp_then(acc, node_map(m[j], node_sl(m[j], nb[j]), a.cap).f);
+    Clamp pre = block_excl_scan<kRT>(acc, smem, &stotal);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        Clamp agg = stotal;
+        if (threadIdx.x == 0) {
+            tile_agg[t] = agg;
+            if (t == 0) fb.tile_inc[0] = agg;
+            __threadfence();
+            atomicExch(fb.tflag + t, t == 0 ? 2u : 1u);
+        }
+        Clamp prefix = t > 0 ? clamp_lookback(tile_agg, fb.tile_inc, fb.tflag, t) : clamp_identity();
+        if (threadIdx.x == 0) {
+            if (t > 0) {
+                fb.tile_inc[t] = clamp_then(prefix, agg);
+                __threadfence();
+                atomicExch(fb.tflag + t, 2u);
+            }
+            sprefix = prefix;
+        }
+    }
+    __syncthreads();
+    const long long xin = clamp_apply(sprefix, x0);
+    if (clean && (long long)out.x[t * kRTile] == xin) {
+        // clean tile entered with last round's exact x: decisions, tie guesses
+        // and x are the last round's; only the next window-centre buffer is copied
+        int32_t xs[kRI];
+        load8_32(out.x + base, xs);
+        store8_32(out.xalt + base, xs);
+        if (base + kRI > a.nc && base <= a.nc) out.xalt[a.nc] = out.x[a.nc];
+        return;
+    }
+    if (!clean) store8_u8(a.meta + base, m);   // preference bits (tie guesses are rewritten below)
+    long long x = clamp_apply(pre, xin);
+    uint32_t g[kRI];
+    load8_32(a.nodes + base, g);
+    uint8_t tc[kRI];
+    load8_u8(out.tlc + base, tc);
+    int32_t xs[kRI];
+    int nbad = 0, ch = 0;
+    long long mybad = kInf, mybad_ch = kInf;
+#pragma unroll
+    for (int j = 0; j < kRI; ++j) {
+        xs[j] = (int32_t)x;
+        uint8_t mm = m[j];
+        if (meta_active(mm)) {
+            long long sl = node_sl(mm, nb[j]);
+            NodeMap nm = node_map(mm, sl, a.cap);
+            int b = (x - nm.o <= nm.t) ? 0 : 1;
+            if (meta_pref(mm) == 2 && tie_misspeculated(mm, x, nm)) {   // mis-speculated tie
+                nbad++;
+                if (base + j < mybad) mybad = base + j;
+            }
+            int cur = tc[j] & 0xF, code = b + 1;
+            tc[j] = (uint8_t)(code | (cur << 4));
+            if (code != cur) {
+                ch++;
+                if (base + j < mybad_ch) mybad_ch = base + j;
+                out.tl[g[j]] = tc[j];
+                atomicOr(&out.chg[g[j] >> 5], 1u << (g[j] & 31));
+                mark_changed_coarse(out.chgc, out.chg_shift, g[j]);
+            }
+            bool tie0 = (x - nm.o) <= (sl >> 1);
+            m[j] = (uint8_t)(tie0 ? (mm & ~M_SPEC) : (mm | M_SPEC));
+            if (meta_pref(mm) == 2 && m[j] != mm) sspec = 1;
+            x = clamp_apply(nm.f, x);
+        }
+    }
+    store8_32(out.x + base, xs);
+    store8_32(out.xalt + base, xs);
+    store8_u8(a.meta + base, m);
+    store8_u8(out.tlc + base, tc);
+    if (base + kRI > a.nc && base <= a.nc) out.x[a.nc] = xs[a.nc - base];   // padding is identity
+    for (int off = 16; off; off >>= 1) {
+        nbad += __shfl_down_sync(0xffffffffu, nbad, off);
+        ch += __shfl_down_sync(0xffffffffu, ch, off);
+    }
+    if (mybad != kInf) atomicMin(&sbad, mybad);
+    if (mybad_ch != kInf) atomicMin(&sfirst, mybad_ch);
+    if ((threadIdx.x & 31) == 0) {
+        if (nbad) atomicAdd((unsigned long long*)(out.scal + 4), (unsigned long long)nbad);
+        if (ch) atomicAdd((unsigned long long*)(out.scal + 1), (unsigned long long)ch);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && sbad != kInf) atomicMin(out.scal + 6, sbad);
+    if (threadIdx.x == 0 && sfirst != kInf) atomicMin(out.scal + 9, sfirst);
+    if (threadIdx.x == 0 && sspec) a.dnext[t] = 1;
+}
+
 __global__ void k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p, long long* tile_x,
                                  const long long* gate);
 void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_round, int incremental,
@@ -827,9 +1003,16 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
     RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc, first_round ? nullptr : b.gate,
                 b.dcur, b.dnext, incremental};
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
+    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.chgc, b.chg_shift, b.scal};
+    static const bool fused = getenv("GREM_ROUND_FUSED") != nullptr;   // measured: no gain over 3 launches
+    if (fused && b.tflag) {
+        cudaMemsetAsync(b.tflag, 0, sizeof(unsigned) * (ntiles + 1), s);   // flags + ticket (last word)
+        FusedBufs fb{b.tile_inc, b.tflag, b.tflag + ntiles};
+        k_round_fused<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, fb, o, first_round);
+        return;
+    }
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
     k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
-    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.chgc, b.chg_shift, b.scal};
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
 }
 

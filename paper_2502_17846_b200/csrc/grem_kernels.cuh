@@ -49,6 +49,8 @@ struct ChunkBufs {
     int chg_shift;
     // per scan tile
     Clamp* tile_agg;
+    Clamp* tile_inc;            // single-pass round: inclusive look-back prefixes
+    unsigned* tflag;            // single-pass round: look-back flags (+1 word: ticket)
     long long* tile_x;
     long long* tile_bad;
     // device scalars

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <exception>
 #include <mutex>
+#include <functional>
 #include <thread>
 #include <cstring>
 #include <new>
@@ -129,7 +130,8 @@ struct grem_ctx {
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
-    DBuf<Clamp> tile_agg{"tile_agg"};
+    DBuf<Clamp> tile_agg{"tile_agg"}, tile_inc{"tile_inc"};
+    DBuf<unsigned> tflag{"tflag"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
     // seed
     DBuf<int32_t> start{"start"}, cursor{"cursor"};
@@ -168,6 +170,8 @@ struct grem_ctx {
     size_t pin_bytes = 0;
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     DBuf<uint2> edges_owned;
+    bool staged_last = false;   // edges_owned holds the last call's host edge list
+    int64_t staged_m = 0;
     // count_cuts
     DBuf<unsigned long long> cc_sizes;
     DBuf<int32_t> lab32;
@@ -295,6 +299,8 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192, c->s);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
     c->tile_agg.ensure(tiles, c->s);
+    c->tile_inc.ensure(tiles, c->s);
+    c->tflag.ensure(tiles + 2, c->s);
     c->tile_x.ensure(tiles, c->s);
     c->tile_bad.ensure(tiles, c->s);
     ensure_temp(c, scan_temp_bytes(nc_cap + 1));
@@ -353,6 +359,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.chgc = c->chgc.p;
     b.chg_shift = chg_coarse_shift(c->live_n);
     b.tile_agg = c->tile_agg.p;
+    b.tile_inc = c->tile_inc.p;
+    b.tflag = c->tflag.p;
     b.tile_x = c->tile_x.p;
     b.tile_bad = c->tile_bad.p;
     b.sizes = c->d_sizes;
@@ -1064,6 +1072,8 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
     if (n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
     if (n >= (1LL << 31)) fail(GREM_E_FORMAT, "num_nodes >= 2^31 is not supported by the GPU path");
     const uint2* d;
+    c->staged_last = !(on_device || m == 0);
+    c->staged_m = m;
     if (on_device || m == 0) {
         d = reinterpret_cast<const uint2*>(edges);
     } else {
@@ -1268,6 +1278,14 @@ struct PartCtx {
     const grem_hooks* hooks;
     int32_t* final_lab;
     int shard_rank = 0;   // multi-GPU subtree sharding: this process's rank
+    // GREM_DEFER=1: the smaller sides split off the root context's chain run
+    // after that chain (concurrently with each other) instead of alongside it
+    struct Deferred {
+        grem_ctx* ch;
+        cudaEvent_t ready;
+        std::function<void()> run;
+    };
+    std::vector<Deferred> deferred;
 };
 
 // ranks [r0, r1) own this recursion node; a node with several owners is
@@ -1365,6 +1383,29 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
     bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
     bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
+    static const bool defer = getenv("GREM_DEFER") && atoi(getenv("GREM_DEFER")) > 0;
+    if (par && defer && c == c->root) {
+        cudaEvent_t ready;
+        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(ready, s));
+        int big = (e_off[1] - e_off[0]) >= (e_off[2] - e_off[1]) ? 0 : 1;
+        int sm = 1 - big;
+        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + sm * (p_level / 2)));
+        const uint2* se = side_e[sm];
+        int64_t sm_m = e_off[sm + 1] - e_off[sm], sm_n = n_off[sm + 1] - n_off[sm];
+        const int32_t* so = sub_o + n_off[sm];
+        int64_t base = leaf_base + sm * (p_level / 2), pl = p_level / 2;
+        int r0s = sr0[sm], r1s = sr1[sm], lv = level + 1;
+        PartCtx* ppc = &pc;
+        pc.deferred.push_back({ch, ready, [=]() {
+                                   CK(cudaSetDevice(ch->device));
+                                   CK(cudaStreamWaitEvent(ch->s, ready, 0));
+                                   recurse(ch, *ppc, se, sm_m, sm_n, so, pl, lv, base, r0s, r1s);
+                                   CK(cudaStreamSynchronize(ch->s));
+                               }});
+        side_call(c, big);
+        return;
+    }
     if (par) {
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -1420,6 +1461,27 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
     try {
         recurse(c, pc, d, m, n, orig, p, 0, 0, 0, shard_world);
+        if (!pc.deferred.empty()) {   // GREM_DEFER: the split-off subtrees, concurrently
+            std::vector<std::thread> ths;
+            std::vector<std::exception_ptr> errs(pc.deferred.size());
+            for (size_t i = 0; i < pc.deferred.size(); ++i)
+                ths.emplace_back([&, i] {
+                    try {
+                        pc.deferred[i].run();
+                    } catch (...) {
+                        errs[i] = std::current_exception();
+                        cudaStreamSynchronize(pc.deferred[i].ch->s);
+                    }
+                });
+            for (auto& t : ths) t.join();
+            for (auto& dfr : pc.deferred) {
+                cudaEventDestroy(dfr.ready);
+                ctx_release(c, dfr.ch);
+            }
+            pc.deferred.clear();
+            for (auto& e : errs)
+                if (e) std::rethrow_exception(e);
+        }
         if (shard_world == 1) {
             count_cuts_dev(c, d, m, fin, n, rep);
             c->stats.path_bytes += 10 * m;   // final cut pass
@@ -1593,6 +1655,13 @@ int grem_partition_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n,
         const uint2* d = stage_edges(c, edges, m, n, on_device, true);
         partition_entry(c, d, m, n, p, cfg, hooks, labels_out, rep);
     });
+}
+
+int grem_staged_edges(grem_ctx* c, const uint32_t** dev_edges, int64_t* num_edges) {
+    if (!c || !dev_edges) return GREM_E_FORMAT;
+    *dev_edges = c->staged_last ? reinterpret_cast<const uint32_t*>(c->edges_owned.p) : nullptr;
+    if (num_edges) *num_edges = c->staged_last ? c->staged_m : 0;
+    return GREM_OK;
 }
 
 int grem_partition_shard_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device, int64_t p,

@@ -107,20 +107,28 @@ def count_cuts_device(edges_ptr: int, num_edges: int, num_nodes: int, labels, p:
     return _report(int(num_nodes), rep, sizes)
 
 
-def partition_distributed(edges_ptr: int, num_edges: int, num_nodes: int, p: int, config, group=None):
+def partition_distributed(edges_ptr: int, num_edges: int, num_nodes: int, p: int, config, group=None,
+                          edges_on_device: bool = True):
     """partition() over all ranks of ``group``: returns (labels device tensor,
-    CutReport), identical on every rank."""
+    CutReport), identical on every rank.  With ``edges_on_device=False`` the
+    pointer is a (page-locked) host edge list: every rank uploads it with the
+    overlapped ingest of its level-0 bisection, and count_cuts reuses that copy."""
     import torch
     import torch.distributed as dist
 
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     labels = torch.empty(int(num_nodes), dtype=torch.int32, device="cuda")
-    partition_shard(edges_ptr, num_edges, num_nodes, p, config, rank, world, labels)
+    partition_shard(edges_ptr, num_edges, num_nodes, p, config, rank, world, labels, edges_on_device)
+    dev_ptr = int(edges_ptr)
+    if not edges_on_device:
+        staged, cnt = ctypes.c_void_p(), ctypes.c_int64()
+        _raise(_abi.lib().grem_staged_edges(context(), ctypes.byref(staged), ctypes.byref(cnt)))
+        dev_ptr = int(staged.value or 0)
     if world > 1:
         merge_labels(labels, group)
         torch.cuda.synchronize()      # NCCL stream -> library stream
-    return labels, count_cuts_device(edges_ptr, num_edges, num_nodes, labels, p)
+    return labels, count_cuts_device(dev_ptr, num_edges, num_nodes, labels, p)
 
 
 __all__ = ["owner_split", "owned_leaves", "partition_shard", "merge_labels", "count_cuts_device",
