@@ -132,6 +132,26 @@ int grem_partition_shard_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_e
                              int edges_on_device, int64_t p, const grem_config* cfg, int rank, int world,
                              int32_t* labels_out);
 
+/* write_buckets (streamcut/store.py:55-104): stable p x p scatter of the edge
+ * list by (labels[src], labels[dst]).  p = 1 + the largest label >= 0 (1 if
+ * none; < 65536) -> *p_out.  out_edges (2*num_edges u32, host or device)
+ * receives the buckets row-major, input order inside a bucket; counts_out
+ * (host, counts_cap >= p*p entries) the bucket sizes.  Errors: FormatError
+ * "unlabeled endpoint encountered" (store.py:77-78), or counts_cap too small
+ * (then *p_out is still set). */
+int grem_write_buckets_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                           int edges_on_device, const int32_t* labels, int labels_on_device, uint32_t* out_edges,
+                           int out_on_device, uint64_t* counts_out, int64_t counts_cap, int64_t* p_out);
+
+/* reorder_features (store.py:201-235): nodes grouped by label, ascending id
+ * inside a partition.  perm_out[node] = slot (int64, host); counts_out (host,
+ * counts_cap >= p) = nodes per partition; records (host, num_nodes x
+ * record_width bytes, optional) gathered into out_records in slot order.
+ * Every node must be labeled (FormatError otherwise, store.py:216-217). */
+int grem_reorder_records(grem_ctx* ctx, const int32_t* labels, int64_t num_nodes, int labels_on_device,
+                         const uint8_t* records, int64_t record_width, uint8_t* out_records, int64_t* perm_out,
+                         uint64_t* counts_out, int64_t counts_cap, int64_t* p_out);
+
 /* Device copy of the host edge list staged by the last call on this context
  * (edges_on_device = 0); valid until the next call.  Lets a sharded caller run
  * grem_count_cuts_u32 on the merged labels without a second upload.

@@ -258,6 +258,21 @@ void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t
 void launch_count_cuts_packed(const uint2* e, int64_t m, const int32_t* lab, int64_t n, int lb, uint32_t* packed,
                               unsigned long long* d_cut, int* d_neg, cudaStream_t s);
 
+// --- partitioned storage (grem_store.cu; store.py:55-104, 201-235) ---
+void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s);
+size_t bucket_sort_temp_bytes(int64_t m);
+// stable p x p bucket scatter of the edges (keys_a/keys_b: m u32 scratch);
+// counts: p*p extents; *d_bad != 0 when an endpoint is unlabeled
+void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, uint32_t p, uint32_t* keys_a,
+                          uint32_t* keys_b, uint2* out, unsigned long long* counts, int* d_bad, void* temp,
+                          size_t temp_bytes, cudaStream_t s);
+size_t order_sort_temp_bytes(int64_t n);
+// nodes grouped by label (stable): order (slot -> node), perm (node -> slot),
+// counts per label; optionally the records gathered into out
+void launch_reorder(const int32_t* lab, int64_t n, uint32_t p, uint32_t* keys_b, uint32_t* ids_a, uint32_t* order,
+                    long long* perm, unsigned long long* counts, const uint8_t* rec, int64_t width, uint8_t* out,
+                    void* temp, size_t temp_bytes, cudaStream_t s);
+
 // generic CUB helpers
 size_t scan_temp_bytes(int64_t n);
 void exclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t s);

@@ -170,6 +170,12 @@ struct grem_ctx {
     size_t pin_bytes = 0;
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     DBuf<uint2> edges_owned;
+    // partitioned storage (grem_store.cu)
+    DBuf<uint32_t> bk_keys_a{"bk_keys_a"}, bk_keys_b{"bk_keys_b"}, bk_order{"bk_order"};
+    DBuf<uint2> bk_out{"bk_out"};
+    DBuf<unsigned long long> bk_counts{"bk_counts"};
+    DBuf<long long> bk_perm{"bk_perm"};
+    DBuf<uint8_t> bk_rec{"bk_rec"}, bk_rec_out{"bk_rec_out"};
     bool staged_last = false;   // edges_owned holds the last call's host edge list
     int64_t staged_m = 0;
     // count_cuts
@@ -1654,6 +1660,104 @@ int grem_partition_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n,
             fail(GREM_E_FORMAT, "number of parts must be a power of two >= 2, got " + std::to_string(p));
         const uint2* d = stage_edges(c, edges, m, n, on_device, true);
         partition_entry(c, d, m, n, p, cfg, hooks, labels_out, rep);
+    });
+}
+
+// ------------------------------------------------ partitioned storage
+namespace {
+const int32_t* stage_labels(grem_ctx* c, const int32_t* labels, int64_t n, int on_device) {
+    if (on_device) return labels;
+    c->lab32.ensure(n > 0 ? n : 1, c->s);
+    if (n > 0) CK(cudaMemcpyAsync(c->lab32.p, labels, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->s));
+    return c->lab32.p;
+}
+int64_t label_parts(grem_ctx* c, const int32_t* lab, int64_t n, bool* any_negative = nullptr) {
+    c->cc_sizes.ensure(4, c->s);
+    int* d_max = reinterpret_cast<int*>(c->cc_sizes.p);
+    launch_label_max(lab, n, d_max, c->s);
+    CK(cudaMemcpyAsync(&c->h_pin[0], d_max, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    int mx[2];
+    memcpy(mx, &c->h_pin[0], 2 * sizeof(int));
+    if (any_negative) *any_negative = mx[1] != 0;
+    return mx[0] >= 0 ? (int64_t)mx[0] + 1 : 1;
+}
+}  // namespace
+
+int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device,
+                           const int32_t* labels, int labels_on_device, uint32_t* out_edges, int out_on_device,
+                           uint64_t* counts_out, int64_t counts_cap, int64_t* p_out) {
+    if (!c || !labels || !counts_out || (m > 0 && !out_edges)) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        cudaStream_t s = c->s;
+        const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
+        const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
+        int64_t p = label_parts(c, lab, n);   // store.py:71-72
+        if (p_out) *p_out = p;
+        if (p >= 65536) fail(GREM_E_FORMAT, "write_buckets supports fewer than 65536 partitions");
+        int64_t nb = p * p;
+        if (nb > counts_cap) fail(GREM_E_FORMAT, "counts buffer holds " + std::to_string(counts_cap) +
+                                                      " entries, p*p = " + std::to_string(nb));
+        c->bk_keys_a.ensure(m + 1, s);
+        c->bk_keys_b.ensure(m + 1, s);
+        c->bk_counts.ensure(nb, s);
+        uint2* out = out_on_device ? reinterpret_cast<uint2*>(out_edges) : nullptr;
+        if (!out) {
+            c->bk_out.ensure(m + 1, s);
+            out = c->bk_out.p;
+        }
+        ensure_temp(c, bucket_sort_temp_bytes(m));
+        int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
+        launch_write_buckets(d, m, lab, (uint32_t)p, c->bk_keys_a.p, c->bk_keys_b.p, out, c->bk_counts.p, d_bad,
+                             c->temp.p, c->temp.cap, s);
+        c->kernels += 4;
+        CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int bad;
+        memcpy(&bad, &c->h_pin[1], sizeof(int));
+        if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+        CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, s));
+        if (!out_on_device && m > 0)
+            CK(cudaMemcpyAsync(out_edges, out, sizeof(uint2) * m, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int grem_reorder_records(grem_ctx* c, const int32_t* labels, int64_t n, int labels_on_device, const uint8_t* records,
+                         int64_t record_width, uint8_t* out_records, int64_t* perm_out, uint64_t* counts_out,
+                         int64_t counts_cap, int64_t* p_out) {
+    if (!c || !labels || !perm_out || !counts_out) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        cudaStream_t s = c->s;
+        if (n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+        const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
+        bool neg = false;
+        int64_t p = label_parts(c, lab, n, &neg);
+        if (neg) fail(GREM_E_FORMAT, "all nodes must be labeled");   // store.py:216-217
+        if (p_out) *p_out = p;
+        if (p > counts_cap) fail(GREM_E_FORMAT, "counts buffer too small");
+        c->bk_keys_a.ensure(n + 1, s);
+        c->bk_keys_b.ensure(n + 1, s);
+        c->bk_order.ensure(n + 1, s);
+        c->bk_perm.ensure(n + 1, s);
+        c->bk_counts.ensure(p, s);
+        ensure_temp(c, order_sort_temp_bytes(n));
+        uint8_t* drec = nullptr;
+        uint8_t* dout = nullptr;
+        if (records && out_records && record_width > 0) {
+            c->bk_rec.ensure(n * record_width, s);
+            c->bk_rec_out.ensure(n * record_width, s);
+            drec = c->bk_rec.p;
+            dout = c->bk_rec_out.p;
+            CK(cudaMemcpyAsync(drec, records, (size_t)(n * record_width), cudaMemcpyHostToDevice, s));
+        }
+        launch_reorder(lab, n, (uint32_t)p, c->bk_keys_b.p, c->bk_keys_a.p, c->bk_order.p, c->bk_perm.p,
+                       c->bk_counts.p, drec, record_width, dout, c->temp.p, c->temp.cap, s);
+        c->kernels += 5;
+        CK(cudaMemcpyAsync(perm_out, c->bk_perm.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * p, cudaMemcpyDeviceToHost, s));
+        if (dout) CK(cudaMemcpyAsync(out_records, dout, (size_t)(n * record_width), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
     });
 }
 

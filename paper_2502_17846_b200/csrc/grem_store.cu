@@ -1,0 +1,152 @@
+// grem_store.cu — the partitioned storage layout on the GPU:
+// write_buckets (streamcut/store.py:55-104), a stable p x p scatter of the
+// edge list by (label[src], label[dst]), and the partition-grouping
+// permutation of reorder_features (store.py:201-235).
+//
+// Buckets: key = label[u] * p + label[v] per edge (one pass: edge read + two
+// label gathers), then one stable LSD radix sort of (key, edge) pairs over
+// ceil(log2 p^2) bits (stable: input order inside a bucket, store.py:92), and
+// the bucket extents by binary search of the sorted keys.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "grem_kernels.cuh"
+
+namespace grem {
+
+__global__ void k_label_max(const int32_t* __restrict__ lab, int64_t n, int* mx) {   // mx[1]: some label < 0
+    int m = -1, neg = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        m = lab[i] > m ? lab[i] : m;
+        neg |= lab[i] < 0;
+    }
+    if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) atomicOr(mx + 1, 1);
+    for (int off = 16; off; off >>= 1) {
+        int o = __shfl_down_sync(0xffffffffu, m, off);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m >= 0) atomicMax(mx, m);
+}
+
+__global__ void k_bucket_keys(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ lab, uint32_t p,
+                              uint32_t* __restrict__ keys, int* bad) {
+    int b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 ed = e[i];
+        int lu = lab[ed.x], lv = lab[ed.y];
+        if (lu < 0 || lv < 0) {   // store.py:77-78
+            b = 1;
+            keys[i] = 0;
+            continue;
+        }
+        keys[i] = (uint32_t)lu * p + (uint32_t)lv;
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// counts[b] = upper_bound(b) - lower_bound(b) in the sorted keys
+__global__ void k_bucket_counts(const uint32_t* __restrict__ skeys, int64_t m, int64_t nb,
+                                unsigned long long* __restrict__ counts) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    auto lower = [&](uint64_t key) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((uint64_t)skeys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    counts[b] = (unsigned long long)(lower((uint64_t)b + 1) - lower((uint64_t)b));
+}
+
+size_t bucket_sort_temp_bytes(int64_t m) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)m);
+    return bytes;
+}
+
+void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s) {
+    cudaMemsetAsync(d_max, 0xFF, sizeof(int), s);
+    cudaMemsetAsync(d_max + 1, 0, sizeof(int), s);
+    int grid = (int)((n + 255) / 256);
+    if (grid > num_sms() * 8) grid = num_sms() * 8;
+    if (grid < 1) grid = 1;
+    k_label_max<<<grid, 256, 0, s>>>(lab, n, d_max);
+}
+
+void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, uint32_t p, uint32_t* keys_a,
+                          uint32_t* keys_b, uint2* out, unsigned long long* counts, int* d_bad, void* temp,
+                          size_t temp_bytes, cudaStream_t s) {
+    cudaMemsetAsync(d_bad, 0, sizeof(int), s);
+    int64_t nb = (int64_t)p * p;
+    if (m > 0) {
+        int grid = (int)((m + 255) / 256);
+        if (grid > num_sms() * 16) grid = num_sms() * 16;
+        k_bucket_keys<<<grid, 256, 0, s>>>(e, m, lab, p, keys_a, d_bad);
+        int end_bit = 1;
+        while (end_bit < 32 && ((uint64_t)(nb - 1) >> end_bit) != 0) ++end_bit;
+        cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b,
+                                        reinterpret_cast<const unsigned long long*>(e),
+                                        reinterpret_cast<unsigned long long*>(out), (int)m, 0, end_bit, s);
+        k_bucket_counts<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(keys_b, m, nb, counts);
+    } else {
+        cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nb, s);
+    }
+}
+
+// reorder_features: stable order of nodes by label (ties by node id,
+// store.py:221), its inverse (node -> slot) and the per-partition extents
+__global__ void k_iota_u32n(uint32_t* a, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+__global__ void k_perm_inverse(const uint32_t* __restrict__ order, int64_t n, long long* __restrict__ perm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        perm[order[i]] = i;
+}
+__global__ void k_gather_records(const uint8_t* __restrict__ rec, const uint32_t* __restrict__ order, int64_t n,
+                                 int64_t width, uint8_t* __restrict__ out) {
+    // one warp per output record, byte-striped (records are small, arbitrary width)
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (; w < n; w += nw) {
+        const uint8_t* src = rec + (int64_t)order[w] * width;
+        uint8_t* dst = out + w * width;
+        for (int64_t k = lane; k < width; k += 32) dst[k] = src[k];
+    }
+}
+
+size_t order_sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+    return bytes;
+}
+
+void launch_reorder(const int32_t* lab, int64_t n, uint32_t p, uint32_t* keys_b, uint32_t* ids_a, uint32_t* order,
+                    long long* perm, unsigned long long* counts, const uint8_t* rec, int64_t width, uint8_t* out,
+                    void* temp, size_t temp_bytes, cudaStream_t s) {
+    int grid = (int)((n + 255) / 256);
+    if (grid > num_sms() * 16) grid = num_sms() * 16;
+    if (grid < 1) grid = 1;
+    k_iota_u32n<<<grid, 256, 0, s>>>(ids_a, n);
+    int end_bit = 1;
+    while (end_bit < 32 && ((uint64_t)p >> end_bit) != 0) ++end_bit;
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, reinterpret_cast<const uint32_t*>(lab), keys_b, ids_a, order,
+                                    (int)n, 0, end_bit, s);
+    k_perm_inverse<<<grid, 256, 0, s>>>(order, n, perm);
+    k_bucket_counts<<<(unsigned)((p + 255) / 256), 256, 0, s>>>(keys_b, n, p, counts);
+    if (rec && out && width > 0) {
+        int64_t g = (n * 32 + 255) / 256;
+        if (g > num_sms() * 16) g = num_sms() * 16;
+        k_gather_records<<<(unsigned)(g < 1 ? 1 : g), 256, 0, s>>>(rec, order, n, width, out);
+    }
+}
+
+}  // namespace grem
