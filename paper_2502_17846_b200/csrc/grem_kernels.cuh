@@ -263,9 +263,9 @@ void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s)
 size_t bucket_sort_temp_bytes(int64_t m);
 // stable p x p bucket scatter of the edges (keys_a/keys_b: m u32 scratch);
 // counts: p*p extents; *d_bad != 0 when an endpoint is unlabeled
-void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, uint32_t p, uint32_t* keys_a,
-                          uint32_t* keys_b, uint2* out, unsigned long long* counts, int* d_bad, void* temp,
-                          size_t temp_bytes, cudaStream_t s);
+void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, int64_t n, bool any_unlabeled, uint32_t p,
+                          uint32_t* keys_a, uint32_t* keys_b, uint32_t* packed, uint2* out,
+                          unsigned long long* counts, int* d_bad, void* temp, size_t temp_bytes, cudaStream_t s);
 size_t order_sort_temp_bytes(int64_t n);
 // nodes grouped by label (stable): order (slot -> node), perm (node -> slot),
 // counts per label; optionally the records gathered into out

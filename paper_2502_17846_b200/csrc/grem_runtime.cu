@@ -1692,7 +1692,8 @@ int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_
         cudaStream_t s = c->s;
         const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
         const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
-        int64_t p = label_parts(c, lab, n);   // store.py:71-72
+        bool neg = false;
+        int64_t p = label_parts(c, lab, n, &neg);   // store.py:71-72
         if (p_out) *p_out = p;
         if (p >= 65536) fail(GREM_E_FORMAT, "write_buckets supports fewer than 65536 partitions");
         int64_t nb = p * p;
@@ -1708,8 +1709,9 @@ int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_
         }
         ensure_temp(c, bucket_sort_temp_bytes(m));
         int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
-        launch_write_buckets(d, m, lab, (uint32_t)p, c->bk_keys_a.p, c->bk_keys_b.p, out, c->bk_counts.p, d_bad,
-                             c->temp.p, c->temp.cap, s);
+        c->packed_lab.ensure(n / 2 + 2, s);   // <= 16-bit packed labels (p < 65536)
+        launch_write_buckets(d, m, lab, n, neg, (uint32_t)p, c->bk_keys_a.p, c->bk_keys_b.p, c->packed_lab.p, out,
+                             c->bk_counts.p, d_bad, c->temp.p, c->temp.cap, s);
         c->kernels += 4;
         CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

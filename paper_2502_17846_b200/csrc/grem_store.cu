@@ -46,6 +46,33 @@ __global__ void k_bucket_keys(const uint2* __restrict__ e, int64_t m, const int3
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
+// all labels >= 0: labels packed to 2^lb bits (L2-resident for small p), so
+// the two gathers per edge hit L2 instead of the int32 array in HBM
+__global__ void k_pack_lab(const int32_t* __restrict__ lab, int64_t n, int lb, uint32_t* __restrict__ out,
+                           int64_t nwords) {
+    const int per = 32 >> lb, width = 1 << lb;
+    const uint32_t mask = width == 32 ? 0xFFFFFFFFu : ((1u << width) - 1);
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int j = 0; j < per; ++j) {
+            int64_t i = w * per + j;
+            if (i < n) v |= ((uint32_t)lab[i] & mask) << (j * width);
+        }
+        out[w] = v;
+    }
+}
+__global__ void k_bucket_keys_packed(const uint2* __restrict__ e, int64_t m, const uint32_t* __restrict__ pl,
+                                     int lb, uint32_t p, uint32_t* __restrict__ keys) {
+    const int lpw = 5 - lb;
+    const uint32_t mask = lb == 5 ? 0xFFFFFFFFu : ((1u << (1 << lb)) - 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 ed = __ldcs(e + i);
+        uint32_t lu = (__ldg(pl + (ed.x >> lpw)) >> ((ed.x & ((1u << lpw) - 1)) << lb)) & mask;
+        uint32_t lv = (__ldg(pl + (ed.y >> lpw)) >> ((ed.y & ((1u << lpw) - 1)) << lb)) & mask;
+        keys[i] = lu * p + lv;
+    }
+}
+
 // counts[b] = upper_bound(b) - lower_bound(b) in the sorted keys
 __global__ void k_bucket_counts(const uint32_t* __restrict__ skeys, int64_t m, int64_t nb,
                                 unsigned long long* __restrict__ counts) {
@@ -79,15 +106,25 @@ void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s)
     k_label_max<<<grid, 256, 0, s>>>(lab, n, d_max);
 }
 
-void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, uint32_t p, uint32_t* keys_a,
-                          uint32_t* keys_b, uint2* out, unsigned long long* counts, int* d_bad, void* temp,
-                          size_t temp_bytes, cudaStream_t s) {
+void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, int64_t n, bool any_unlabeled, uint32_t p,
+                          uint32_t* keys_a, uint32_t* keys_b, uint32_t* packed, uint2* out,
+                          unsigned long long* counts, int* d_bad, void* temp, size_t temp_bytes, cudaStream_t s) {
     cudaMemsetAsync(d_bad, 0, sizeof(int), s);
     int64_t nb = (int64_t)p * p;
     if (m > 0) {
         int grid = (int)((m + 255) / 256);
         if (grid > num_sms() * 16) grid = num_sms() * 16;
-        k_bucket_keys<<<grid, 256, 0, s>>>(e, m, lab, p, keys_a, d_bad);
+        if (!any_unlabeled && packed) {
+            int lb = 0;
+            while (lb < 5 && ((uint64_t)(p - 1) >> (1 << lb)) != 0) ++lb;
+            int64_t nwords = (n + (32 >> lb) - 1) / (32 >> lb);
+            int pg = (int)((nwords + 255) / 256);
+            if (pg > num_sms() * 16) pg = num_sms() * 16;
+            k_pack_lab<<<pg < 1 ? 1 : pg, 256, 0, s>>>(lab, n, lb, packed, nwords);
+            k_bucket_keys_packed<<<grid, 256, 0, s>>>(e, m, packed, lb, p, keys_a);
+        } else {
+            k_bucket_keys<<<grid, 256, 0, s>>>(e, m, lab, p, keys_a, d_bad);
+        }
         int end_bit = 1;
         while (end_bit < 32 && ((uint64_t)(nb - 1) >> end_bit) != 0) ++end_bit;
         cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b,
