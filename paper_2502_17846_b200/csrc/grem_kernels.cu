@@ -1439,7 +1439,8 @@ __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __re
 int64_t bundle_segment_len(int64_t nc) {
     // the chain costs ~140 cycles per segment (dependent smem lookups) and a
     // segment's simulation ~6 cycles per node: L ~ sqrt(24 nc) balances them
-    int64_t L = (int64_t)std::sqrt(24.0 * (double)nc);
+    static const double kb = getenv("GREM_BUNDLE_K") ? atof(getenv("GREM_BUNDLE_K")) : 24.0;
+    int64_t L = (int64_t)std::sqrt(kb * (double)nc);
     if (L < kCkpt) L = kCkpt;
     if ((nc + L - 1) / L > 4096) L = (nc + 4095) / 4096;
     return (L + kCkpt - 1) / kCkpt * kCkpt;
