@@ -1505,6 +1505,25 @@ void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
     k_commit<<<grid_for(nc, 256), 256, 0, s>>>(b.nodes, nc, b.meta, b.cntc, b.nbrc, b.nbr, b.lab, b.tlc, b.lab2);
 }
 
+// start of a round: one launch instead of five memsets -- per-round scalars
+// (changed, mis-speculated ties, first bad / first change = +large), next
+// round's dirty tiles cleared, round 1: every tile dirty
+__global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all, int64_t nt) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[1] = 0;
+        scal[4] = 0;
+        scal[6] = 0x7F7F7F7F7F7F7F7FLL;
+        scal[9] = 0x7F7F7F7F7F7F7F7FLL;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
+        dnext[i] = 0;
+        if (dcur_all) dcur_all[i] = 1;
+    }
+}
+void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, cudaStream_t s) {
+    k_round_start<<<grid_for(nt, 256), 256, 0, s>>>(b.scal, b.dnext, first_round ? b.dcur : nullptr, nt);
+}
+
 // end of a round: the next round runs only if this one changed a label;
 // scal[8] counts the rounds that actually ran
 __global__ void k_round_gate(long long* scal) {

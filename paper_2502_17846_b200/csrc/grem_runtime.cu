@@ -660,8 +660,8 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     for (int r = 1;; ++r) {
         b.dcur = dbuf[r & 1];
         b.dnext = dbuf[(r + 1) & 1];
-        CK(cudaMemsetAsync(b.dnext, 0, rtiles + 1, s));
-        if (r == 1) CK(cudaMemsetAsync(b.dcur, 1, rtiles + 1, s));
+        launch_round_start(b, rtiles + 1, r == 1, s);   // scalars, dirty tiles
+        c->kernels++;
         if (r > 1) {
             PhaseScope ps(c, PH_DELTA);
             launch_count_delta(e, mc, b, s);
@@ -669,10 +669,6 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             CK(cudaMemsetAsync(c->chgc.p, 0, kChgCoarseBits / 8, s));
             c->kernels++;
         }
-        CK(cudaMemsetAsync(c->d_scal + 1, 0, sizeof(long long), s));
-        CK(cudaMemsetAsync(c->d_scal + 4, 0, sizeof(long long), s));
-        CK(cudaMemsetAsync(c->d_scal + 6, 0x7F, sizeof(long long), s));   // first bad = +large
-        CK(cudaMemsetAsync(c->d_scal + 9, 0x7F, sizeof(long long), s));   // first changed = +large
         {
             PhaseScope ps(c, PH_SCAN);
             launch_round_scan(b, nc, a.cap, r == 1, incr_on && r >= 3, s);
