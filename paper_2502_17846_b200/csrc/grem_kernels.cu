@@ -1508,20 +1508,34 @@ void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
 // start of a round: one launch instead of five memsets -- per-round scalars
 // (changed, mis-speculated ties, first bad / first change = +large), next
 // round's dirty tiles cleared, round 1: every tile dirty
-__global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all, int64_t nt) {
+// Round r >= 2 also closes round r-1's gate (it ran iff scal[7] != 0; round r
+// runs iff round r-1 changed a label) and clears this round's changed-label
+// bitmaps (double buffered: round r writes chg[r&1], count_delta(r+1) reads it).
+__global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all, int64_t nt, int first_round,
+                              uint32_t* chg, int64_t nchg, uint32_t* chgc, int64_t nchgc) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (!first_round) {
+            if (scal[7]) scal[8] += 1;
+            scal[7] = scal[1];
+        }
         scal[1] = 0;
         scal[4] = 0;
         scal[6] = 0x7F7F7F7F7F7F7F7FLL;
         scal[9] = 0x7F7F7F7F7F7F7F7FLL;
     }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt; i += stride) {
         dnext[i] = 0;
         if (dcur_all) dcur_all[i] = 1;
     }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nchg; i += stride) chg[i] = 0u;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nchgc; i += stride) chgc[i] = 0u;
 }
-void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, cudaStream_t s) {
-    k_round_start<<<grid_for(nt, 256), 256, 0, s>>>(b.scal, b.dnext, first_round ? b.dcur : nullptr, nt);
+void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, int64_t nchg_words, cudaStream_t s) {
+    int64_t work = nt > nchg_words ? nt : nchg_words;
+    k_round_start<<<grid_for(work, 256), 256, 0, s>>>(b.scal, b.dnext, first_round ? b.dcur : nullptr, nt,
+                                                       first_round ? 1 : 0, b.chg, nchg_words, b.chgc,
+                                                       kChgCoarseBits / 32);
 }
 
 // end of a round: the next round runs only if this one changed a label;

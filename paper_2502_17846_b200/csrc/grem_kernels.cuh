@@ -132,7 +132,7 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
                        cudaStream_t s);
 void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 void launch_round_gate(const ChunkBufs& b, cudaStream_t s);
-void launch_round_start(const ChunkBufs& b, int64_t ntiles, bool first_round, cudaStream_t s);
+void launch_round_start(const ChunkBufs& b, int64_t ntiles, bool first_round, int64_t nchg_words, cudaStream_t s);
 void launch_sizes_update(const ChunkBufs& b, int64_t nc, cudaStream_t s);
 
 // --- chunk membership ---

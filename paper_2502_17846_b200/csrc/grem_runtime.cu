@@ -126,7 +126,7 @@ struct grem_ctx {
     DBuf<unsigned long long> cntc{"cntc"};
     DBuf<double2> nbrc{"nbrc"};
     DBuf<uint8_t> tlc{"tlc"};
-    DBuf<uint32_t> chg{"chg"}, chgc{"chgc"};
+    DBuf<uint32_t> chg{"chg"}, chgc{"chgc"}, chg2{"chg2"}, chgc2{"chgc2"};
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
@@ -278,6 +278,8 @@ void ensure_nodes(grem_ctx* c, int64_t n) {
     c->rank.ensure(n, c->s);
     c->chg.ensure(n / 32 + 2, c->s);
     c->chgc.ensure(kChgCoarseBits / 32, c->s);
+    c->chg2.ensure(n / 32 + 2, c->s);
+    c->chgc2.ensure(kChgCoarseBits / 32, c->s);
     c->scratch.ensure(2 * n + 2, c->s);
     c->newid.ensure(n + 1, c->s);
     ensure_temp(c, select_nodes_temp_bytes(n));
@@ -657,16 +659,22 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     c->dirty0.ensure(rtiles + 1, s);
     c->dirty1.ensure(rtiles + 1, s);
     uint8_t* dbuf[2] = {c->dirty0.p, c->dirty1.p};
+    uint32_t* chgbuf[2] = {c->chg.p, c->chg2.p};
+    uint32_t* chgcbuf[2] = {c->chgc.p, c->chgc2.p};
+    const int64_t nchg = a.n / 32 + 2;
     for (int r = 1;; ++r) {
         b.dcur = dbuf[r & 1];
         b.dnext = dbuf[(r + 1) & 1];
-        launch_round_start(b, rtiles + 1, r == 1, s);   // scalars, dirty tiles
+        b.chg = chgbuf[r & 1];     // written this round (round_down, bundle_fix)
+        b.chgc = chgcbuf[r & 1];
+        launch_round_start(b, rtiles + 1, r == 1, nchg, s);   // gate, scalars, dirty tiles, this round's bitmaps
         c->kernels++;
         if (r > 1) {
             PhaseScope ps(c, PH_DELTA);
-            launch_count_delta(e, mc, b, s);
-            CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));   // consumed
-            CK(cudaMemsetAsync(c->chgc.p, 0, kChgCoarseBits / 8, s));
+            ChunkBufs bd = b;      // the previous round's changes
+            bd.chg = chgbuf[(r - 1) & 1];
+            bd.chgc = chgcbuf[(r - 1) & 1];
+            launch_count_delta(e, mc, bd, s);
             c->kernels++;
         }
         {
@@ -688,8 +696,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
             c->kernels += 5;
         }
-        launch_round_gate(b, s);
-        c->kernels++;
+
         if (getenv("GREM_DEBUG_BUNDLE")) {
             scal_read(c, c->d_scal + 1, 9);
             fprintf(stderr, "[bundle] n %lld round %d nc %lld changed %lld first %lld nbad %lld misses(cum) %lld\n",
@@ -702,11 +709,13 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         b.xalt = c->xalt.p;
         b.xnext = c->xnext.p;
         if (r % batch == 0) {
-            scal_read(c, c->d_scal + 7, 1);
+            scal_read(c, c->d_scal + 1, 1);   // this round's changed count (the next round's gate)
             if (c->h_pin[0] == 0) break;
         }
         if (r > nc + 2 + batch) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
     }
+    launch_round_gate(b, s);   // closes the last launched round's gate
+    c->kernels++;
     scal_read(c, c->d_scal + 8, 1);
     int64_t rounds = c->h_pin[0];
     c->stats.count_bytes += 9 * mc * (rounds - 1);   // rounds >= 2: 8 B edge read + 1 B tentative-label gather
