@@ -127,6 +127,7 @@ struct grem_ctx {
     DBuf<double2> nbrc{"nbrc"};
     DBuf<uint8_t> tlc{"tlc"};
     DBuf<uint32_t> chg{"chg"}, chgc{"chgc"}, chg2{"chg2"}, chgc2{"chgc2"};
+    cudaGraphExec_t round_exec = nullptr;   // replayed pair of rounds (process_chunk)
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
@@ -662,7 +663,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     uint32_t* chgbuf[2] = {c->chg.p, c->chg2.p};
     uint32_t* chgcbuf[2] = {c->chgc.p, c->chgc2.p};
     const int64_t nchg = a.n / 32 + 2;
-    for (int r = 1;; ++r) {
+    auto issue = [&](int r) {   // one round's launches (all device-gated)
         b.dcur = dbuf[r & 1];
         b.dnext = dbuf[(r + 1) & 1];
         b.chg = chgbuf[r & 1];     // written this round (round_down, bundle_fix)
@@ -696,7 +697,6 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
             c->kernels += 5;
         }
-
         if (getenv("GREM_DEBUG_BUNDLE")) {
             scal_read(c, c->d_scal + 1, 9);
             fprintf(stderr, "[bundle] n %lld round %d nc %lld changed %lld first %lld nbad %lld misses(cum) %lld\n",
@@ -708,11 +708,52 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         std::swap(c->xalt.p, c->xnext.p);
         b.xalt = c->xalt.p;
         b.xnext = c->xnext.p;
-        if (r % batch == 0) {
-            scal_read(c, c->d_scal + 1, 1);   // this round's changed count (the next round's gate)
+    };
+    // Rounds >= 3 repeat with period 2 (double buffers), so the pair (3, 4) is
+    // captured once per chunk as a CUDA graph and replayed: one launch per two
+    // rounds instead of ~20 (the small chunks of the sparse subtrees are
+    // launch-latency bound).
+    static const bool graphs_on = !getenv("GREM_NO_GRAPH") && !getenv("GREM_DEBUG_BUNDLE");
+    const bool use_graph = graphs_on && batch == 2 && !c->profiling;
+    bool graph_ready = false;
+    long long pair_kernels = 0;
+    for (int r = 1;;) {
+        if (use_graph && r >= 3) {
+            if (!graph_ready) {
+                long long k0 = c->kernels;
+                cudaGraph_t g = nullptr;
+                CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                issue(r);
+                issue(r + 1);
+                CK(cudaStreamEndCapture(s, &g));
+                pair_kernels = c->kernels - k0;
+                c->kernels = k0;
+                bool ok = false;
+                if (c->round_exec) {
+                    cudaGraphExecUpdateResultInfo info;
+                    ok = cudaGraphExecUpdate(c->round_exec, g, &info) == cudaSuccess;
+                    if (!ok) {
+                        cudaGetLastError();
+                        cudaGraphExecDestroy(c->round_exec);
+                        c->round_exec = nullptr;
+                    }
+                }
+                if (!ok) CK(cudaGraphInstantiate(&c->round_exec, g, 0));
+                CK(cudaGraphDestroy(g));
+                graph_ready = true;
+            }
+            CK(cudaGraphLaunch(c->round_exec, s));
+            c->kernels += pair_kernels;
+            r += 2;
+        } else {
+            issue(r);
+            r += 1;
+        }
+        if ((r - 1) % batch == 0) {
+            scal_read(c, c->d_scal + 1, 1);   // the last round's changed count (the next round's gate)
             if (c->h_pin[0] == 0) break;
         }
-        if (r > nc + 2 + batch) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
+        if (r > nc + 4 + batch) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
     }
     launch_round_gate(b, s);   // closes the last launched round's gate
     c->kernels++;
@@ -1581,6 +1622,8 @@ void grem_destroy(grem_ctx* c) {
     c->pool_all.clear();
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->s);
+    if (c->round_exec) cudaGraphExecDestroy(c->round_exec);
+    c->round_exec = nullptr;
     c->lab.release();
     c->lab2.release();
     c->bin_recs.release();
