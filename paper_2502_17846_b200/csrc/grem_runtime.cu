@@ -16,6 +16,9 @@
 #include <cstdlib>
 #include <exception>
 #include <mutex>
+#include <condition_variable>
+#include <fcntl.h>
+#include <unistd.h>
 #include <functional>
 #include <thread>
 #include <cstring>
@@ -171,6 +174,19 @@ struct grem_ctx {
     size_t pin_bytes = 0;
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     DBuf<uint2> edges_owned;
+    // file ingest (load_grpe): a reader thread preads GRPE pieces into a ring
+    // of pinned slots and queues their DMA + check on copy_s; ingest marks are
+    // published under ing_mu, ing_pub = edges whose mark exists
+    static constexpr int RING = 4;
+    std::thread ing_thr;
+    std::mutex ing_mu;
+    std::condition_variable ing_cv;
+    bool ing_live = false, ing_done = false, ing_stop = false;
+    int64_t ing_pub = 0;
+    std::string ing_err;
+    void* ring[RING] = {};
+    cudaEvent_t ring_ev[RING] = {};
+    size_t ring_bytes = 0;
     // partitioned storage (grem_store.cu)
     DBuf<uint32_t> bk_keys_a{"bk_keys_a"}, bk_keys_b{"bk_keys_b"}, bk_order{"bk_order"};
     DBuf<uint2> bk_out{"bk_out"};
@@ -1083,23 +1099,48 @@ void staged_upload(grem_ctx* c, void* dst, uint64_t total, Fill fill) {
     CK(cudaStreamSynchronize(c->s));
 }
 
+// file ingest: wait for / stop the reader thread of load_grpe
+void ingest_join(grem_ctx* c) {
+    if (!c->ing_live) return;
+    c->ing_thr.join();
+    c->ing_live = false;
+}
+void ingest_reader_failed(grem_ctx* c) {
+    std::string msg;
+    {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        msg = c->ing_err;
+    }
+    if (!msg.empty()) fail(GREM_E_FORMAT, msg);
+}
+
 // make c->s wait until the ingested edges [base, end) are resident and checked
+// (file ingest: first block the host until the reader has queued that piece)
 void ingest_wait(grem_ctx* c, const uint2* end) {
-    if (c->ingest.empty() || end <= c->ingest_base || end > c->ingest_base + c->ingest_m) return;
+    if (!c->ingest_base || end <= c->ingest_base || end > c->ingest_base + c->ingest_m) return;
     int64_t idx = end - c->ingest_base;
-    for (auto& mk : c->ingest)
-        if (mk.end >= idx) {
-            CK(cudaStreamWaitEvent(c->s, mk.ev, 0));
-            return;
-        }
+    {
+        std::unique_lock<std::mutex> lk(c->ing_mu);
+        if (c->ing_live) c->ing_cv.wait(lk, [&] { return c->ing_pub >= idx || c->ing_done; });
+        for (auto& mk : c->ingest)
+            if (mk.end >= idx) {
+                CK(cudaStreamWaitEvent(c->s, mk.ev, 0));
+                return;
+            }
+    }
+    ingest_reader_failed(c);
+    fail(GREM_E_FORMAT, "ingest: edges not staged");
 }
 void ingest_wait_all(grem_ctx* c) {
+    if (!c->ingest_base) return;
+    ingest_join(c);
+    ingest_reader_failed(c);
     if (!c->ingest.empty()) CK(cudaStreamWaitEvent(c->s, c->ingest.back().ev, 0));
 }
 // end of a call: every piece consumed; raise the reference's FormatError if an
 // endpoint was out of range (edgefile.py:63-65)
 void ingest_finish(grem_ctx* c) {
-    if (c->ingest.empty()) return;
+    if (!c->ingest_base) return;
     ingest_wait_all(c);
     uint32_t bad = 0;
     CK(cudaMemcpyAsync(&c->h_pin[0], c->d_bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->s));
@@ -1113,10 +1154,31 @@ void ingest_finish(grem_ctx* c) {
         fail(GREM_E_FORMAT, "edge endpoint " + std::to_string((int64_t)bad - 1) + " >= num_nodes " + std::to_string(n));
 }
 void ingest_abort(grem_ctx* c) {
+    {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        c->ing_stop = true;
+    }
+    ingest_join(c);
     if (c->copy_s) cudaStreamSynchronize(c->copy_s);
     for (auto& mk : c->ingest) cudaEventDestroy(mk.ev);
     c->ingest.clear();
     c->ingest_base = nullptr;
+}
+
+// copy stream + bad-id flag for an overlapped ingest into dst (ordered after
+// the buffer's stream-ordered allocation on c->s)
+void ingest_begin(grem_ctx* c, const uint2* dst, int64_t m, int64_t n) {
+    if (!c->copy_s) CK(cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking));
+    if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(uint32_t)));
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CK(cudaEventRecord(ready, c->s));
+    CK(cudaStreamWaitEvent(c->copy_s, ready, 0));
+    cudaEventDestroy(ready);
+    CK(cudaMemsetAsync(c->d_bad, 0, sizeof(uint32_t), c->copy_s));
+    c->ingest_base = dst;
+    c->ingest_m = m;
+    c->ingest_n = n;
 }
 
 const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int on_device,
@@ -1134,16 +1196,9 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
         bool pinned = cudaPointerGetAttributes(&at, edges) == cudaSuccess && at.type == cudaMemoryTypeHost;
         cudaGetLastError();
         if (pinned && overlap) {   // page-locked source: DMA pieces overlapped with the first bisection
-            if (!c->copy_s) CK(cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking));
-            if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(uint32_t)));
-            cudaEvent_t ready;
-            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-            CK(cudaEventRecord(ready, c->s));   // the buffer's stream-ordered allocation
-            CK(cudaStreamWaitEvent(c->copy_s, ready, 0));
-            cudaEventDestroy(ready);
-            CK(cudaMemsetAsync(c->d_bad, 0, sizeof(uint32_t), c->copy_s));
-            const int64_t piece = 1LL << 24;   // 128 MB of edges per DMA
             uint2* dst = c->edges_owned.p;
+            ingest_begin(c, dst, m, n);
+            const int64_t piece = 1LL << 24;   // 128 MB of edges per DMA
             for (int64_t off = 0; off < m; off += piece) {
                 int64_t cnt = m - off < piece ? m - off : piece;
                 CK(cudaMemcpyAsync(dst + off, edges + 2 * off, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->copy_s));
@@ -1153,9 +1208,6 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
                 CK(cudaEventRecord(ev, c->copy_s));
                 c->ingest.push_back({off + cnt, ev});
             }
-            c->ingest_base = dst;
-            c->ingest_m = m;
-            c->ingest_n = n;
             return dst;
         } else if (pinned) {   // page-locked source: DMA straight into HBM
             PhaseScope ps(c, PH_INGEST);
@@ -1211,21 +1263,123 @@ GrpeHeader read_grpe_header(const char* path) {
     return GrpeHeader{(int64_t)n, (int64_t)m};
 }
 
+// GRPE u32 file -> HBM (edgefile.py:107-126,186-219), overlapped with the
+// path: a reader thread preads 128 MB pieces with GREM_INGEST_THREADS threads
+// into a ring of pinned slots, queues each piece's DMA and id check on copy_s
+// and publishes its mark; the bisection waits only for the pieces covering the
+// chunk it is about to read (ingest_wait), so reading the file overlaps the
+// first chunks' work.  Bad ids raise the reference's FormatError at the end.
+void ensure_ring(grem_ctx* c) {
+    const size_t bytes = 128ull << 20;
+    if (c->ring_bytes == bytes) return;
+    for (int i = 0; i < grem_ctx::RING; ++i) {
+        CK(cudaHostAlloc(&c->ring[i], bytes, cudaHostAllocDefault));
+        CK(cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming));
+    }
+    c->ring_bytes = bytes;
+}
+
+void ingest_reader(grem_ctx* c, std::string path, uint2* dst, int64_t m, uint32_t n) {
+    int fd = -1;
+    try {
+        CK(cudaSetDevice(c->device));
+        fd = open(path.c_str(), O_RDONLY);
+        if (fd < 0) fail(GREM_E_FORMAT, path + ": cannot open");
+        static const int threads = [] {
+            const char* v = getenv("GREM_INGEST_THREADS");
+            int hw = (int)std::thread::hardware_concurrency();
+            int t = v ? atoi(v) : (hw < 16 ? hw : 16);
+            return t < 1 ? 1 : t;
+        }();
+        int64_t piece = (int64_t)(c->ring_bytes / 8);
+        if (const char* v = getenv("GREM_INGEST_PIECE")) {   // test knob: piece size in edges
+            int64_t pv = atoll(v);
+            if (pv > 0 && pv < piece) piece = pv;
+        }
+        for (int64_t off = 0, i = 0; off < m; off += piece, ++i) {
+            {
+                std::lock_guard<std::mutex> lk(c->ing_mu);
+                if (c->ing_stop) break;
+            }
+            int64_t cnt = m - off < piece ? m - off : piece;
+            int slot = (int)(i % grem_ctx::RING);
+            if (i >= grem_ctx::RING) CK(cudaEventSynchronize(c->ring_ev[slot]));   // slot's previous DMA done
+            char* buf = (char*)c->ring[slot];
+            const size_t bytes = (size_t)cnt * 8;
+            const off_t base = 28 + (off_t)off * 8;
+            size_t part = (bytes + threads - 1) / threads;
+            part = (part + 4095) & ~(size_t)4095;
+            std::vector<std::thread> ws;
+            std::vector<char> ok(threads, 1);
+            for (int t = 0; t < threads; ++t) {
+                size_t lo = (size_t)t * part;
+                if (lo >= bytes) break;
+                size_t hi = lo + part < bytes ? lo + part : bytes;
+                ws.emplace_back([=, &ok] {
+                    size_t done = lo;
+                    while (done < hi) {
+                        ssize_t r = pread(fd, buf + done, hi - done, base + (off_t)done);
+                        if (r <= 0) {
+                            ok[t] = 0;
+                            return;
+                        }
+                        done += (size_t)r;
+                    }
+                });
+            }
+            for (auto& w : ws) w.join();
+            for (char o : ok)
+                if (!o) fail(GREM_E_FORMAT, path + ": truncated payload");
+            CK(cudaMemcpyAsync(dst + off, buf, bytes, cudaMemcpyHostToDevice, c->copy_s));
+            CK(cudaEventRecord(c->ring_ev[slot], c->copy_s));
+            launch_check_piece(dst + off, cnt, n, c->d_bad, c->copy_s);
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, c->copy_s));
+            {
+                std::lock_guard<std::mutex> lk(c->ing_mu);
+                c->ingest.push_back({off + cnt, ev});
+                c->ing_pub = off + cnt;
+            }
+            c->ing_cv.notify_all();
+        }
+    } catch (const GremError& e) {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        c->ing_err = e.msg;
+    } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        c->ing_err = e.what();
+    }
+    if (fd >= 0) close(fd);
+    {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        c->ing_done = true;
+    }
+    c->ing_cv.notify_all();
+}
+
 const uint2* load_grpe(grem_ctx* c, const char* path, GrpeHeader* hd) {
     *hd = read_grpe_header(path);
-    int64_t m = hd->m;
+    int64_t m = hd->m, n = hd->n;
+    c->staged_last = false;
+    c->staged_m = m;
+    if (n < 1) fail(GREM_E_FORMAT, "num_nodes must be >= 1");
+    if (n >= (1LL << 31)) fail(GREM_E_FORMAT, "num_nodes >= 2^31 is not supported by the GPU path");
     if (m == 0) return nullptr;
     c->edges_owned.ensure(m, c->s);
-    FILE* f = fopen(path, "rb");
-    if (!f) fail(GREM_E_FORMAT, std::string(path) + ": cannot open");
-    fseek(f, 28, SEEK_SET);
-    bool ok = true;
-    staged_upload(c, c->edges_owned.p, (uint64_t)m * 8, [&](void* buf, uint64_t, size_t len) {
-        if (fread(buf, 1, len, f) != len) ok = false;
-    });
-    fclose(f);
-    if (!ok) fail(GREM_E_FORMAT, std::string(path) + ": truncated payload");
-    return stage_edges(c, reinterpret_cast<const uint32_t*>(c->edges_owned.p), m, hd->n, 1);
+    ensure_ring(c);
+    uint2* dst = c->edges_owned.p;
+    ingest_begin(c, dst, m, n);
+    {
+        std::lock_guard<std::mutex> lk(c->ing_mu);
+        c->ing_pub = 0;
+        c->ing_done = false;
+        c->ing_stop = false;
+        c->ing_err.clear();
+    }
+    c->ing_live = true;
+    c->ing_thr = std::thread(ingest_reader, c, std::string(path), dst, m, (uint32_t)n);
+    return dst;
 }
 
 void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_config* cfg, int64_t capacity,
@@ -1654,6 +1808,10 @@ void grem_destroy(grem_ctx* c) {
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
+    }
+    for (int i = 0; i < grem_ctx::RING; ++i) {
+        if (c->ring[i]) cudaFreeHost(c->ring[i]);
+        if (c->ring_ev[i]) cudaEventDestroy(c->ring_ev[i]);
     }
     if (c->d_sizes) cudaFree(c->d_sizes);
     if (c->d_scal) cudaFree(c->d_scal);

@@ -351,3 +351,33 @@ print("variant ok")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, **env), capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_file_ingest_pieces(tmp_path, golden_dir, monkeypatch):
+    """GRPE file front end (grem_partition_file / grem_bisect_file): the reader
+    thread streams the file in pieces through the pinned ring (forced small
+    here so the ring wraps ~100 times) overlapped with the path; labels equal
+    the reference's (golden tiny_k4) and the in-memory entry point; an
+    out-of-range id in a late piece raises FormatError and the context stays
+    usable."""
+    monkeypatch.setenv("GREM_INGEST_PIECE", "997")
+    gs = json.load(open(os.path.join(golden_dir, "golden_shapes.json")))["tiny_k4"]
+    s = synth.SHAPES[gs["shape"]]
+    e = synth.shape_edges(s)
+    f = open_edge_file(write_grpe(tmp_path / "t.grpe", e, s.num_nodes))
+    cfg = GremConfig(chunk_frac=gs["chunk_frac"])
+    lab, rep = partition(f, gs["k"], cfg, str(tmp_path / "w"))
+    assert np.array_equal(lab, np.load(os.path.join(golden_dir, "golden_tiny_k4.npy")))
+    assert rep.cut_edges == gs["cut_edges"]
+    b, brep = bisect(f, GremConfig(chunk_frac=0.01))
+    b2, brep2 = grem.bisect_edges(e, s.num_nodes, GremConfig(chunk_frac=0.01))
+    assert np.array_equal(b, b2) and brep == brep2
+    bad = e.copy()
+    bad[len(bad) - 5] = (0, s.num_nodes + 3)
+    fb = open_edge_file(write_grpe(tmp_path / "bad.grpe", bad, s.num_nodes))
+    for fn in (lambda: bisect(fb, GremConfig(chunk_frac=0.1)),
+               lambda: partition(fb, 4, GremConfig(chunk_frac=0.1), str(tmp_path / "w2"))):
+        with pytest.raises(FormatError):
+            fn()
+    lab3, _ = partition(f, gs["k"], cfg, str(tmp_path / "w3"))
+    assert np.array_equal(lab3, lab)
