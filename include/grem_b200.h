@@ -152,6 +152,16 @@ int grem_reorder_records(grem_ctx* ctx, const int32_t* labels, int64_t num_nodes
                          const uint8_t* records, int64_t record_width, uint8_t* out_records, int64_t* perm_out,
                          uint64_t* counts_out, int64_t counts_cap, int64_t* p_out);
 
+/* compute_node_stats (streamcut/theory.py:97-122): per node, k = non-self-loop
+ * neighbour endpoints (with multiplicity) and k0 = those on its majority side
+ * of the bisection `labels`.  k_out / k0_out: num_nodes int64 (host or
+ * device).  Errors: FormatError "reference labels are not a bisection" (a
+ * label > 1, theory.py:107-108), "unlabeled endpoint encountered"
+ * (theory.py:114-115). */
+int grem_node_stats_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                        int edges_on_device, const int32_t* labels, int labels_on_device, int64_t* k_out,
+                        int64_t* k0_out);
+
 /* Device copy of the host edge list staged by the last call on this context
  * (edges_on_device = 0); valid until the next call.  Lets a sharded caller run
  * grem_count_cuts_u32 on the merged labels without a second upload.

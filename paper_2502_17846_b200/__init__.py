@@ -12,6 +12,7 @@ existing callers (CLI, tests) use the GPU path unchanged.
 
 from .config import ChunkPlan, CutReport, GremConfig, SeedConfig, default_capacity
 from .errors import CapacityError, DeviceError, FormatError, StreamcutError
+from .theory import compute_node_stats, node_stats_edges
 from .grem import bisect, bisect_edges, count_cuts, last_stats, partition, partition_edges, set_device
 
 __version__ = "0.1.0"
@@ -29,6 +30,13 @@ def install_into_streamcut():
         mod.bisect = bisect
         mod.partition = partition
         mod.count_cuts = count_cuts
+    streamcut.compute_node_stats = compute_node_stats
+    try:
+        import streamcut.theory as st  # type: ignore
+
+        st.compute_node_stats = compute_node_stats
+    except Exception:  # noqa: BLE001
+        pass
     try:
         import streamcut.cli as cli  # type: ignore
 
@@ -43,4 +51,5 @@ __all__ = [
     "bisect", "partition", "count_cuts", "bisect_edges", "partition_edges", "set_device", "last_stats",
     "GremConfig", "SeedConfig", "ChunkPlan", "CutReport", "default_capacity",
     "StreamcutError", "FormatError", "CapacityError", "DeviceError", "install_into_streamcut",
+    "compute_node_stats", "node_stats_edges",
 ]

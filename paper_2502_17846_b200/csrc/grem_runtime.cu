@@ -191,6 +191,8 @@ struct grem_ctx {
     DBuf<uint32_t> bk_keys_a{"bk_keys_a"}, bk_keys_b{"bk_keys_b"}, bk_order{"bk_order"};
     DBuf<uint2> bk_out{"bk_out"};
     DBuf<unsigned long long> bk_counts{"bk_counts"};
+    DBuf<unsigned long long> ns_cnt{"ns_cnt"};   // node stats (theory)
+    DBuf<int64_t> ns_k{"ns_k"}, ns_k0{"ns_k0"};
     DBuf<long long> bk_perm{"bk_perm"};
     DBuf<uint8_t> bk_rec{"bk_rec"}, bk_rec_out{"bk_rec_out"};
     bool staged_last = false;   // edges_owned holds the last call's host edge list
@@ -1805,6 +1807,8 @@ void grem_destroy(grem_ctx* c) {
     }
     c->part_fin.release();
     c->part_orig.release();
+    c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
+    c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release();
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -1927,6 +1931,31 @@ int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_
         CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, s));
         if (!out_on_device && m > 0)
             CK(cudaMemcpyAsync(out_edges, out, sizeof(uint2) * m, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int grem_node_stats_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device,
+                        const int32_t* labels, int labels_on_device, int64_t* k_out, int64_t* k0_out) {
+    if (!c || !labels || !k_out || !k0_out) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        cudaStream_t s = c->s;
+        const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
+        const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
+        if (label_parts(c, lab, n) > 2) fail(GREM_E_FORMAT, "reference labels are not a bisection");   // theory.py:107-108
+        c->ns_cnt.ensure(2 * n + 2, s);
+        c->ns_k.ensure(n + 1, s);
+        c->ns_k0.ensure(n + 1, s);
+        int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
+        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_k.p, c->ns_k0.p, d_bad, s);
+        c->kernels += 2;
+        CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int bad;
+        memcpy(&bad, &c->h_pin[1], sizeof(int));
+        if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+        CK(cudaMemcpyAsync(k_out, c->ns_k.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+        CK(cudaMemcpyAsync(k0_out, c->ns_k0.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
         CK(cudaStreamSynchronize(s));
     });
 }

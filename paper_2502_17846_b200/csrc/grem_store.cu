@@ -97,6 +97,49 @@ size_t bucket_sort_temp_bytes(int64_t m) {
     return bytes;
 }
 
+// compute_node_stats (streamcut/theory.py:97-122): per node, the non-self-loop
+// neighbour endpoints on side 0 / side 1 of a bisection, with multiplicity.
+// One pass over the edges: two label gathers and two 64-bit REDs per edge
+// into the node's (side 0, side 1) counter pair; then k = c0 + c1, k0 = max.
+__global__ void k_node_side_counts(const uint2* __restrict__ e, int64_t m, const int32_t* __restrict__ lab,
+                                   unsigned long long* __restrict__ cnt, int* bad) {
+    int b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 ed = __ldcs(e + i);
+        if (ed.x == ed.y) continue;   // theory.py:111
+        int lu = __ldg(lab + ed.x), lv = __ldg(lab + ed.y);
+        if (lu < 0 || lv < 0) {       // theory.py:114-115
+            b = 1;
+            continue;
+        }
+        atomicAdd(cnt + 2 * (uint64_t)ed.x + lv, 1ull);
+        atomicAdd(cnt + 2 * (uint64_t)ed.y + lu, 1ull);
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+__global__ void k_node_stats_final(const ulonglong2* __restrict__ cnt, int64_t n, int64_t* __restrict__ k,
+                                   int64_t* __restrict__ k0) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        ulonglong2 c = cnt[i];
+        k[i] = (int64_t)(c.x + c.y);
+        k0[i] = (int64_t)(c.x > c.y ? c.x : c.y);
+    }
+}
+
+void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* cnt,
+                       int64_t* k, int64_t* k0, int* bad, cudaStream_t s) {
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * n, s);
+    cudaMemsetAsync(bad, 0, sizeof(int), s);
+    int cap = num_sms() * 8;
+    int grid = (int)((m + 255) / 256);
+    grid = grid > cap ? cap : (grid < 1 ? 1 : grid);
+    if (m > 0) k_node_side_counts<<<grid, 256, 0, s>>>(e, m, lab, cnt, bad);
+    grid = (int)((n + 255) / 256);
+    grid = grid > cap ? cap : (grid < 1 ? 1 : grid);
+    k_node_stats_final<<<grid, 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(cnt), n, k, k0);
+}
+
 void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s) {
     cudaMemsetAsync(d_max, 0xFF, sizeof(int), s);
     cudaMemsetAsync(d_max + 1, 0, sizeof(int), s);
