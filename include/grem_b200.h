@@ -181,6 +181,11 @@ int grem_bisect_file(grem_ctx* ctx, const char* path, const grem_config* cfg, in
                      const grem_hooks* hooks, int32_t* labels_out, grem_report* rep);
 int grem_partition_file(grem_ctx* ctx, const char* path, int64_t p, const grem_config* cfg,
                         const grem_hooks* hooks, int32_t* labels_out, grem_report* rep);
+/* count_cuts (grem.py:227-252) of a GRPE u32 file: the payload streams in
+ * through the same overlapped reader; labels (num_nodes int32, host or
+ * device) must match the header's num_nodes. */
+int grem_count_cuts_file(grem_ctx* ctx, const char* path, const int32_t* labels, int labels_on_device,
+                         grem_report* rep);
 
 /* During an on_chunk hook: D2H copy of the live parts (int32, -1 unassigned). */
 int grem_state_parts(grem_ctx* ctx, int32_t* out, int64_t n);

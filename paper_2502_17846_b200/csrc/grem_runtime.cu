@@ -2031,6 +2031,17 @@ int grem_count_cuts_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n
     });
 }
 
+int grem_count_cuts_file(grem_ctx* c, const char* path, const int32_t* labels, int labels_on_device,
+                         grem_report* rep) {
+    if (!c || !path || !labels) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        GrpeHeader hd;
+        const uint2* d = load_grpe(c, path, &hd);
+        const int32_t* dl = stage_labels(c, labels, hd.n, labels_on_device);
+        count_cuts_dev(c, d, hd.m, dl, hd.n, rep);
+    });
+}
+
 int grem_bisect_file(grem_ctx* c, const char* path, const grem_config* cfg, int64_t capacity,
                      const grem_hooks* hooks, int32_t* labels_out, grem_report* rep) {
     if (!c || !cfg || !path) return GREM_E_FORMAT;

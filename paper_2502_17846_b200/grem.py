@@ -249,11 +249,15 @@ def count_cuts(efile, labels):
     if labels.shape[0] != n:
         raise FormatError(f"labels cover {labels.shape[0]} nodes, file has {n}")
     lab = np.ascontiguousarray(labels.astype(np.int32))
-    e = edges_u32(efile)
     cap = max(2, int(lab.max()) + 1 if lab.size else 2)
     rep, sizes = _report_struct(cap)
-    rc = _abi.lib().grem_count_cuts_u32(context(), e.ctypes.data, e.shape[0], n, 0, lab.ctypes.data, 0,
-                                        ctypes.byref(rep))
+    if is_native_binary(efile):
+        rc = _abi.lib().grem_count_cuts_file(context(), os.fsencode(efile.path), lab.ctypes.data, 0,
+                                             ctypes.byref(rep))
+    else:
+        e = edges_u32(efile)
+        rc = _abi.lib().grem_count_cuts_u32(context(), e.ctypes.data, e.shape[0], n, 0, lab.ctypes.data, 0,
+                                            ctypes.byref(rep))
     _raise(rc)
     return _report(n, rep, sizes)
 

@@ -376,8 +376,10 @@ def test_file_ingest_pieces(tmp_path, golden_dir, monkeypatch):
     bad[len(bad) - 5] = (0, s.num_nodes + 3)
     fb = open_edge_file(write_grpe(tmp_path / "bad.grpe", bad, s.num_nodes))
     for fn in (lambda: bisect(fb, GremConfig(chunk_frac=0.1)),
-               lambda: partition(fb, 4, GremConfig(chunk_frac=0.1), str(tmp_path / "w2"))):
+               lambda: partition(fb, 4, GremConfig(chunk_frac=0.1), str(tmp_path / "w2")),
+               lambda: count_cuts(fb, lab)):
         with pytest.raises(FormatError):
             fn()
     lab3, _ = partition(f, gs["k"], cfg, str(tmp_path / "w3"))
     assert np.array_equal(lab3, lab)
+    assert count_cuts(f, lab) == rep   # grem_count_cuts_file
