@@ -1170,7 +1170,12 @@ void ingest_abort(grem_ctx* c) {
 // copy stream + bad-id flag for an overlapped ingest into dst (ordered after
 // the buffer's stream-ordered allocation on c->s)
 void ingest_begin(grem_ctx* c, const uint2* dst, int64_t m, int64_t n) {
-    if (!c->copy_s) CK(cudaStreamCreateWithFlags(&c->copy_s, cudaStreamNonBlocking));
+    if (!c->copy_s) {   // highest priority: the per-piece id checks must not queue behind SM-filling round kernels
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        static const bool low = getenv("GREM_COPY_PRIO_LOW") != nullptr;   // A/B switch
+        CK(cudaStreamCreateWithPriority(&c->copy_s, cudaStreamNonBlocking, low ? lo : hi));
+    }
     if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(uint32_t)));
     cudaEvent_t ready;
     CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
