@@ -193,6 +193,7 @@ struct grem_ctx {
     DBuf<unsigned long long> bk_counts{"bk_counts"};
     DBuf<unsigned long long> ns_cnt{"ns_cnt"};   // node stats (theory)
     DBuf<int64_t> ns_k{"ns_k"}, ns_k0{"ns_k0"};
+    DBuf<uint32_t> ns_pack{"ns_pack"};
     DBuf<long long> bk_perm{"bk_perm"};
     DBuf<uint8_t> bk_rec{"bk_rec"}, bk_rec_out{"bk_rec_out"};
     bool staged_last = false;   // edges_owned holds the last call's host edge list
@@ -1813,7 +1814,7 @@ void grem_destroy(grem_ctx* c) {
     c->part_fin.release();
     c->part_orig.release();
     c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
-    c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release();
+    c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release(); c->ns_pack.release();
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -1952,8 +1953,9 @@ int grem_node_stats_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n
         c->ns_k.ensure(n + 1, s);
         c->ns_k0.ensure(n + 1, s);
         int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
-        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_k.p, c->ns_k0.p, d_bad, s);
-        c->kernels += 2;
+        c->ns_pack.ensure(n / 16 + 2, s);
+        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_pack.p, c->ns_k.p, c->ns_k0.p, d_bad, s);
+        c->kernels += 3;
         CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         int bad;

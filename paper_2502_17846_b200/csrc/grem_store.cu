@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "grem_kernels.cuh"
 
@@ -118,6 +119,57 @@ __global__ void k_node_side_counts(const uint2* __restrict__ e, int64_t m, const
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
+// Packed form for m < 2^32 (a node's per-side count is <= m): labels as 2-bit
+// codes (0, 1, 2 = unlabeled; n/4 bytes, L2-resident) and ONE u64 counter per
+// node holding side 0 in the low and side 1 in the high 32 bits, so each
+// endpoint is one RED into an 8-byte word (half the counter footprint).
+__global__ void k_pack_labels2(const int32_t* __restrict__ lab, int64_t n, uint32_t* __restrict__ packed) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (n + 15) / 16;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t word = 0;
+        int64_t base = w * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            int64_t i = base + j;
+            uint32_t code = 2;
+            if (i < n) {
+                int l = __ldcs(lab + i);
+                code = l < 0 ? 2u : (uint32_t)(l & 1);
+            }
+            word |= code << (2 * j);
+        }
+        packed[w] = word;
+    }
+}
+
+__global__ void k_node_side_counts_packed(const uint2* __restrict__ e, int64_t m, const uint32_t* __restrict__ packed,
+                                          unsigned long long* __restrict__ cnt, int* bad) {
+    int b = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 ed = __ldcs(e + i);
+        if (ed.x == ed.y) continue;   // theory.py:111
+        uint32_t lu = (__ldg(packed + (ed.x >> 4)) >> (2 * (ed.x & 15))) & 3u;
+        uint32_t lv = (__ldg(packed + (ed.y >> 4)) >> (2 * (ed.y & 15))) & 3u;
+        if ((lu | lv) & 2u) {         // theory.py:114-115
+            b = 1;
+            continue;
+        }
+        atomicAdd(cnt + ed.x, 1ull << (32 * lv));
+        atomicAdd(cnt + ed.y, 1ull << (32 * lu));
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+__global__ void k_node_stats_final_packed(const unsigned long long* __restrict__ cnt, int64_t n,
+                                          int64_t* __restrict__ k, int64_t* __restrict__ k0) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long c = cnt[i];
+        int64_t c0 = (int64_t)(c & 0xffffffffull), c1 = (int64_t)(c >> 32);
+        k[i] = c0 + c1;
+        k0[i] = c0 > c1 ? c0 : c1;
+    }
+}
+
 __global__ void k_node_stats_final(const ulonglong2* __restrict__ cnt, int64_t n, int64_t* __restrict__ k,
                                    int64_t* __restrict__ k0) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -127,17 +179,26 @@ __global__ void k_node_stats_final(const ulonglong2* __restrict__ cnt, int64_t n
     }
 }
 
+// cnt: 2n u64 (the unpacked fallback needs all of it); packed: n/16 + 1 u32
 void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* cnt,
-                       int64_t* k, int64_t* k0, int* bad, cudaStream_t s) {
-    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * n, s);
+                       uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s) {
     cudaMemsetAsync(bad, 0, sizeof(int), s);
     int cap = num_sms() * 8;
-    int grid = (int)((m + 255) / 256);
-    grid = grid > cap ? cap : (grid < 1 ? 1 : grid);
-    if (m > 0) k_node_side_counts<<<grid, 256, 0, s>>>(e, m, lab, cnt, bad);
-    grid = (int)((n + 255) / 256);
-    grid = grid > cap ? cap : (grid < 1 ? 1 : grid);
-    k_node_stats_final<<<grid, 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(cnt), n, k, k0);
+    auto grid_for = [&](int64_t work) {
+        int64_t g = (work + 255) / 256;
+        return (int)(g > cap ? cap : (g < 1 ? 1 : g));
+    };
+    static const bool unpacked = getenv("GREM_NODE_STATS_UNPACKED") != nullptr;   // A/B switch
+    if (m < (1LL << 32) && !unpacked) {
+        cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * n, s);
+        k_pack_labels2<<<grid_for((n + 15) / 16), 256, 0, s>>>(lab, n, packed);
+        if (m > 0) k_node_side_counts_packed<<<grid_for(m), 256, 0, s>>>(e, m, packed, cnt, bad);
+        k_node_stats_final_packed<<<grid_for(n), 256, 0, s>>>(cnt, n, k, k0);
+        return;
+    }
+    cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 2 * n, s);
+    if (m > 0) k_node_side_counts<<<grid_for(m), 256, 0, s>>>(e, m, lab, cnt, bad);
+    k_node_stats_final<<<grid_for(n), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(cnt), n, k, k0);
 }
 
 void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s) {

@@ -104,3 +104,28 @@ def test_gpu_random_and_large_vs_oracle():
     st = node_stats_edges(edges, n, lab)
     k, k0 = theory_oracle.node_stats(edges, n, lab)
     assert np.array_equal(st.k, k) and np.array_equal(st.k0, k0)
+
+
+@pytest.mark.gpu
+def test_gpu_unpacked_fallback_matches():
+    """The two-counter form (used when num_edges >= 2^32) gives the same stats:
+    forced with GREM_NODE_STATS_UNPACKED in a subprocess (the switch is read once)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import numpy as np\n"
+            "from helpers import random_multigraph\n"
+            "from oracle import theory_oracle\n"
+            "from paper_2502_17846_b200 import node_stats_edges\n"
+            "rng = np.random.default_rng(21)\n"
+            "for _ in range(10):\n"
+            "    e, n = random_multigraph(rng, max_nodes=300, max_edges=4000)\n"
+            "    lab = rng.integers(0, 2, size=n)\n"
+            "    st = node_stats_edges(e, n, lab)\n"
+            "    k, k0 = theory_oracle.node_stats(e, n, lab)\n"
+            "    assert np.array_equal(st.k, k) and np.array_equal(st.k0, k0)\n"
+            "print('ok')\n") % (root, os.path.join(root, "tests"))
+    env = dict(os.environ, GREM_NODE_STATS_UNPACKED="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
