@@ -2449,6 +2449,54 @@ __global__ void k_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max
     }
     if (any) atomicMax(bad_max, v + 1);   // 0 = no bad endpoint
 }
+// compute_node_stats (theory.py:97-122), hub-privatised form of the packed
+// count (grem_store.cu): the bisection's hub table (detect_hubs) is loaded
+// into shared memory and endpoints that are hubs accumulate in per-CTA
+// shared counters (flushed once per CTA), so the top nodes' millions of
+// endpoints stop serialising on single L2 addresses; the rest are REDs into
+// one u64 per node (side 0 low / side 1 high half).
+__global__ void __launch_bounds__(512) k_node_side_counts_hub(const uint2* __restrict__ e, int64_t m,
+                                                              const uint32_t* __restrict__ packed,
+                                                              const uint32_t* __restrict__ hub_keys,
+                                                              unsigned long long* __restrict__ cnt, int* bad) {
+    __shared__ __align__(16) uint32_t s_keys[kHubSlots];
+    __shared__ unsigned long long s_cnt[kHubSlots];
+    hub_load(s_keys, hub_keys);
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = 0;
+    __syncthreads();
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    int b = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        uint2 ed = __ldcs(e + i);
+        if (ed.x == ed.y) continue;   // theory.py:111
+        uint32_t lu = (__ldg(packed + (ed.x >> 4)) >> (2 * (ed.x & 15))) & 3u;
+        uint32_t lv = (__ldg(packed + (ed.y >> 4)) >> (2 * (ed.y & 15))) & 3u;
+        if ((lu | lv) & 2u) {         // theory.py:114-115
+            b = 1;
+            continue;
+        }
+        unsigned long long iu = 1ull << (32 * lv), iv = 1ull << (32 * lu);
+        int hu = hub_find(s_keys, ed.x), hv = hub_find(s_keys, ed.y);
+        if (hu >= 0) atomicAdd(s_cnt + hu, iu);
+        else atomicAdd(cnt + ed.x, iu);
+        if (hv >= 0) atomicAdd(s_cnt + hv, iv);
+        else atomicAdd(cnt + ed.y, iv);
+    }
+    if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x)
+        if (s_cnt[k]) atomicAdd(cnt + s_keys[k], s_cnt[k]);
+}
+
+void launch_node_side_counts_hub(const uint2* e, int64_t m, const uint32_t* packed, const uint32_t* hub_keys,
+                                 unsigned long long* cnt, int* bad, cudaStream_t s) {
+    if (m <= 0) return;
+    int64_t g = (m + 511) / 512;
+    int cap = num_sms() * 4;
+    k_node_side_counts_hub<<<(int)(g < cap ? (g < 1 ? 1 : g) : cap), 512, 0, s>>>(e, m, packed, hub_keys, cnt, bad);
+}
+
 void launch_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max, cudaStream_t s) {
     if (m > 0) k_check_piece<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, n, bad_max);
 }

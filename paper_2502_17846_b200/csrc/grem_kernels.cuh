@@ -260,8 +260,11 @@ void launch_count_cuts_packed(const uint2* e, int64_t m, const int32_t* lab, int
                               unsigned long long* d_cut, int* d_neg, cudaStream_t s);
 
 // --- partitioned storage (grem_store.cu; store.py:55-104, 201-235) ---
+void launch_node_side_counts_hub(const uint2* e, int64_t m, const uint32_t* packed, const uint32_t* hub_keys,
+                                 unsigned long long* cnt, int* bad, cudaStream_t s);
 void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* cnt,
-                       uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s);
+                       uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s,
+                       const uint32_t* hub_keys = nullptr);
 void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s);
 size_t bucket_sort_temp_bytes(int64_t m);
 // stable p x p bucket scatter of the edges (keys_a/keys_b: m u32 scratch);

@@ -1954,7 +1954,20 @@ int grem_node_stats_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n
         c->ns_k0.ensure(n + 1, s);
         int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
         c->ns_pack.ensure(n / 16 + 2, s);
-        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_pack.p, c->ns_k.p, c->ns_k0.p, d_bad, s);
+        // hubs of the edge list (a 4M-edge degree sample), privatised in shared memory
+        static const bool no_hubs = getenv("GREM_NODE_STATS_NO_HUBS") != nullptr;   // A/B switch
+        c->hubs_on = false;
+        if (!no_hubs && d) {
+            c->scratch.ensure(n + 2, s);
+            BisectArgs ha{};
+            ha.e = d;
+            ha.m = m;
+            ha.n = n;
+            ha.chunk = m;
+            detect_hubs(c, ha);
+        }
+        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_pack.p, c->ns_k.p, c->ns_k0.p, d_bad, s,
+                          c->hubs_on ? c->hub_table.p : nullptr);
         c->kernels += 3;
         CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

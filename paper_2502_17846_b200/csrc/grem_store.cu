@@ -181,7 +181,8 @@ __global__ void k_node_stats_final(const ulonglong2* __restrict__ cnt, int64_t n
 
 // cnt: 2n u64 (the unpacked fallback needs all of it); packed: n/16 + 1 u32
 void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* cnt,
-                       uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s) {
+                       uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s,
+                       const uint32_t* hub_keys) {
     cudaMemsetAsync(bad, 0, sizeof(int), s);
     int cap = num_sms() * 8;
     auto grid_for = [&](int64_t work) {
@@ -192,7 +193,8 @@ void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n,
     if (m < (1LL << 32) && !unpacked) {
         cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * n, s);
         k_pack_labels2<<<grid_for((n + 15) / 16), 256, 0, s>>>(lab, n, packed);
-        if (m > 0) k_node_side_counts_packed<<<grid_for(m), 256, 0, s>>>(e, m, packed, cnt, bad);
+        if (hub_keys) launch_node_side_counts_hub(e, m, packed, hub_keys, cnt, bad, s);
+        else if (m > 0) k_node_side_counts_packed<<<grid_for(m), 256, 0, s>>>(e, m, packed, cnt, bad);
         k_node_stats_final_packed<<<grid_for(n), 256, 0, s>>>(cnt, n, k, k0);
         return;
     }
