@@ -161,6 +161,9 @@ int grem_reorder_records(grem_ctx* ctx, const int32_t* labels, int64_t num_nodes
 int grem_node_stats_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
                         int edges_on_device, const int32_t* labels, int labels_on_device, int64_t* k_out,
                         int64_t* k0_out);
+/* The same on a GRPE u32 file, streamed in through the overlapped reader. */
+int grem_node_stats_file(grem_ctx* ctx, const char* path, const int32_t* labels, int labels_on_device,
+                         int64_t* k_out, int64_t* k0_out);
 
 /* Device copy of the host edge list staged by the last call on this context
  * (edges_on_device = 0); valid until the next call.  Lets a sharded caller run

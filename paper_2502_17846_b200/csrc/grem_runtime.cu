@@ -1941,42 +1941,58 @@ int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_
     });
 }
 
+// compute_node_stats body on staged edges / labels (theory.py:97-122)
+static void node_stats_dev(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const int32_t* lab, int64_t* k_out,
+                    int64_t* k0_out) {
+    cudaStream_t s = c->s;
+    ingest_wait_all(c);
+    if (label_parts(c, lab, n) > 2) fail(GREM_E_FORMAT, "reference labels are not a bisection");   // theory.py:107-108
+    c->ns_cnt.ensure(2 * n + 2, s);
+    c->ns_k.ensure(n + 1, s);
+    c->ns_k0.ensure(n + 1, s);
+    int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
+    c->ns_pack.ensure(n / 16 + 2, s);
+    // hubs of the edge list (a 4M-edge degree sample), privatised in shared memory
+    static const bool no_hubs = getenv("GREM_NODE_STATS_NO_HUBS") != nullptr;   // A/B switch
+    c->hubs_on = false;
+    if (!no_hubs && d) {
+        c->scratch.ensure(n + 2, s);
+        BisectArgs ha{};
+        ha.e = d;
+        ha.m = m;
+        ha.n = n;
+        ha.chunk = m;
+        detect_hubs(c, ha);
+    }
+    launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_pack.p, c->ns_k.p, c->ns_k0.p, d_bad, s,
+                      c->hubs_on ? c->hub_table.p : nullptr);
+    c->kernels += 3;
+    CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int bad;
+    memcpy(&bad, &c->h_pin[1], sizeof(int));
+    if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+    CK(cudaMemcpyAsync(k_out, c->ns_k.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+    CK(cudaMemcpyAsync(k0_out, c->ns_k0.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+    CK(cudaStreamSynchronize(s));
+}
+
 int grem_node_stats_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device,
                         const int32_t* labels, int labels_on_device, int64_t* k_out, int64_t* k0_out) {
     if (!c || !labels || !k_out || !k0_out) return GREM_E_FORMAT;
     return guarded(c, [&] {
-        cudaStream_t s = c->s;
         const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
-        const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
-        if (label_parts(c, lab, n) > 2) fail(GREM_E_FORMAT, "reference labels are not a bisection");   // theory.py:107-108
-        c->ns_cnt.ensure(2 * n + 2, s);
-        c->ns_k.ensure(n + 1, s);
-        c->ns_k0.ensure(n + 1, s);
-        int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
-        c->ns_pack.ensure(n / 16 + 2, s);
-        // hubs of the edge list (a 4M-edge degree sample), privatised in shared memory
-        static const bool no_hubs = getenv("GREM_NODE_STATS_NO_HUBS") != nullptr;   // A/B switch
-        c->hubs_on = false;
-        if (!no_hubs && d) {
-            c->scratch.ensure(n + 2, s);
-            BisectArgs ha{};
-            ha.e = d;
-            ha.m = m;
-            ha.n = n;
-            ha.chunk = m;
-            detect_hubs(c, ha);
-        }
-        launch_node_stats(d, m, lab, n, c->ns_cnt.p, c->ns_pack.p, c->ns_k.p, c->ns_k0.p, d_bad, s,
-                          c->hubs_on ? c->hub_table.p : nullptr);
-        c->kernels += 3;
-        CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        int bad;
-        memcpy(&bad, &c->h_pin[1], sizeof(int));
-        if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
-        CK(cudaMemcpyAsync(k_out, c->ns_k.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
-        CK(cudaMemcpyAsync(k0_out, c->ns_k0.p, sizeof(int64_t) * n, cudaMemcpyDefault, s));
-        CK(cudaStreamSynchronize(s));
+        node_stats_dev(c, d, m, n, stage_labels(c, labels, n, labels_on_device), k_out, k0_out);
+    });
+}
+
+int grem_node_stats_file(grem_ctx* c, const char* path, const int32_t* labels, int labels_on_device,
+                         int64_t* k_out, int64_t* k0_out) {
+    if (!c || !path || !labels || !k_out || !k0_out) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        GrpeHeader hd;
+        const uint2* d = load_grpe(c, path, &hd);
+        node_stats_dev(c, d, hd.m, hd.n, stage_labels(c, labels, hd.n, labels_on_device), k_out, k0_out);
     });
 }
 

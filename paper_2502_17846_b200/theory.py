@@ -14,12 +14,12 @@ reference's.
 
 from __future__ import annotations
 
-import ctypes
+import os
 
 import numpy as np
 
 from . import _abi
-from .edgefile import edges_u32
+from .edgefile import edges_u32, is_native_binary
 from .errors import FormatError
 from .grem import _raise, context
 
@@ -75,4 +75,12 @@ def compute_node_stats(efile, labels):
     labels = np.asarray(labels)
     if labels.shape[0] != n:
         raise FormatError(f"labels cover {labels.shape[0]} nodes, file has {n}")
-    return node_stats_edges(edges_u32(efile), n, labels)
+    if not is_native_binary(efile):
+        return node_stats_edges(edges_u32(efile), n, labels)
+    lab = np.ascontiguousarray(labels.astype(np.int32))
+    k = np.empty(n, dtype=np.int64)
+    k0 = np.empty(n, dtype=np.int64)
+    rc = _abi.lib().grem_node_stats_file(context(), os.fsencode(efile.path), lab.ctypes.data, 0, k.ctypes.data,
+                                         k0.ctypes.data)
+    _raise(rc)
+    return NodeStats(k, k0)

@@ -129,3 +129,25 @@ def test_gpu_unpacked_fallback_matches():
     env = dict(os.environ, GREM_NODE_STATS_UNPACKED="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_gpu_file_front_end(tmp_path, monkeypatch):
+    """compute_node_stats on a GRPE u32 file goes through grem_node_stats_file
+    (overlapped reader, small pieces forced): equal to the array entry point
+    and the oracle on a hub-sized case; an out-of-range id raises FormatError."""
+    from paper_2502_17846_b200 import FormatError, compute_node_stats, node_stats_edges, synth
+    from paper_2502_17846_b200.edgefile import open_edge_file
+    monkeypatch.setenv("GREM_INGEST_PIECE", "100003")
+    n, m = 300_000, 3_000_000
+    edges = synth.powerlaw_edges(n, m, seed=8)
+    lab = np.random.default_rng(8).integers(0, 2, size=n)
+    st = compute_node_stats(open_edge_file(write_grpe(tmp_path / "p.grpe", edges, n)), lab)
+    st2 = node_stats_edges(edges, n, lab)
+    k, k0 = theory_oracle.node_stats(edges, n, lab)
+    assert np.array_equal(st.k, k) and np.array_equal(st.k0, k0)
+    assert np.array_equal(st2.k, k) and np.array_equal(st2.k0, k0)
+    bad = edges.astype(np.int64)
+    bad[m - 3] = (1, n + 7)
+    with pytest.raises(FormatError):
+        compute_node_stats(open_edge_file(write_grpe(tmp_path / "b.grpe", bad, n)), lab)
