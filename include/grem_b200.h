@@ -142,6 +142,11 @@ int grem_partition_shard_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_e
 int grem_write_buckets_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
                            int edges_on_device, const int32_t* labels, int labels_on_device, uint32_t* out_edges,
                            int out_on_device, uint64_t* counts_out, int64_t counts_cap, int64_t* p_out);
+/* The same on a GRPE u32 file, streamed in through the overlapped reader
+ * (out_edges: header num_edges pairs). */
+int grem_write_buckets_file(grem_ctx* ctx, const char* path, const int32_t* labels, int labels_on_device,
+                            uint32_t* out_edges, int out_on_device, uint64_t* counts_out, int64_t counts_cap,
+                            int64_t* p_out);
 
 /* reorder_features (store.py:201-235): nodes grouped by label, ascending id
  * inside a partition.  perm_out[node] = slot (int64, host); counts_out (host,

@@ -1900,48 +1900,68 @@ int64_t label_parts(grem_ctx* c, const int32_t* lab, int64_t n, bool* any_negati
 }
 }  // namespace
 
+// write_buckets body on staged edges / labels (store.py:55-104)
+static void write_buckets_dev(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const int32_t* lab,
+                              uint32_t* out_edges, int out_on_device, uint64_t* counts_out, int64_t counts_cap,
+                              int64_t* p_out) {
+    cudaStream_t s = c->s;
+    ingest_wait_all(c);
+    bool neg = false;
+    int64_t p = label_parts(c, lab, n, &neg);   // store.py:71-72
+    if (p_out) *p_out = p;
+    if (p >= 65536) fail(GREM_E_FORMAT, "write_buckets supports fewer than 65536 partitions");
+    int64_t nb = p * p;
+    if (nb > counts_cap) fail(GREM_E_FORMAT, "counts buffer holds " + std::to_string(counts_cap) +
+                                                  " entries, p*p = " + std::to_string(nb));
+    c->bk_keys_a.ensure(m + 1, s);
+    c->bk_keys_b.ensure(m + 1, s);
+    c->bk_counts.ensure(nb, s);
+    uint2* out = out_on_device ? reinterpret_cast<uint2*>(out_edges) : nullptr;
+    if (!out) {
+        c->bk_out.ensure(m + 1, s);
+        out = c->bk_out.p;
+    }
+    ensure_temp(c, bucket_sort_temp_bytes(m));
+    int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
+    c->packed_lab.ensure(n / 2 + 2, s);   // <= 16-bit packed labels (p < 65536)
+    launch_write_buckets(d, m, lab, n, neg, (uint32_t)p, c->bk_keys_a.p, c->bk_keys_b.p, c->packed_lab.p, out,
+                         c->bk_counts.p, d_bad, c->temp.p, c->temp.cap, s);
+    c->kernels += 4;
+    CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int bad;
+    memcpy(&bad, &c->h_pin[1], sizeof(int));
+    if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
+    CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, s));
+    if (!out_on_device && m > 0)
+        CK(cudaMemcpyAsync(out_edges, out, sizeof(uint2) * m, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
 int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device,
                            const int32_t* labels, int labels_on_device, uint32_t* out_edges, int out_on_device,
                            uint64_t* counts_out, int64_t counts_cap, int64_t* p_out) {
     if (!c || !labels || !counts_out || (m > 0 && !out_edges)) return GREM_E_FORMAT;
     return guarded(c, [&] {
-        cudaStream_t s = c->s;
         const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
-        const int32_t* lab = stage_labels(c, labels, n, labels_on_device);
-        bool neg = false;
-        int64_t p = label_parts(c, lab, n, &neg);   // store.py:71-72
-        if (p_out) *p_out = p;
-        if (p >= 65536) fail(GREM_E_FORMAT, "write_buckets supports fewer than 65536 partitions");
-        int64_t nb = p * p;
-        if (nb > counts_cap) fail(GREM_E_FORMAT, "counts buffer holds " + std::to_string(counts_cap) +
-                                                      " entries, p*p = " + std::to_string(nb));
-        c->bk_keys_a.ensure(m + 1, s);
-        c->bk_keys_b.ensure(m + 1, s);
-        c->bk_counts.ensure(nb, s);
-        uint2* out = out_on_device ? reinterpret_cast<uint2*>(out_edges) : nullptr;
-        if (!out) {
-            c->bk_out.ensure(m + 1, s);
-            out = c->bk_out.p;
-        }
-        ensure_temp(c, bucket_sort_temp_bytes(m));
-        int* d_bad = reinterpret_cast<int*>(c->cc_sizes.p) + 2;
-        c->packed_lab.ensure(n / 2 + 2, s);   // <= 16-bit packed labels (p < 65536)
-        launch_write_buckets(d, m, lab, n, neg, (uint32_t)p, c->bk_keys_a.p, c->bk_keys_b.p, c->packed_lab.p, out,
-                             c->bk_counts.p, d_bad, c->temp.p, c->temp.cap, s);
-        c->kernels += 4;
-        CK(cudaMemcpyAsync(&c->h_pin[1], d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        int bad;
-        memcpy(&bad, &c->h_pin[1], sizeof(int));
-        if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
-        CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, s));
-        if (!out_on_device && m > 0)
-            CK(cudaMemcpyAsync(out_edges, out, sizeof(uint2) * m, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        write_buckets_dev(c, d, m, n, stage_labels(c, labels, n, labels_on_device), out_edges, out_on_device,
+                          counts_out, counts_cap, p_out);
     });
 }
 
-// compute_node_stats body on staged edges / labels (theory.py:97-122)
+int grem_write_buckets_file(grem_ctx* c, const char* path, const int32_t* labels, int labels_on_device,
+                            uint32_t* out_edges, int out_on_device, uint64_t* counts_out, int64_t counts_cap,
+                            int64_t* p_out) {
+    if (!c || !path || !labels || !counts_out) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        GrpeHeader hd = read_grpe_header(path);
+        if (hd.m > 0 && !out_edges) fail(GREM_E_FORMAT, "out_edges is NULL");
+        const uint2* d = load_grpe(c, path, &hd);
+        write_buckets_dev(c, d, hd.m, hd.n, stage_labels(c, labels, hd.n, labels_on_device), out_edges,
+                          out_on_device, counts_out, counts_cap, p_out);
+    });
+}
+
 static void node_stats_dev(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const int32_t* lab, int64_t* k_out,
                     int64_t* k0_out) {
     cudaStream_t s = c->s;

@@ -30,7 +30,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from .edgefile import FLAG_WIDE_IDS, edges_u32
+from .edgefile import FLAG_WIDE_IDS, edges_u32, is_native_binary
 from .errors import FormatError
 from .grem import _raise, context
 
@@ -105,17 +105,24 @@ def write_buckets(efile, labels, out_path: str):
     if labels.shape[0] != n:
         raise FormatError(f"labels cover {labels.shape[0]} nodes, file has {n}")
     lab = np.ascontiguousarray(labels.astype(np.int32))
-    edges = edges_u32(efile)
-    m = int(edges.shape[0])
     width = int(getattr(efile.meta, "node_id_width", 32))
     assigned = lab[lab >= 0]
     p_guess = int(assigned.max()) + 1 if assigned.size else 1
     counts = np.zeros(p_guess * p_guess, dtype=np.uint64)
-    out = np.empty((m, 2), dtype=np.uint32)
     p_out = ctypes.c_int64()
-    rc = _abi.lib().grem_write_buckets_u32(context(), edges.ctypes.data, m, n, 0, lab.ctypes.data, 0,
-                                           out.ctypes.data, 0, counts.ctypes.data, counts.size,
-                                           ctypes.byref(p_out))
+    if is_native_binary(efile):   # GRPE u32: the overlapped native reader
+        m = int(efile.meta.num_edges)
+        out = np.empty((m, 2), dtype=np.uint32)
+        rc = _abi.lib().grem_write_buckets_file(context(), os.fsencode(efile.path), lab.ctypes.data, 0,
+                                                out.ctypes.data, 0, counts.ctypes.data, counts.size,
+                                                ctypes.byref(p_out))
+    else:
+        edges = edges_u32(efile)
+        m = int(edges.shape[0])
+        out = np.empty((m, 2), dtype=np.uint32)
+        rc = _abi.lib().grem_write_buckets_u32(context(), edges.ctypes.data, m, n, 0, lab.ctypes.data, 0,
+                                               out.ctypes.data, 0, counts.ctypes.data, counts.size,
+                                               ctypes.byref(p_out))
     _raise(rc)
     p = int(p_out.value)
     pair = 2 * (width // 8)
