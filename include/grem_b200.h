@@ -170,6 +170,15 @@ int grem_node_stats_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges,
 int grem_node_stats_file(grem_ctx* ctx, const char* path, const int32_t* labels, int labels_on_device,
                          int64_t* k_out, int64_t* k0_out);
 
+/* external_shuffle (streamcut/edgefile.py:248-327): a uniform random
+ * permutation of the edge list, deterministic per seed (64-bit counter-hash
+ * keys + one radix sort; the reference's numpy-PCG64 order is not
+ * reproduced).  out_edges: num_edges pairs, host or device. */
+int grem_shuffle_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges, int64_t num_nodes,
+                     int edges_on_device, uint64_t seed, uint32_t* out_edges, int out_on_device);
+/* The same from a GRPE u32 file (overlapped reader) to a GRPE u32 file. */
+int grem_shuffle_file(grem_ctx* ctx, const char* in_path, uint64_t seed, const char* out_path);
+
 /* Device copy of the host edge list staged by the last call on this context
  * (edges_on_device = 0); valid until the next call.  Lets a sharded caller run
  * grem_count_cuts_u32 on the merged labels without a second upload.

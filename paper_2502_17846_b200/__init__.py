@@ -13,6 +13,7 @@ existing callers (CLI, tests) use the GPU path unchanged.
 from .config import ChunkPlan, CutReport, GremConfig, SeedConfig, default_capacity
 from .errors import CapacityError, DeviceError, FormatError, StreamcutError
 from .theory import compute_node_stats, node_stats_edges
+from .shuffle import external_shuffle
 from .grem import bisect, bisect_edges, count_cuts, last_stats, partition, partition_edges, set_device
 
 __version__ = "0.1.0"
@@ -51,5 +52,5 @@ __all__ = [
     "bisect", "partition", "count_cuts", "bisect_edges", "partition_edges", "set_device", "last_stats",
     "GremConfig", "SeedConfig", "ChunkPlan", "CutReport", "default_capacity",
     "StreamcutError", "FormatError", "CapacityError", "DeviceError", "install_into_streamcut",
-    "compute_node_stats", "node_stats_edges",
+    "compute_node_stats", "node_stats_edges", "external_shuffle",
 ]

@@ -262,6 +262,9 @@ void launch_count_cuts_packed(const uint2* e, int64_t m, const int32_t* lab, int
 // --- partitioned storage (grem_store.cu; store.py:55-104, 201-235) ---
 void launch_node_side_counts_hub(const uint2* e, int64_t m, const uint32_t* packed, const uint32_t* hub_keys,
                                  unsigned long long* cnt, int* bad, cudaStream_t s);
+size_t shuffle_temp_bytes(int64_t m);
+void launch_shuffle(const uint2* e, int64_t m, unsigned long long seed, unsigned long long* keys,
+                    unsigned long long* vals, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* cnt,
                        uint32_t* packed, int64_t* k, int64_t* k0, int* bad, cudaStream_t s,
                        const uint32_t* hub_keys = nullptr);

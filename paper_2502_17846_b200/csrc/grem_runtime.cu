@@ -194,6 +194,7 @@ struct grem_ctx {
     DBuf<unsigned long long> ns_cnt{"ns_cnt"};   // node stats (theory)
     DBuf<int64_t> ns_k{"ns_k"}, ns_k0{"ns_k0"};
     DBuf<uint32_t> ns_pack{"ns_pack"};
+    DBuf<unsigned long long> sh_keys{"sh_keys"}, sh_vals{"sh_vals"};   // external shuffle
     DBuf<long long> bk_perm{"bk_perm"};
     DBuf<uint8_t> bk_rec{"bk_rec"}, bk_rec_out{"bk_rec_out"};
     bool staged_last = false;   // edges_owned holds the last call's host edge list
@@ -1815,6 +1816,7 @@ void grem_destroy(grem_ctx* c) {
     c->part_orig.release();
     c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
     c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release(); c->ns_pack.release();
+    c->sh_keys.release(); c->sh_vals.release();
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -1959,6 +1961,94 @@ int grem_write_buckets_file(grem_ctx* c, const char* path, const int32_t* labels
         const uint2* d = load_grpe(c, path, &hd);
         write_buckets_dev(c, d, hd.m, hd.n, stage_labels(c, labels, hd.n, labels_on_device), out_edges,
                           out_on_device, counts_out, counts_cap, p_out);
+    });
+}
+
+// external_shuffle (edgefile.py:248-327) on staged edges: the shuffled list
+// (device) is returned; see launch_shuffle for the permutation.
+static const uint2* shuffle_dev(grem_ctx* c, const uint2* d, int64_t m, uint64_t seed) {
+    cudaStream_t s = c->s;
+    ingest_wait_all(c);
+    if (m <= 0) return nullptr;
+    c->sh_keys.ensure(2 * m, s);
+    c->sh_vals.ensure(2 * m, s);
+    ensure_temp(c, shuffle_temp_bytes(m));
+    launch_shuffle(d, m, (unsigned long long)seed, c->sh_keys.p, c->sh_vals.p, c->temp.p, c->temp.cap, s);
+    c->kernels += 5;
+    return reinterpret_cast<const uint2*>(c->sh_vals.p + m);
+}
+
+int grem_shuffle_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device, uint64_t seed,
+                     uint32_t* out_edges, int out_on_device) {
+    if (!c || (m > 0 && !out_edges)) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
+        const uint2* r = shuffle_dev(c, d, m, seed);
+        if (m > 0) CK(cudaMemcpyAsync(out_edges, r, sizeof(uint2) * m, cudaMemcpyDefault, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        (void)out_on_device;
+    });
+}
+
+// GRPE u32 file -> shuffled GRPE u32 file; the payload is written in 128 MB
+// pieces (device -> pinned ring slot -> pwrite by GREM_INGEST_THREADS threads)
+int grem_shuffle_file(grem_ctx* c, const char* in_path, uint64_t seed, const char* out_path) {
+    if (!c || !in_path || !out_path) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        GrpeHeader hd;
+        const uint2* d = load_grpe(c, in_path, &hd);
+        const uint2* r = shuffle_dev(c, d, hd.m, seed);
+        int fd = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (fd < 0) fail(GREM_E_FORMAT, std::string(out_path) + ": cannot create");
+        unsigned char h[28];
+        uint32_t version = 1, flags = 0;
+        uint64_t n = (uint64_t)hd.n, m = (uint64_t)hd.m;
+        memcpy(h, "GRPE", 4);
+        memcpy(h + 4, &version, 4);
+        memcpy(h + 8, &flags, 4);
+        memcpy(h + 12, &n, 8);
+        memcpy(h + 20, &m, 8);
+        bool ok = pwrite(fd, h, 28, 0) == 28;
+        if (hd.m > 0) {
+            ensure_ring(c);
+            const int threads = [] {
+                const char* v = getenv("GREM_INGEST_THREADS");
+                int hw = (int)std::thread::hardware_concurrency();
+                int t = v ? atoi(v) : (hw < 16 ? hw : 16);
+                return t < 1 ? 1 : t;
+            }();
+            const int64_t piece = (int64_t)(c->ring_bytes / 8);
+            for (int64_t off = 0; off < hd.m && ok; off += piece) {
+                int64_t cnt = hd.m - off < piece ? hd.m - off : piece;
+                char* buf = (char*)c->ring[0];
+                CK(cudaMemcpyAsync(buf, r + off, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->s));
+                CK(cudaStreamSynchronize(c->s));
+                const size_t bytes = (size_t)cnt * 8;
+                size_t part = ((bytes + threads - 1) / threads + 4095) & ~(size_t)4095;
+                std::vector<std::thread> ws;
+                std::vector<char> wok(threads, 1);
+                for (int t = 0; t < threads; ++t) {
+                    size_t lo = (size_t)t * part;
+                    if (lo >= bytes) break;
+                    size_t hi = lo + part < bytes ? lo + part : bytes;
+                    ws.emplace_back([=, &wok] {
+                        size_t done = lo;
+                        while (done < hi) {
+                            ssize_t w = pwrite(fd, buf + done, hi - done, 28 + (off_t)off * 8 + (off_t)done);
+                            if (w <= 0) {
+                                wok[t] = 0;
+                                return;
+                            }
+                            done += (size_t)w;
+                        }
+                    });
+                }
+                for (auto& w : ws) w.join();
+                for (char o : wok) ok = ok && o;
+            }
+        }
+        close(fd);
+        if (!ok) fail(GREM_E_FORMAT, std::string(out_path) + ": write failed");
     });
 }
 

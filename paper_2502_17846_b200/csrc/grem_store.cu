@@ -203,6 +203,46 @@ void launch_node_stats(const uint2* e, int64_t m, const int32_t* lab, int64_t n,
     k_node_stats_final<<<grid_for(n), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(cnt), n, k, k0);
 }
 
+// external_shuffle (streamcut/edgefile.py:248-327): a uniform random
+// permutation of the edge list.  Each edge gets a 64-bit key from a
+// counter-based hash of (seed, position) and one radix sort of (key, edge)
+// pairs puts the edges in key order: every permutation is equally likely up
+// to 64-bit key ties (stable: input order), deterministic per seed.  The
+// reference's order comes from numpy's PCG64 Generator and is not
+// reproduced (parity is by multiset, determinism and uniformity).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_shuffle_keys(const uint2* __restrict__ e, int64_t m, unsigned long long seed,
+                               unsigned long long* __restrict__ keys, unsigned long long* __restrict__ vals) {
+    const unsigned long long sk = mix64(seed + 0x9E3779B97F4A7C15ull);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint2 ed = __ldcs(e + i);
+        keys[i] = mix64(sk ^ mix64((unsigned long long)i));
+        vals[i] = ((unsigned long long)ed.y << 32) | ed.x;
+    }
+}
+
+size_t shuffle_temp_bytes(int64_t m) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (const unsigned long long*)nullptr, (unsigned long long*)nullptr, m);
+    return bytes;
+}
+
+// keys/vals: 2 x m u64 each (ping-pong); the shuffled edges land in vals + m
+void launch_shuffle(const uint2* e, int64_t m, unsigned long long seed, unsigned long long* keys,
+                    unsigned long long* vals, void* temp, size_t temp_bytes, cudaStream_t s) {
+    if (m <= 0) return;
+    int cap = num_sms() * 8;
+    int64_t g = (m + 255) / 256;
+    k_shuffle_keys<<<(int)(g < cap ? g : cap), 256, 0, s>>>(e, m, seed, keys, vals);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys + m, vals, vals + m, m, 0, 64, s);
+}
+
 void launch_label_max(const int32_t* lab, int64_t n, int* d_max, cudaStream_t s) {
     cudaMemsetAsync(d_max, 0xFF, sizeof(int), s);
     cudaMemsetAsync(d_max + 1, 0, sizeof(int), s);
