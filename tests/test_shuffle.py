@@ -9,7 +9,6 @@ import pytest
 
 from helpers import write_grpe
 
-pytestmark = pytest.mark.gpu
 
 
 def _read(ef):
@@ -22,6 +21,7 @@ def _multiset(a):
     return a[np.lexsort((a[:, 1], a[:, 0]))]
 
 
+@pytest.mark.gpu
 def test_permutation_and_deterministic(tmp_path):
     from paper_2502_17846_b200 import external_shuffle
     from paper_2502_17846_b200.edgefile import open_edge_file
@@ -37,6 +37,7 @@ def test_permutation_and_deterministic(tmp_path):
     assert out1.meta.num_nodes == 10 and out1.meta.num_edges == 10
 
 
+@pytest.mark.gpu
 def test_budget_errors_and_scatter_sized_input(tmp_path):
     from paper_2502_17846_b200 import FormatError, external_shuffle
     from paper_2502_17846_b200.edgefile import open_edge_file
@@ -49,16 +50,22 @@ def test_budget_errors_and_scatter_sized_input(tmp_path):
     out = external_shuffle(ef, str(tmp_path / "t.grpe"), 1 << 16, rng_seed=1)   # :101-111
     sh = _read(out)
     assert np.array_equal(_multiset(sh), _multiset(edges)) and not np.array_equal(sh, edges)
-    big = open_edge_file(write_grpe(tmp_path / "b.grpe", np.zeros((600_000, 2)), 1))
-    with pytest.raises(FormatError):   # > 4096 scatter buckets (edgefile.py:271-275)
-        external_shuffle(big, str(tmp_path / "u.grpe"), IO_BLOCK(), rng_seed=0)
 
 
-def IO_BLOCK():
-    from paper_2502_17846_b200.shuffle import IO_BLOCK as b
-    return b
+def test_budget_rules_host():
+    """The reference's budget arithmetic (edgefile.py:262-263, 271-275): below one
+    I/O block, or more than 4096 scatter buckets of budget/2 bytes, is a FormatError."""
+    from paper_2502_17846_b200 import FormatError
+    from paper_2502_17846_b200.shuffle import IO_BLOCK, _check_budget
+    _check_budget(600_000, IO_BLOCK)                 # 9.6 MB / 32 KB = 293 buckets
+    _check_budget(10, 1 << 20)                       # in-memory path
+    with pytest.raises(FormatError):
+        _check_budget(9_000_000, IO_BLOCK)           # 4395 buckets
+    with pytest.raises(FormatError):
+        _check_budget(1, IO_BLOCK - 1)
 
 
+@pytest.mark.gpu
 def test_uniform_positions_chi_squared(tmp_path):
     """test_edgefile.py:120-135: where the first edge of a 10-edge file lands over 1000 seeds."""
     import scipy.stats
@@ -75,6 +82,7 @@ def test_uniform_positions_chi_squared(tmp_path):
     assert stat < scipy.stats.chi2.ppf(0.99, df=9), counts
 
 
+@pytest.mark.gpu
 def test_large_wide_and_multi_piece(tmp_path, monkeypatch):
     """A 3M-edge power-law file (reader and writer in many pieces), a 64-bit-id
     file and an in-memory array: multiset preserved, seeds give different orders."""
