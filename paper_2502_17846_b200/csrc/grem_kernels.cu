@@ -272,6 +272,7 @@ __device__ __forceinline__ void cta_range(int64_t m, int64_t& lo, int64_t& hi) {
 }
 
 constexpr int kEdgeThreads = 512;
+constexpr int kDeltaUnroll = 4;
 
 // round 1: every chunk neighbour read with its pre-sweep label (cnt_nbrs,
 // grem.py:82-97 / 138-145); nodes whose counts stay zero get a flag so the
@@ -340,7 +341,7 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
-__global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __restrict__ e, int64_t m,
+__global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
                                                               const uint32_t* __restrict__ chg,
                                                               const int32_t* __restrict__ pos,
@@ -359,24 +360,35 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_delta(const uint2* __res
     __syncthreads();
     int64_t lo, hi;
     cta_range(m, lo, hi);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        uint2 ed = e[i];
-        uint32_t u = ed.x, v = ed.y;
-        if (u == v) continue;
-        uint32_t a = u < v ? u : v, b = u < v ? v : u;
-        uint32_t ca = a >> cshift;
-        if (!((s_chgc[ca >> 5] >> (ca & 31)) & 1u)) continue;   // coarse filter in shared memory
-        if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
-        uint8_t t = tl[a];
-        int cur = t & 0xF, prev = t >> 4;
-        unsigned long long d = enc_label(cur) - enc_label(prev);
-        int hb = hub_find(s_keys, b);
-        if (hb >= 0) {
-            atomicAdd(&s_cnt[hb], d);
-        } else {
-            int32_t pb = pos[b];
-            atomicAdd(&cntc[pb], d);
-            dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
+    // kDeltaUnroll independent edge loads in flight per thread before any of
+    // them is filtered: the stream is latency bound with one load per thread.
+    const int64_t bd = blockDim.x;
+    for (int64_t i0 = lo + threadIdx.x; i0 < hi; i0 += kDeltaUnroll * bd) {
+        uint2 ed[kDeltaUnroll];
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) {
+            int64_t i = i0 + j * bd;
+            ed[j] = i < hi ? __ldcs(&e[i]) : make_uint2(0u, 0u);   // (0,0): a self-loop, skipped
+        }
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) {
+            uint32_t u = ed[j].x, v = ed[j].y;
+            if (u == v) continue;
+            uint32_t a = u < v ? u : v, b = u < v ? v : u;
+            uint32_t ca = a >> cshift;
+            if (!((s_chgc[ca >> 5] >> (ca & 31)) & 1u)) continue;   // coarse filter in shared memory
+            if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
+            uint8_t t = tl[a];
+            int cur = t & 0xF, prev = t >> 4;
+            unsigned long long d = enc_label(cur) - enc_label(prev);
+            int hb = hub_find(s_keys, b);
+            if (hb >= 0) {
+                atomicAdd(&s_cnt[hb], d);
+            } else {
+                int32_t pb = pos[b];
+                atomicAdd(&cntc[pb], d);
+                dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
+            }
         }
     }
     __syncthreads();
