@@ -19,32 +19,34 @@ from .grem import bisect, bisect_edges, count_cuts, last_stats, partition, parti
 __version__ = "0.1.0"
 
 
-def install_into_streamcut():
+def install_into_streamcut(support: bool = False):
     """Swap streamcut's GREM entry points for the B200 ones (before callers
     bind them by name).  partition() inside streamcut resolves bisect through
     the grem module globals (grem.py:300), so rebinding grem.* covers
-    recursion as well."""
+    recursion as well.  ``support=True`` also swaps the label consumers this
+    package provides (store.write_buckets / reorder_features,
+    theory.compute_node_stats, edgefile.external_shuffle), everywhere the
+    reference binds them (package, module, CLI)."""
+    import importlib
+
     import streamcut  # type: ignore
-    import streamcut.grem as sg  # type: ignore
 
-    for mod in (streamcut, sg):
-        mod.bisect = bisect
-        mod.partition = partition
-        mod.count_cuts = count_cuts
-    streamcut.compute_node_stats = compute_node_stats
-    try:
-        import streamcut.theory as st  # type: ignore
+    from . import store as _store
 
-        st.compute_node_stats = compute_node_stats
-    except Exception:  # noqa: BLE001
-        pass
-    try:
-        import streamcut.cli as cli  # type: ignore
-
-        cli.partition = partition
-        cli.count_cuts = count_cuts
-    except Exception:  # noqa: BLE001
-        pass
+    swaps = {"bisect": bisect, "partition": partition, "count_cuts": count_cuts}
+    mods = ["streamcut", "streamcut.grem", "streamcut.cli"]
+    if support:
+        swaps.update(compute_node_stats=compute_node_stats, write_buckets=_store.write_buckets,
+                     reorder_features=_store.reorder_features, external_shuffle=external_shuffle)
+        mods += ["streamcut.theory", "streamcut.store", "streamcut.edgefile"]
+    for name in mods:
+        try:
+            mod = importlib.import_module(name)
+        except Exception:  # noqa: BLE001
+            continue
+        for attr, fn in swaps.items():
+            if hasattr(mod, attr):
+                setattr(mod, attr, fn)
     return streamcut
 
 

@@ -1681,9 +1681,9 @@ __global__ void k_seed_map(const uint32_t* __restrict__ skeys, const uint32_t* _
 size_t seed_csr_temp_bytes(int64_t entries) {
     size_t a = 0, b = 0;
     cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr), dv(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, (int)entries);
+    cub::DeviceRadixSort::SortPairs(nullptr, a, dk, dv, entries);
     cub::DeviceRunLengthEncode::Encode(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
-                                       (long long*)nullptr, (int)entries);
+                                       (long long*)nullptr, entries);
     return a > b ? a : b;
 }
 // keysA/valsA, keysB/valsB: two entries-sized buffer pairs (A = row_of/adj of
@@ -1696,9 +1696,9 @@ void launch_seed_sort(const uint2* e, int64_t m, uint32_t* keysA, uint32_t* vals
     k_seed_pairs<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, reinterpret_cast<uint2*>(keysA),
                                                       reinterpret_cast<uint2*>(valsA));
     cub::DoubleBuffer<uint32_t> dk(keysA, keysB), dv(valsA, valsB);
-    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk, dv, (int)entries, 0, end_bit, s);
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk, dv, entries, 0, end_bit, s);
     *sorted_in_b = dk.Current() == keysB;
-    cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, dk.Current(), nodes, counts, d_nruns, (int)entries, s);
+    cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, dk.Current(), nodes, counts, d_nruns, entries, s);
 }
 void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const int32_t* rank,
                      uint32_t* row_of, uint32_t* adj, int32_t* selfc, cudaStream_t s) {
@@ -2448,18 +2448,20 @@ __global__ void k_max_id(const uint2* __restrict__ e, int64_t m, uint32_t* mx) {
 // ingest piece check (edgefile.py:63-65): endpoints >= n are recorded (max)
 // and replaced by 0 so that kernels that run before the host sees the error
 // stay in bounds; the call then fails with the reference's FormatError.
-__global__ void k_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max) {
+// bad_max: u64, max bad id + 1 (0 = no bad endpoint); 64-bit so that a bad id
+// of 0xFFFFFFFF (the usual -1 sentinel) is still recorded
+__global__ void k_check_piece(uint2* e, int64_t m, uint32_t n, unsigned long long* bad_max) {
     uint32_t v = 0;
     bool any = false;
     GRID_STRIDE(i, m) {
         uint2 ed = e[i];
         if (ed.x >= n || ed.y >= n) {
-            v = max(v, max(ed.x, ed.y));
+            v = max(v, max(ed.x >= n ? ed.x : 0u, ed.y >= n ? ed.y : 0u));
             any = true;
             e[i] = make_uint2(ed.x >= n ? 0u : ed.x, ed.y >= n ? 0u : ed.y);
         }
     }
-    if (any) atomicMax(bad_max, v + 1);   // 0 = no bad endpoint
+    if (any) atomicMax(bad_max, (unsigned long long)v + 1ull);
 }
 // compute_node_stats (theory.py:97-122), hub-privatised form of the packed
 // count (grem_store.cu): the bisection's hub table (detect_hubs) is loaded
@@ -2509,7 +2511,7 @@ void launch_node_side_counts_hub(const uint2* e, int64_t m, const uint32_t* pack
     k_node_side_counts_hub<<<(int)(g < cap ? (g < 1 ? 1 : g) : cap), 512, 0, s>>>(e, m, packed, hub_keys, cnt, bad);
 }
 
-void launch_check_piece(uint2* e, int64_t m, uint32_t n, uint32_t* bad_max, cudaStream_t s) {
+void launch_check_piece(uint2* e, int64_t m, uint32_t n, unsigned long long* bad_max, cudaStream_t s) {
     if (m > 0) k_check_piece<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, n, bad_max);
 }
 void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_t s) {
@@ -2776,7 +2778,7 @@ struct SidePred {
 };
 size_t extract_temp_bytes(int64_t m) {
     size_t bytes = 0;
-    cub::DeviceSelect::If(nullptr, bytes, (const uint2*)nullptr, (uint2*)nullptr, (long long*)nullptr, (int)m,
+    cub::DeviceSelect::If(nullptr, bytes, (const uint2*)nullptr, (uint2*)nullptr, (long long*)nullptr, m,
                           SidePred{nullptr, 0});
     return bytes;
 }
@@ -2790,7 +2792,7 @@ __global__ void k_remap(uint2* e, const long long* cnt, const int32_t* newid) {
 void launch_extract(const uint2* e, int64_t m, const int8_t* lab, int side, const int32_t* newid, uint2* out,
                     long long* d_count, void* temp, size_t temp_bytes, cudaStream_t s) {
     // kept edges in file order (stable selection), dense ids = rank among members
-    cub::DeviceSelect::If(temp, temp_bytes, e, out, d_count, (int)m, SidePred{lab, side}, s);
+    cub::DeviceSelect::If(temp, temp_bytes, e, out, d_count, m, SidePred{lab, side}, s);
     k_remap<<<grid_for(m, 256, 8), 256, 0, s>>>(out, d_count, newid);
 }
 

@@ -165,7 +165,7 @@ struct grem_ctx {
     std::vector<IngestMark> ingest;
     const uint2* ingest_base = nullptr;
     int64_t ingest_m = 0, ingest_n = 0;
-    uint32_t* d_bad = nullptr;
+    unsigned long long* d_bad = nullptr;   // ingest: max bad endpoint + 1 (0 = none)
     long long* h_pin = nullptr;     // [32] pinned mirror
     // cub temp
     DBuf<unsigned char> temp{"temp"};
@@ -1146,16 +1146,15 @@ void ingest_wait_all(grem_ctx* c) {
 void ingest_finish(grem_ctx* c) {
     if (!c->ingest_base) return;
     ingest_wait_all(c);
-    uint32_t bad = 0;
-    CK(cudaMemcpyAsync(&c->h_pin[0], c->d_bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaMemcpyAsync(&c->h_pin[0], c->d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
-    memcpy(&bad, &c->h_pin[0], sizeof(uint32_t));
+    unsigned long long bad = (unsigned long long)c->h_pin[0];
     for (auto& mk : c->ingest) cudaEventDestroy(mk.ev);
     c->ingest.clear();
     int64_t n = c->ingest_n;
     c->ingest_base = nullptr;
     if (bad)
-        fail(GREM_E_FORMAT, "edge endpoint " + std::to_string((int64_t)bad - 1) + " >= num_nodes " + std::to_string(n));
+        fail(GREM_E_FORMAT, "edge endpoint " + std::to_string(bad - 1) + " >= num_nodes " + std::to_string(n));
 }
 void ingest_abort(grem_ctx* c) {
     {
@@ -1178,13 +1177,13 @@ void ingest_begin(grem_ctx* c, const uint2* dst, int64_t m, int64_t n) {
         static const bool low = getenv("GREM_COPY_PRIO_LOW") != nullptr;   // A/B switch
         CK(cudaStreamCreateWithPriority(&c->copy_s, cudaStreamNonBlocking, low ? lo : hi));
     }
-    if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(uint32_t)));
+    if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
     cudaEvent_t ready;
     CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     CK(cudaEventRecord(ready, c->s));
     CK(cudaStreamWaitEvent(c->copy_s, ready, 0));
     cudaEventDestroy(ready);
-    CK(cudaMemsetAsync(c->d_bad, 0, sizeof(uint32_t), c->copy_s));
+    CK(cudaMemsetAsync(c->d_bad, 0, sizeof(unsigned long long), c->copy_s));
     c->ingest_base = dst;
     c->ingest_m = m;
     c->ingest_n = n;
@@ -1970,6 +1969,31 @@ static const uint2* shuffle_dev(grem_ctx* c, const uint2* d, int64_t m, uint64_t
     cudaStream_t s = c->s;
     ingest_wait_all(c);
     if (m <= 0) return nullptr;
+    // the permutation is done in HBM (2 x m u64 keys + 2 x m u64 values + the
+    // sort's temp space): refuse up front, naming the limit, instead of
+    // failing an allocation half way (the reference is an external-memory
+    // shuffle, edgefile.py:248-327; here the bound is device memory)
+    {
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        auto have = [](size_t cap_elems, int64_t want) { return cap_elems >= (size_t)want ? (size_t)want : 0; };
+        size_t need = 2 * 2 * sizeof(unsigned long long) * (size_t)m + shuffle_temp_bytes(m);
+        size_t held = sizeof(unsigned long long) * (have(c->sh_keys.cap, 2 * m) + have(c->sh_vals.cap, 2 * m));
+        if (need > held && need - held > free_b) {   // memory the stream-ordered pool holds but does not use
+            int dev = 0;
+            cudaMemPool_t pool;
+            CK(cudaStreamSynchronize(s));
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+            CK(cudaMemPoolTrimTo(pool, 0));
+            CK(cudaMemGetInfo(&free_b, &total_b));
+        }
+        if (need > held && need - held > free_b)
+            fail(GREM_E_NOMEM, "external_shuffle of " + std::to_string(m) + " edges needs " +
+                                   std::to_string((need - held) >> 20) + " MiB more device memory than the " +
+                                   std::to_string(free_b >> 20) + " MiB free (limit: ~" +
+                                   std::to_string(total_b / 40 / 1000000) + " M edges on this GPU)");
+    }
     c->sh_keys.ensure(2 * m, s);
     c->sh_vals.ensure(2 * m, s);
     ensure_temp(c, shuffle_temp_bytes(m));
@@ -2000,6 +2024,10 @@ int grem_shuffle_file(grem_ctx* c, const char* in_path, uint64_t seed, const cha
         const uint2* r = shuffle_dev(c, d, hd.m, seed);
         int fd = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
         if (fd < 0) fail(GREM_E_FORMAT, std::string(out_path) + ": cannot create");
+        struct Unlink {   // a failed call leaves no partial output file behind
+            const char* path; int fd; bool keep = false;
+            ~Unlink() { if (!keep) { if (fd >= 0) close(fd); unlink(path); } }
+        } guard{out_path, fd};
         unsigned char h[28];
         uint32_t version = 1, flags = 0;
         uint64_t n = (uint64_t)hd.n, m = (uint64_t)hd.m;
@@ -2047,8 +2075,9 @@ int grem_shuffle_file(grem_ctx* c, const char* in_path, uint64_t seed, const cha
                 for (char o : wok) ok = ok && o;
             }
         }
-        close(fd);
         if (!ok) fail(GREM_E_FORMAT, std::string(out_path) + ": write failed");
+        guard.keep = true;
+        close(fd);
     });
 }
 

@@ -94,7 +94,7 @@ __global__ void k_bucket_counts(const uint32_t* __restrict__ skeys, int64_t m, i
 size_t bucket_sort_temp_bytes(int64_t m) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)m);
+                                    (const unsigned long long*)nullptr, (unsigned long long*)nullptr, m);   // 64-bit item count
     return bytes;
 }
 
@@ -275,7 +275,7 @@ void launch_write_buckets(const uint2* e, int64_t m, const int32_t* lab, int64_t
         while (end_bit < 32 && ((uint64_t)(nb - 1) >> end_bit) != 0) ++end_bit;
         cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_a, keys_b,
                                         reinterpret_cast<const unsigned long long*>(e),
-                                        reinterpret_cast<unsigned long long*>(out), (int)m, 0, end_bit, s);
+                                        reinterpret_cast<unsigned long long*>(out), m, 0, end_bit, s);
         k_bucket_counts<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(keys_b, m, nb, counts);
     } else {
         cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nb, s);
@@ -308,7 +308,7 @@ __global__ void k_gather_records(const uint8_t* __restrict__ rec, const uint32_t
 size_t order_sort_temp_bytes(int64_t n) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, n);
     return bytes;
 }
 
@@ -322,7 +322,7 @@ void launch_reorder(const int32_t* lab, int64_t n, uint32_t p, uint32_t* keys_b,
     int end_bit = 1;
     while (end_bit < 32 && ((uint64_t)p >> end_bit) != 0) ++end_bit;
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, reinterpret_cast<const uint32_t*>(lab), keys_b, ids_a, order,
-                                    (int)n, 0, end_bit, s);
+                                    n, 0, end_bit, s);
     k_perm_inverse<<<grid, 256, 0, s>>>(order, n, perm);
     k_bucket_counts<<<(unsigned)((p + 255) / 256), 256, 0, s>>>(keys_b, n, p, counts);
     if (rec && out && width > 0) {

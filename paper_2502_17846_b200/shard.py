@@ -118,7 +118,9 @@ def partition_distributed(edges_ptr: int, num_edges: int, num_nodes: int, p: int
 
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    labels = torch.empty(int(num_nodes), dtype=torch.int32, device="cuda")
+    from .grem import _current_device
+    dev = _current_device()     # the native context's device (GREM_DEVICE / LOCAL_RANK), not torch's current one
+    labels = torch.empty(int(num_nodes), dtype=torch.int32, device=f"cuda:{dev}")
     partition_shard(edges_ptr, num_edges, num_nodes, p, config, rank, world, labels, edges_on_device)
     dev_ptr = int(edges_ptr)
     if not edges_on_device:
@@ -127,7 +129,7 @@ def partition_distributed(edges_ptr: int, num_edges: int, num_nodes: int, p: int
         dev_ptr = int(staged.value or 0)
     if world > 1:
         merge_labels(labels, group)
-        torch.cuda.synchronize()      # NCCL stream -> library stream
+        torch.cuda.synchronize(labels.device)      # NCCL stream -> library stream
     return labels, count_cuts_device(dev_ptr, num_edges, num_nodes, labels, p)
 
 

@@ -201,6 +201,10 @@ def load_layout(path: str):
     return FeatureLayout(record_width, perm, tuple((int(s), int(c)) for s, c in ext.reshape(num_parts, 2)))
 
 
+_REORDER_DEVICE_MAX_BYTES = int(os.environ.get("GREM_REORDER_DEVICE_MAX", str(1 << 30)))
+_REORDER_BLOCK_BYTES = 16 << 20   # store.py:226-231 streams 16 MB blocks
+
+
 def reorder_features(features_path: str, labels, record_width: int, out_path: str):
     """store.py:201-235 on the GPU: records regrouped by partition (ascending
     node id inside one), layout saved as ``<out>.layout``."""
@@ -215,15 +219,21 @@ def reorder_features(features_path: str, labels, record_width: int, out_path: st
         raise FormatError(f"{features_path}: length {size} != num_nodes {n} x width {record_width}")
     lab = np.ascontiguousarray(labels.astype(np.int32))
     p_guess = int(lab.max()) + 1 if n else 1
-    records = np.fromfile(features_path, dtype=np.uint8)
-    out = np.empty_like(records)
+    # small stores: records gathered on the device in one go; large ones
+    # (e.g. papers100M x 128 fp32 = 57 GB): only the permutation on the
+    # device, records streamed through bounded blocks of a memmap like the
+    # reference (store.py:226-231), so neither host RAM nor HBM holds a copy
+    streamed = size > _REORDER_DEVICE_MAX_BYTES
+    records = None if streamed else np.fromfile(features_path, dtype=np.uint8)
+    out = None if streamed else np.empty_like(records)
     perm = np.empty(max(n, 1), dtype=np.int64)
     counts = np.zeros(max(p_guess, 1), dtype=np.uint64)
     p_out = ctypes.c_int64()
     if n:
-        rc = _abi.lib().grem_reorder_records(context(), lab.ctypes.data, n, 0, records.ctypes.data, record_width,
-                                             out.ctypes.data, perm.ctypes.data, counts.ctypes.data, counts.size,
-                                             ctypes.byref(p_out))
+        rc = _abi.lib().grem_reorder_records(context(), lab.ctypes.data, n, 0,
+                                             None if streamed else records.ctypes.data, record_width,
+                                             None if streamed else out.ctypes.data, perm.ctypes.data,
+                                             counts.ctypes.data, counts.size, ctypes.byref(p_out))
         _raise(rc)
         p = int(p_out.value)
     else:
@@ -233,7 +243,17 @@ def reorder_features(features_path: str, labels, record_width: int, out_path: st
     if p > 1:
         np.cumsum(cnt[:-1], out=starts[1:])
     extents = tuple((int(s), int(c)) for s, c in zip(starts, cnt))
-    out.tofile(out_path)
+    if streamed:
+        order = np.empty(n, dtype=np.int64)          # slot -> node (perm: node -> slot)
+        order[perm[:n]] = np.arange(n, dtype=np.int64)
+        src = np.memmap(features_path, dtype=np.uint8, mode="r", shape=(n, record_width))
+        per = max(1, _REORDER_BLOCK_BYTES // record_width)
+        with open(out_path, "wb") as fh:
+            for lo in range(0, n, per):
+                fh.write(np.ascontiguousarray(src[order[lo:lo + per]]).tobytes())
+        del src
+    else:
+        out.tofile(out_path)
     layout = FeatureLayout(record_width, perm[:n].copy(), extents)
     _save_layout(layout, out_path + ".layout")
     return layout

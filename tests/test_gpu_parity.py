@@ -380,6 +380,15 @@ def test_file_ingest_pieces(tmp_path, golden_dir, monkeypatch):
                lambda: count_cuts(fb, lab)):
         with pytest.raises(FormatError):
             fn()
+    # the all-ones id (the usual -1 sentinel) must not wrap the bad-id record
+    bad2 = e.copy()
+    bad2[len(bad2) // 3] = (0xFFFFFFFF, 1)
+    fb2 = open_edge_file(write_grpe(tmp_path / "bad2.grpe", bad2, s.num_nodes))
+    for fn in (lambda: bisect(fb2, GremConfig(chunk_frac=0.1)),
+               lambda: partition(fb2, 4, GremConfig(chunk_frac=0.1), str(tmp_path / "w4")),
+               lambda: count_cuts(fb2, lab)):
+        with pytest.raises(FormatError, match="4294967295"):
+            fn()
     lab3, _ = partition(f, gs["k"], cfg, str(tmp_path / "w3"))
     assert np.array_equal(lab3, lab)
     assert count_cuts(f, lab) == rep   # grem_count_cuts_file

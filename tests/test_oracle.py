@@ -111,3 +111,13 @@ def test_oracle_known_answers(tmp_path):
     assert cut == 1
     with pytest.raises(oracle.OracleError):
         oracle.partition(np.array([[0, 1]]), 2, 3)
+
+
+def test_numpy_generator_matches_library_generator():
+    """oracle/gen_np.py (the reference arm's input, no product library) ==
+    the library's host generator (csrc/grem_gen.h), byte for byte."""
+    from oracle import gen_np
+    from paper_2502_17846_b200 import synth
+    for (n, m, beta, seed, e0) in [(10_000, 100_000, 11, 0, 0), (169_343, 50_000, 11, 0, 777),
+                                   (65_608_366, 40_000, 4, 0, 0), (111_059_956, 40_000, 11, 3, 10**9), (7, 1000, 11, 5, 0)]:
+        assert np.array_equal(gen_np.powerlaw_edges(n, m, beta, seed, e0), synth.powerlaw_edges(n, m, beta, seed, e0))

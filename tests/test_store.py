@@ -78,6 +78,18 @@ def test_gpu_store_equals_reference_golden(tmp_path, case):
     assert _sha(open(fout, "rb").read()) == case["features_out_sha256"]
     assert _sha(open(fout + ".layout", "rb").read()) == case["layout_sha256"]
     assert lay.num_nodes == n
+    # the streamed form (device permutation + bounded memmap blocks, used for
+    # stores above GREM_REORDER_DEVICE_MAX) writes the same bytes
+    import paper_2502_17846_b200.store as st
+    old = st._REORDER_DEVICE_MAX_BYTES, st._REORDER_BLOCK_BYTES
+    st._REORDER_DEVICE_MAX_BYTES, st._REORDER_BLOCK_BYTES = 0, 3 * case["record_width"]
+    try:
+        lay2 = store.reorder_features(str(fin), labels, case["record_width"], fout + "2")
+    finally:
+        st._REORDER_DEVICE_MAX_BYTES, st._REORDER_BLOCK_BYTES = old
+    assert _sha(open(fout + "2", "rb").read()) == case["features_out_sha256"]
+    assert _sha(open(fout + "2.layout", "rb").read()) == case["layout_sha256"]
+    assert lay2.num_nodes == n
 
 
 @pytest.mark.gpu
