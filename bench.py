@@ -195,7 +195,7 @@ def main():
             kernels += st["kernels"]
     barrier()
     wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-    grem.set_profiling(True)
+    grem.set_profiling(2)
     _, _, st_p = step_device()
     for name, (ms, cnt) in (st_p.pop("_phases", None) or grem.phase_times()).items():
         phases[name] = [ms * args.steps, cnt * args.steps]   # per-step figures below divide by steps
@@ -252,42 +252,54 @@ def main():
                "h2d_bytes_per_step": E * 8, "d2h_bytes_per_step": n * 4}
         del host
 
-    # roofline of the dominant HBM-streaming kernel, k_count_delta (one pass
-    # over a chunk's edges per fixpoint round; 9 algorithmic B/edge: 8 B edge
-    # read + 1 B label of the lower endpoint).  Its launches are timed with CUDA
-    # events on the library stream in a level-0 bisection (k=2: one stream, no
-    # concurrent sibling subtrees), right after the timed steps.
+    # Roofline.  Lead: the whole path, SURVEY.md 8(d) algorithmic bytes of the
+    # step (grem_stats.path_bytes) / step time.  Rows: the top kernels by
+    # share of the step, each timed with CUDA events on the library stream
+    # around its launches (kernel marks, profiling level 2) in a level-0
+    # bisection (k=2: one stream, no concurrent sibling subtrees), achieved =
+    # the kernel's algorithmic bytes per launch / its average
+    # launch time; traffic = ncu DRAM bytes per launch of this build
+    # (profiles/r02_traffic.json) when captured.
     peak, peak_kind = measured_peak()
-    top = {kk: v for kk, v in phases.items() if "." not in kk}
-    roof = None
-    grem.set_profiling(True)
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    grem.set_profiling(2)
     grem.partition_edges(None, n, 2, cfg, on_device_ptr=dptr.value, num_edges=E)
-    st_l0, ph_l0 = grem.last_stats(), grem.phase_times()
+    ph_l0, by_l0 = grem.phase_times(), grem.phase_bytes()
     grem.set_profiling(False)
-    d_ms, d_n = ph_l0.get("count_delta", (0.0, 0))
-    if d_ms > 0 and d_n > 0:
-        achieved = st_l0["delta_bytes"] / (d_ms / 1e3) / 1e9
-        traffic = None
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r01b_traffic.json")))["k_count_delta"]
-            traffic = tr["dram_bytes_per_launch"]
-        except Exception:  # noqa: BLE001
-            pass
-        roof = {"bound": "hbm", "kernel": "k_count_delta", "achieved": achieved, "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": st_l0["delta_bytes"] / d_n, "launches_timed": d_n,
-                "avg_launch_ms": d_ms / d_n, "timed_in": f"{args.workload} level-0 bisection (k=2), CUDA events",
-                "share_of_step": top.get("count_delta", (0.0, 0))[0] / max(1e-9, sum(v[0] for v in top.values()))}
+    step_ms_sum = sum(v[0] for kk, v in phases.items() if "." not in kk) or 1e-9
+    rows = []
+    for kk, (ms_l0, cnt_l0) in ph_l0.items():
+        if not kk.startswith("k.") or cnt_l0 <= 0 or ms_l0 <= 0 or by_l0.get(kk, 0) <= 0:
+            continue
+        kname = "k_" + kk[2:]
+        ach = by_l0[kk] / (ms_l0 / 1e3) / 1e9
+        tr = traffic.get(kname, {})
+        rows.append({"kernel": kname, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "algorithmic_bytes_per_launch": by_l0[kk] / cnt_l0, "avg_launch_ms": ms_l0 / cnt_l0,
+                     "launches_timed": cnt_l0,
+                     "traffic": tr.get("dram_bytes_per_launch"), "traffic_source": tr.get("source"),
+                     "share_of_step": phases.get(kk, (0.0, 0))[0] / step_ms_sum})
+    rows.sort(key=lambda r: -r["share_of_step"])
     path_bytes = st.get("path_bytes")
-    roof_path = None
+    roof = None
     if path_bytes:
         ach = path_bytes / (ms_step / 1e3) / 1e9
-        roof_path = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "algorithmic_bytes_per_step": path_bytes, "formula": "SURVEY.md 8(d)"}
+        roof = {"bound": "hbm", "kernel": "whole path (partition to k)", "achieved": ach, "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": ach / peak,
+                "traffic": (traffic.get("step", {}) or {}).get("dram_bytes"),
+                "traffic_source": (traffic.get("step", {}) or {}).get("source"),
+                "algorithmic_bytes_per_step": path_bytes, "formula": "SURVEY.md 8(d): per level 8E+2E+34V, "
+                "+10E_l+8E_(l+1) per extraction, +10E final cut",
+                "kernels": rows[:3], "kernels_timed_in": f"{args.workload} level-0 bisection (k=2), CUDA events",
+                "kernel_share_from": "kernel marks in the profiled k-way step (sum of kernel times across streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_port(shape)
+        cpu = cpu_baseline_port(args.workload, k)
 
     if rank == 0:
         out = {
@@ -296,14 +308,10 @@ def main():
             "ms_per_step": ms_step, "wall_ms_per_step": wall_ms, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.workload}-shaped power-law k={k}", "num_nodes": n, "num_edges": E,
-                       "k": k, "chunk_frac": 0.1, "capacity_slack": 0.0, "refine": True, "passes": 1,
-                       "seed": "bfs_grow/2", "parallelism": (f"subtree-sharded x{world}" if sharded else
-                                       f"replicas x{world}" if world > 1 else "single"),
-                       "l2": "inputs larger than L2 (edge list %.1f GB)" % (E * 8 / 1e9)},
+            "config": bench_config(args.workload, k, world, sharded),
             "report": {"cut_edges": rep.cut_edges, "cut_fraction": rep.cut_fraction,
                        "balance_ratio": rep.balance_ratio, "labels_sha256": labels_sha},
-            "e2e": e2e, "roofline": roof, "roofline_path": roof_path, "cpu_baseline": cpu,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": kernels, "clocks": sampler.summary(),
             "phases_ms_per_step": {kk: round(v[0] / args.steps, 3) for kk, v in sorted(phases.items())},
             "phases_note": "one extra step with the phase profiler on (CUDA events per launch group; sums of concurrent subtrees exceed the step)",
@@ -315,53 +323,101 @@ def main():
     return 0
 
 
-def cpu_baseline_port(shape):
+# Shapes of paper_2502_17846_b200/synth.SHAPES (tests/test_host.py checks the
+# two tables agree), repeated here so the reference arm never imports the
+# product package: (num_nodes, num_edges, default k, generator beta, seed)
+SHAPES = {
+    "tiny": (10_000, 100_000, 4, 11, 0),
+    "arxiv": (169_343, 1_166_243, 8, 11, 0),
+    "products": (2_449_029, 61_859_140, 16, 11, 0),
+    "papers100m": (111_059_956, 1_615_685_872, 16, 11, 0),
+    "friendster": (65_608_366, 1_806_067_135, 16, 4, 0),
+}
+
+
+def bench_config(workload, k, world, sharded):
+    """The workload; identical for both arms (the reference arm's bounded
+    sample is described in its cpu_baseline.sample)."""
+    n, E = SHAPES[workload][:2]
+    return {"workload": f"{workload}-shaped power-law k={k}", "num_nodes": n, "num_edges": E,
+            "k": k, "chunk_frac": 0.1, "capacity_slack": 0.0, "refine": True, "passes": 1,
+            "seed": "bfs_grow/2", "parallelism": (f"subtree-sharded x{world}" if sharded else
+                                                  f"replicas x{world}" if world > 1 else "single"),
+            "l2": "inputs larger than L2 (edge list %.1f GB)" % (E * 8 / 1e9)}
+
+
+def _golden_full_run(workload, k):
+    """The committed same-config single-thread run of the C restatement
+    (tests/golden/golden_shapes.json, measured in the build container)."""
+    try:
+        gs = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_shapes.json")))
+        g = gs.get(f"{workload}_k{k}") or {}
+        sec = g.get("oracle_seconds") or g.get("reference_seconds") or g.get("seconds")
+        if not sec or g.get("chunk_frac", 0.1) != 0.1:
+            return None
+        who = ("streamcut itself (pure Python)" if "reference_seconds" in g else
+               "C restatement oracle/grem_oracle.c (bit-exact with streamcut)")
+        return {"value": g["num_edges"] / sec, "unit": "edges/s", "cores": 1, "seconds": sec,
+                "source": f"tests/golden/golden_shapes.json[{workload}_k{k}]: {who}, full graph, 1 core, "
+                          "build container (Intel Xeon), not this host"}
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def cpu_baseline_port(workload, k):
     """The C restatement (oracle/, single thread) on a bounded sample of the
-    same workload: a 1/100-scale graph of the same shape family (same
-    generator, same average degree), partitioned to the same k."""
-    from oracle import oracle
-    from paper_2502_17846_b200 import synth
-    # ~1.5-2 M edges/s single-thread: size the sample for ~10-30 s of CPU work
-    scale = max(1, shape.num_edges // 30_000_000)
-    n = max(1000, shape.num_nodes // scale)
-    m = max(10000, shape.num_edges // scale)
-    e = synth.powerlaw_edges(n, m, beta=shape.beta, seed=shape.seed)
+    same workload on this host: a 1/scale graph of the same shape family (same
+    generator, same average degree), partitioned to the same k; plus the
+    committed full-size run of the same config."""
+    from oracle import gen_np, oracle
+    n0, m0, _, beta, seed = SHAPES[workload]
+    # ~0.5-4 M edges/s single-thread: size the sample for ~10-30 s of CPU work
+    scale = max(1, m0 // 30_000_000)
+    n = max(1000, n0 // scale)
+    m = max(10000, m0 // scale)
+    e = gen_np.powerlaw_edges(n, m, beta=beta, seed=seed)
     t = time.perf_counter()
-    oracle.partition(e, n, shape.k, chunk_frac=0.1)
+    oracle.partition(e, n, k, chunk_frac=0.1)
     dt = time.perf_counter() - t
     return {"value": m / dt, "unit": "edges/s", "cores": 1, "kind": "port",
-            "sample": f"{shape.name}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator), k={shape.k}, "
-                      f"C restatement of streamcut (oracle/grem_oracle.c, bit-exact), {dt:.1f} s"}
+            "sample": f"{workload}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator), k={k}, "
+                      f"C restatement of streamcut (oracle/grem_oracle.c, bit-exact), {dt:.1f} s on this host",
+            "same_config": _golden_full_run(workload, k)}
 
 
 def run_reference_arm(args):
     """--impl reference: the reference's own CPU implementation (streamcut,
-    pure Python, from baseline/_ref) on a bounded sample of the workload on
-    this host; falls back to the C restatement if streamcut is absent."""
+    pure Python, single-threaded by construction, from baseline/_ref) on a
+    bounded sample of the workload on this host.  The input comes from the
+    numpy restatement of the generator (oracle/gen_np.py): nothing of the
+    product package or its library is loaded in this arm."""
     import tempfile
 
     import numpy as np
 
-    from paper_2502_17846_b200 import synth
-    shape = synth.SHAPES[args.workload]
-    k = args.k or shape.k
-    scale = 1000 if shape.num_edges > 100_000_000 else 10
-    n = max(1000, shape.num_nodes // scale)
-    m = max(10000, shape.num_edges // scale)
-    e = synth.powerlaw_edges(n, m, beta=shape.beta, seed=shape.seed)
+    from oracle import gen_np
+    workload = args.workload
+    n0, m0, k0, beta, seed = SHAPES[workload]
+    k = args.k or k0
+    scale = 1000 if m0 > 100_000_000 else 10
+    n = max(1000, n0 // scale)
+    m = max(10000, m0 // scale)
+    e = gen_np.powerlaw_edges(n, m, beta=beta, seed=seed)
     ref_dir = os.path.join(ROOT, "baseline", "_ref")
     if os.path.isdir(ref_dir):
         sys.path.insert(0, ref_dir)
     try:
         import streamcut
-        from streamcut import GremConfig, open_edge_file
+        from streamcut import BinaryEdgeWriter, GremConfig, open_edge_file
         kind = "reference"
     except Exception:  # noqa: BLE001
         streamcut = None
         kind = "port"
     tmp = tempfile.mkdtemp()
     path = os.path.join(tmp, "g.grpe")
-    synth.write_grpe(path, e, n)
+    if streamcut is not None:
+        with BinaryEdgeWriter(path, n) as w:
+            w.write(e.astype(np.int64))
     times = []
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
@@ -374,13 +430,14 @@ def run_reference_arm(args):
             times.append(time.perf_counter() - t)
     dt = sum(times) / len(times)
     value = m / dt
-    sample = (f"{shape.name}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator), k={k}, "
-              f"{'streamcut (pure Python, single thread)' if kind == 'reference' else 'C restatement'}")
+    sample = (f"{workload}-shaped 1/{scale} scale ({n} nodes, {m} edges, same generator via oracle/gen_np.py), "
+              f"k={k}, {'streamcut (pure Python, single thread)' if kind == 'reference' else 'C restatement'}; "
+              f"{dt:.2f} s per partition")
     out = {"impl": "reference", "metric": "GREM edges/s (partition to k, bit-equal labels/edge-cut)",
            "value": value, "unit": "edges/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "u32/f64", "data": "synthetic",
-           "config": {"workload": f"{args.workload}-shaped power-law k={k}", "sample_scale": f"1/{scale}"},
+           "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+           "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+           "config": bench_config(workload, k, args.gpus, args.gpus > 1 and not args.replicas),
            "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": kind, "sample": sample},
            "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))

@@ -105,6 +105,10 @@ int grem_get_stats(grem_ctx* ctx, grem_stats* out);
  * when profiling is on.  Returns the number of phases; fills up to `cap`. */
 int grem_set_profiling(grem_ctx* ctx, int on);
 int grem_get_phase_times(grem_ctx* ctx, double* ms_out, int64_t* count_out, int cap, const char** names_out);
+/* Algorithmic bytes of the kernel-level phases ("k.*", profiling level 2:
+ * grem_set_profiling(ctx, 2)), same order as grem_get_phase_times; 0 for
+ * phases without a byte model.  Returns the number of phases. */
+int grem_get_phase_bytes(grem_ctx* ctx, double* bytes_out, int cap);
 
 /* --------------------------------------------------------------- the path */
 

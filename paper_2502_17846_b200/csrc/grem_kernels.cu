@@ -1023,9 +1023,15 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
         k_round_fused<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, fb, o, first_round);
         return;
     }
+    // kernel marks on full rounds only (incremental rounds skip clean tiles,
+    // so their per-launch bytes are not the per-node figure)
+    if (!incremental) kmark(KM_ROUND_REDUCE, 1, s);
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
+    if (!incremental) kmark(KM_ROUND_REDUCE, 0, s);
     k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
+    if (!incremental) kmark(KM_ROUND_DOWN, 1, s);
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
+    if (!incremental) kmark(KM_ROUND_DOWN, 0, s);
 }
 
 // ------------------------------------------------------- trajectory bundles
@@ -3242,13 +3248,19 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
     cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
     cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
     cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
+    kmark(KM_BIN_HIST, 1, s);
     k_bin_hist<<<G, kScatT, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
+    kmark(KM_BIN_HIST, 0, s);
     exclusive_sum_i32(bb.hist, bb.offs, (int64_t)(bb.nbins + 1) * G, temp, temp_bytes, s);
+    kmark(KM_BIN_SCATTER, 1, s);
     k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
                                                bb.hub_cnt, bb.hub_flag);
+    kmark(KM_BIN_SCATTER, 0, s);
+    kmark(KM_BIN_COMPACT, 1, s);
     k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.offs, G, bb.shift, n, b.hub_keys,
                                                            bb.hub_cnt, bb.hub_flag, refine, b, bb.status,
                                                            bb.ticket, ntiles);
+    kmark(KM_BIN_COMPACT, 0, s);
 }
 int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * num_sms(); }
 int binned_shift(int64_t n) {

@@ -9,6 +9,13 @@
 
 namespace grem {
 
+// Kernel-level timing marks (bench.py's roofline rows): the runtime records a
+// CUDA event pair around the marked launches when kernel profiling is on
+// (grem_set_profiling(ctx, 2)); a no-op otherwise.  Ids index the runtime's
+// kernel phases (KM_* -> "k.<name>").
+enum KMark { KM_BIN_HIST = 0, KM_BIN_SCATTER, KM_BIN_COMPACT, KM_ROUND_REDUCE, KM_ROUND_DOWN, KM_COUNT_DELTA, KM_N };
+void kmark(int km, int begin, cudaStream_t s);
+
 // Hub privatisation (power-law hubs would serialise the counter atomics):
 // up to kMaxHubs high-degree nodes, found per bisection by sampling, live in
 // an open-addressing table (kHubSlots u32 keys, empty = kHubEmpty); edge

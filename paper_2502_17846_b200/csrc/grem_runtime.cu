@@ -90,11 +90,14 @@ enum Phase {
     PH_COUNT = 0, PH_SELECT, PH_NODE, PH_DELTA, PH_SCAN, PH_BUNDLE, PH_COMMIT,
     PH_SEED, PH_FILL, PH_EXTRACT, PH_CUTS, PH_INGEST, PH_HUBS,
     PH_SEED_CSR, PH_SEED_CC, PH_SEED_BFS, PH_SEED_REFINE, PH_SEED_COMMIT,   // inside "seed"
-    PH_N
+    PH_K0,   // kernel-level marks (grem_set_profiling(ctx, 2)): PH_K0 + KM_*
+    PH_N = PH_K0 + KM_N
 };
 static const char* kPhaseNames[PH_N] = {"count_init", "select", "node_init", "count_delta", "scan", "bundle",
                                         "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs",
-                                        "seed.csr", "seed.cc", "seed.bfs", "seed.refine", "seed.commit"};
+                                        "seed.csr", "seed.cc", "seed.bfs", "seed.refine", "seed.commit",
+                                        "k.bin_hist", "k.bin_scatter", "k.bin_compact", "k.round_reduce",
+                                        "k.round_down", "k.count_delta"};
 
 struct grem_ctx {
     int device = 0;
@@ -110,6 +113,8 @@ struct grem_ctx {
     size_t ev_used = 0;
     double phase_ms[PH_N] = {0};
     long long phase_n[PH_N] = {0};
+    double phase_bytes[PH_N] = {0};   // algorithmic bytes of the kernel phases
+    cudaEvent_t kmark_open[KM_N] = {};
     cudaStream_t s = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // per node
@@ -287,6 +292,18 @@ void prof_collect(grem_ctx* c) {
     }
     c->prof_open.clear();
     c->ev_used = 0;
+}
+
+thread_local grem_ctx* tl_ctx = nullptr;   // the context whose bisection runs on this host thread
+
+struct CtxBind {   // binds tl_ctx for the kernel marks of one bisection
+    grem_ctx* prev;
+    explicit CtxBind(grem_ctx* c) : prev(tl_ctx) { tl_ctx = c; }
+    ~CtxBind() { tl_ctx = prev; }
+};
+
+void kbytes(grem_ctx* c, int km, double bytes) {
+    if (c->profiling == 2) c->phase_bytes[PH_K0 + km] += bytes;
 }
 
 void ensure_nodes(grem_ctx* c, int64_t n) {
@@ -653,9 +670,17 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         launch_select_nodes(c->flag.p, c->cnt.p, a.n, c->nodes.p, c->d_scal, c->temp.p, c->temp.cap, s);
         c->kernels += 2;
     }
-    scal_read(c, c->d_scal, 1);
+    scal_read(c, c->d_scal, 3);
     int64_t nc = c->h_pin[0];
+    // refined (previously assigned) chunk nodes: the binned compact leaves the
+    // new-member count in scal[2]; only needed for the kernel byte counters
+    int64_t refined = binned ? nc - c->h_pin[2] : nc;
     c->stats.visits += nc;
+    if (binned) {
+        kbytes(c, KM_BIN_HIST, 8.0 * mc);              // edge read
+        kbytes(c, KM_BIN_SCATTER, 16.0 * mc);          // edge read + two 4-byte records out
+        kbytes(c, KM_BIN_COMPACT, 8.0 * mc + 38.0 * nc + 16.0 * refined + (double)a.n);   // records in, state out, nbr + lab in
+    }
     if (!binned) {   // (the binned path wrote the compact state and newb already)
         PhaseScope ps(c, PH_NODE);
         launch_node_init(b, nc, a.refine, s);
@@ -695,13 +720,20 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             ChunkBufs bd = b;      // the previous round's changes
             bd.chg = chgbuf[(r - 1) & 1];
             bd.chgc = chgcbuf[(r - 1) & 1];
+            kmark(KM_COUNT_DELTA, 1, s);
             launch_count_delta(e, mc, bd, s);
+            kmark(KM_COUNT_DELTA, 0, s);
+            kbytes(c, KM_COUNT_DELTA, 9.0 * mc);   // 8 B edge read + 1 B lower-endpoint label
             c->kernels++;
         }
         {
             PhaseScope ps(c, PH_SCAN);
             launch_round_scan(b, nc, a.cap, r == 1, incr_on && r >= 3, s);
             c->kernels += 3;
+            if (!(incr_on && r >= 3)) {   // full rounds (the marked launches), DESIGN.md §5
+                kbytes(c, KM_ROUND_REDUCE, 14.0 * nc + 16.0 * refined);   // meta r/w, newb, cnt; nbr of refined nodes
+                kbytes(c, KM_ROUND_DOWN, 20.0 * nc);   // meta, newb, nodes, tlc in; x, xalt, meta, tlc out
+            }
         }
         {
             // exact repair by trajectory bundles, gated on the device by the
@@ -813,6 +845,19 @@ struct Meter {
 
 }  // namespace
 
+void grem::kmark(int km, int begin, cudaStream_t s) {
+    grem_ctx* c = tl_ctx;
+    if (!c || c->profiling != 2 || s != c->s) return;
+    cudaEvent_t e = prof_event(c);
+    cudaEventRecord(e, s);
+    if (begin) {
+        c->kmark_open[km] = e;
+    } else if (c->kmark_open[km]) {
+        c->prof_open.push_back({PH_K0 + km, {c->kmark_open[km], e}});
+        c->kmark_open[km] = nullptr;
+    }
+}
+
 // Bucketised cuckoo insertion (2 buckets x 2 slots per key); a key that is
 // still homeless after the displacement budget drops out of the hub set
 // (hubs only change performance, never results).
@@ -896,6 +941,7 @@ cudaEvent_t g_dbg_t0 = nullptr;   // GREM_DEBUG_LEVELS timeline origin
 // bisect (grem.py:192-224) on device-resident edges; leaves labels in c->lab
 void bisect_core(grem_ctx* c, const BisectArgs& a) {
     cudaStream_t s = c->s;
+    CtxBind bind(c);
     static const char* dbg_levels = getenv("GREM_DEBUG_LEVELS");
     cudaEvent_t lv0 = nullptr, lv1 = nullptr;
     int64_t r0 = c->stats.rounds, v0 = c->stats.visits, b0 = c->stats.walk_steps;
@@ -1454,6 +1500,7 @@ grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
     for (int k = 0; k < PH_N; ++k) {
         ch->phase_ms[k] = 0;
         ch->phase_n[k] = 0;
+        ch->phase_bytes[k] = 0;
     }
     ch->prof_open.clear();
     ch->ev_used = 0;
@@ -1480,6 +1527,7 @@ void ctx_release(grem_ctx* parent, grem_ctx* ch) {
     for (int k = 0; k < PH_N; ++k) {
         parent->phase_ms[k] += ch->phase_ms[k];
         parent->phase_n[k] += ch->phase_n[k];
+        parent->phase_bytes[k] += ch->phase_bytes[k];
     }
 }
 
@@ -1720,6 +1768,7 @@ int guarded(grem_ctx* c, F f) {
             for (int k = 0; k < PH_N; ++k) {
                 c->phase_ms[k] = 0;
                 c->phase_n[k] = 0;
+                c->phase_bytes[k] = 0;
             }
             c->prof_open.clear();
             c->ev_used = 0;
@@ -1839,7 +1888,7 @@ void grem_destroy(grem_ctx* c) {
 
 int grem_set_profiling(grem_ctx* c, int on) {
     if (!c) return GREM_E_FORMAT;
-    c->profiling = on ? 1 : 0;
+    c->profiling = on >= 2 ? 2 : (on ? 1 : 0);
     return GREM_OK;
 }
 
@@ -1851,6 +1900,13 @@ int grem_get_phase_times(grem_ctx* c, double* ms_out, int64_t* count_out, int ca
         if (count_out) count_out[k] = c->phase_n[k];
         if (names_out) names_out[k] = kPhaseNames[k];
     }
+    return PH_N;
+}
+
+int grem_get_phase_bytes(grem_ctx* c, double* bytes_out, int cap) {
+    if (!c) return GREM_E_FORMAT;
+    int n = cap < PH_N ? cap : PH_N;
+    for (int k = 0; k < n && bytes_out; ++k) bytes_out[k] = c->phase_bytes[k];
     return PH_N;
 }
 

@@ -308,9 +308,10 @@ def partition_edges(edges, num_nodes: int, p: int, config, on_device_ptr: int | 
     return labels, _report(n, rep, sizes)
 
 
-def set_profiling(on: bool = True) -> None:
-    """Per-phase CUDA-event timing of subsequent calls (see phase_times())."""
-    _abi.lib().grem_set_profiling(context(), 1 if on else 0)
+def set_profiling(on=True) -> None:
+    """Per-phase CUDA-event timing of subsequent calls (see phase_times());
+    ``on=2`` adds the kernel-level marks ("k.*") and their algorithmic bytes."""
+    _abi.lib().grem_set_profiling(context(), 2 if on == 2 else (1 if on else 0))
 
 
 def phase_times() -> dict:
@@ -321,6 +322,16 @@ def phase_times() -> dict:
     names = (ctypes.c_char_p * 32)()
     n = L.grem_get_phase_times(context(), ms, cnt, 32, names)
     return {names[k].decode(): (ms[k], cnt[k]) for k in range(n)}
+
+
+def phase_bytes() -> dict:
+    """{kernel phase: algorithmic bytes} of the last call (profiling level 2)."""
+    L = _abi.lib()
+    by = (ctypes.c_double * 32)()
+    names = (ctypes.c_char_p * 32)()
+    n = L.grem_get_phase_times(context(), None, None, 32, names)
+    L.grem_get_phase_bytes(context(), by, 32)
+    return {names[k].decode(): by[k] for k in range(n) if by[k] > 0}
 
 
 def count_cuts_edges(edges, num_nodes: int, labels):

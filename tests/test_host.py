@@ -169,3 +169,35 @@ def test_node_maps_match_assign_exhaustive():
                                     assert apply(f, x) == xn
                             continue
                         assert apply(f, x) == xn
+
+
+def test_bench_shapes_match_package_shapes():
+    import bench
+    from paper_2502_17846_b200 import synth
+    for name, s in synth.SHAPES.items():
+        assert bench.SHAPES[name] == (s.num_nodes, s.num_edges, s.k, s.beta, s.seed)
+
+
+def test_reference_arm_loads_no_product_code():
+    """bench.py --impl reference: streamcut on a bounded sample whose input
+    comes from the numpy generator; the product package and its .so are never
+    loaded (the arm's native_so_loaded listed libgrem_b200.so)."""
+    import subprocess
+    import sys
+    code = r'''
+import io, json, os, sys, contextlib
+sys.argv = ["bench.py", "--impl", "reference", "--workload", "tiny", "--steps", "1", "--warmup", "0"]
+import bench
+buf = io.StringIO()
+with contextlib.redirect_stdout(buf):
+    bench.main()
+line = json.loads(buf.getvalue().strip().splitlines()[-1])
+maps = open("/proc/self/maps").read()
+assert "libgrem_b200" not in maps, "product library loaded"
+assert not any(m.startswith("paper_2502_17846_b200") for m in sys.modules), "product package imported"
+assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["k"] == 4
+print("ok", line["cpu_baseline"]["kind"])
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -42,6 +42,8 @@ def _run(files, extra=(), swap_support="1"):
     tail = (r.stdout + r.stderr)[-6000:]
     assert r.returncode == 0, tail
     assert "swapped for paper_2502_17846_b200" in r.stdout, tail
+    summary = [ln for ln in r.stdout.splitlines() if " passed" in ln or " failed" in ln]
+    print(f"[reference suite] {' '.join(files)}: {summary[-1] if summary else '?'}")
     return r.stdout
 
 
