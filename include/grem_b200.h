@@ -109,6 +109,11 @@ int grem_get_phase_times(grem_ctx* ctx, double* ms_out, int64_t* count_out, int 
  * grem_set_profiling(ctx, 2)), same order as grem_get_phase_times; 0 for
  * phases without a byte model.  Returns the number of phases. */
 int grem_get_phase_bytes(grem_ctx* ctx, double* bytes_out, int cap);
+/* High-water marks (bytes) of the device memory pool all library workspaces
+ * come from (cudaMemPoolAttrUsedMemHigh / ReservedMemHigh of the device's
+ * default pool); reset != 0 restarts them.  Buffers the caller allocated with
+ * grem_device_alloc (plain cudaMalloc) are not included. */
+int grem_mem_high_water(grem_ctx* ctx, int64_t* used_high, int64_t* reserved_high, int reset);
 
 /* --------------------------------------------------------------- the path */
 

@@ -1903,6 +1903,25 @@ int grem_get_phase_times(grem_ctx* c, double* ms_out, int64_t* count_out, int ca
     return PH_N;
 }
 
+int grem_mem_high_water(grem_ctx* c, int64_t* used_high, int64_t* reserved_high, int reset) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {   // (no per-call stats reset)
+        CK(cudaSetDevice(c->device));
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+        unsigned long long u = 0, r = 0;
+        CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &u));
+        CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &r));
+        if (used_high) *used_high = (int64_t)u;
+        if (reserved_high) *reserved_high = (int64_t)r;
+        if (reset) {
+            unsigned long long z = 0;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &z));
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &z));
+        }
+    });
+}
+
 int grem_get_phase_bytes(grem_ctx* c, double* bytes_out, int cap) {
     if (!c) return GREM_E_FORMAT;
     int n = cap < PH_N ? cap : PH_N;
