@@ -751,9 +751,11 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     __shared__ Clamp smem[kRT / 32];
     __shared__ long long sbad, sfirst;
     __shared__ int sspec;
+    __shared__ unsigned int s_nbad, s_ch;   // block totals: one global atomic per tile, not per warp
     if (threadIdx.x == 0) {
         sbad = sfirst = kInf;
         sspec = 0;
+        s_nbad = s_ch = 0u;
     }
     int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)threadIdx.x * kRI;
     if (a.incremental && !a.dcur[blockIdx.x] && (long long)out.x[(int64_t)blockIdx.x * kRTile] == tile_x[blockIdx.x]) {
@@ -823,13 +825,17 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     if (mybad != kInf) atomicMin(&sbad, mybad);
     if (mybad_ch != kInf) atomicMin(&sfirst, mybad_ch);
     if ((threadIdx.x & 31) == 0) {
-        if (nbad) atomicAdd((unsigned long long*)(out.scal + 4), (unsigned long long)nbad);
-        if (ch) atomicAdd((unsigned long long*)(out.scal + 1), (unsigned long long)ch);
+        if (nbad) atomicAdd(&s_nbad, (unsigned int)nbad);
+        if (ch) atomicAdd(&s_ch, (unsigned int)ch);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && sbad != kInf) atomicMin(out.scal + 6, sbad);
-    if (threadIdx.x == 0 && sfirst != kInf) atomicMin(out.scal + 9, sfirst);   // first changed decision
-    if (threadIdx.x == 0 && sspec) a.dnext[blockIdx.x] = 1;
+    if (threadIdx.x == 0) {
+        if (s_nbad) atomicAdd((unsigned long long*)(out.scal + 4), (unsigned long long)s_nbad);
+        if (s_ch) atomicAdd((unsigned long long*)(out.scal + 1), (unsigned long long)s_ch);
+        if (sbad != kInf) atomicMin(out.scal + 6, sbad);
+        if (sfirst != kInf) atomicMin(out.scal + 9, sfirst);   // first changed decision
+        if (sspec) a.dnext[blockIdx.x] = 1;
+    }
 }
 
 // ---- single-pass round (GREM_ROUND_FUSED=1; off by default: measured no faster): preferences, tile
@@ -2905,14 +2911,15 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned int s_hist[kMaxBins];
     hub_load(s_keys, hub_keys);
-    for (int k = threadIdx.x; k < nbins; k += kScatT) s_hist[k] = 0;
+    const int bd = blockDim.x;   // 1024 (GREM_SCATTER_V1) or 512: the scatter's CTA decomposition
+    for (int k = threadIdx.x; k < nbins; k += bd) s_hist[k] = 0;
     __syncthreads();
     int64_t lo, hi;
     cta_range(m, lo, hi);
-    for (int64_t i = lo + threadIdx.x; i < hi; i += 4 * kScatT) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += 4 * bd) {
         uint2 ed[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ed[j] = i + j * kScatT < hi ? __ldcs(e + i + j * kScatT) : make_uint2(kHubEmpty, kHubEmpty);
+        for (int j = 0; j < 4; ++j) ed[j] = i + j * bd < hi ? __ldcs(e + i + j * bd) : make_uint2(kHubEmpty, kHubEmpty);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (ed[j].x == kHubEmpty) continue;
@@ -2921,7 +2928,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
         }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k <= nbins; k += kScatT)
+    for (int k = threadIdx.x; k <= nbins; k += bd)
         hist[(int64_t)k * gridDim.x + blockIdx.x] = k < nbins ? (int32_t)s_hist[k] : 0;   // row nbins: total
 }
 
@@ -3063,6 +3070,146 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         }
     }
     for (int k = t; k < kHubSlots; k += kScatT) {
+        if (s_keys[k] == kHubEmpty) continue;
+        if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
+        if (s_hflag[k]) hub_flag[k] = 1u;
+    }
+}
+
+// ---- scatter, second form (default; GREM_SCATTER_V1=1 selects the one above):
+// 512-thread CTAs, two per SM (the block-wide sync phases of one CTA overlap
+// the other's loads), 4096-edge batches and no open-sector carry: a bin's
+// partial 32-byte sector is completed by this CTA's next run of the bin within
+// a few batches, while the line is still in L2 (the open sectors of all CTAs
+// are ~8 MB), so the carry's extra shared-memory traffic bought nothing.
+constexpr int kScat2T = 512;
+constexpr int kScat2IPT = 8;
+constexpr int kScat2Batch = kScat2T * kScat2IPT;   // edges per batch, <= 2 records each
+constexpr int kScat2BPT = kMaxBins / kScat2T;      // bins per thread in the batch scan
+constexpr size_t kScat2Smem = (size_t)kHubSlots * (8 + 4 + 4) + (size_t)kMaxBins * 4 * 3 + (size_t)2 * kScat2Batch * 4 + 64 * 4;
+static_assert(kScat2BPT * kScat2T == kMaxBins, "bins per thread");
+
+__global__ void __launch_bounds__(kScat2T, 2) k_bin_scatter2(const uint2* __restrict__ e, int64_t m,
+                                                            const uint32_t* __restrict__ lab2,
+                                                            const uint32_t* __restrict__ hub_keys, int shift, int nbins,
+                                                            const int32_t* __restrict__ offs,
+                                                            uint32_t* __restrict__ recs,
+                                                            unsigned long long* __restrict__ hub_cnt,
+                                                            uint32_t* __restrict__ hub_flag) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* s_hcnt = reinterpret_cast<unsigned long long*>(smem_raw);
+    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_hcnt + kHubSlots);
+    uint32_t* s_hflag = s_keys + kHubSlots;
+    unsigned int* s_hist = s_hflag + kHubSlots;
+    unsigned int* s_start = s_hist + kMaxBins;
+    unsigned int* s_cur = s_start + kMaxBins;
+    uint32_t* s_out = s_cur + kMaxBins;
+    unsigned int* s_w = s_out + 2 * kScat2Batch;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    hub_load(s_keys, hub_keys);
+    for (int k = t; k < kHubSlots; k += kScat2T) {
+        s_hcnt[k] = 0ULL;
+        s_hflag[k] = 0u;
+    }
+    for (int k = t; k < nbins; k += kScat2T) s_cur[k] = (unsigned int)offs[(int64_t)k * gridDim.x + blockIdx.x];
+    int64_t lo, hi;
+    cta_range(m, lo, hi);
+    for (int64_t b0 = lo; b0 < hi; b0 += kScat2Batch) {
+        for (int k = t; k < nbins; k += kScat2T) s_hist[k] = 0u;
+        uint2 ed[kScat2IPT];
+#pragma unroll
+        for (int k = 0; k < kScat2IPT; ++k) {
+            int64_t i = b0 + (int64_t)k * kScat2T + t;
+            ed[k] = i < hi ? __ldcs(e + i) : make_uint2(kHubEmpty, kHubEmpty);
+        }
+        __syncthreads();
+        uint32_t rec[2 * kScat2IPT], rk[2 * kScat2IPT];
+#pragma unroll
+        for (int k = 0; k < kScat2IPT; ++k) {
+            rec[2 * k] = 0xFFFFFFFFu;
+            rec[2 * k + 1] = 0xFFFFFFFFu;
+            uint32_t u = ed[k].x, v = ed[k].y;
+            if (u != kHubEmpty) {
+                int hu = hub_find(s_keys, u);
+                if (u == v) {   // self-loop: u is a chunk node, no count (model.py:53-55)
+                    if (hu >= 0) s_hflag[hu] = 1u;
+                    else rec[2 * k] = (u << 2) | 3u;
+                } else {
+                    int hv = hub_find(s_keys, v);
+                    uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
+                    if (hu >= 0) {
+                        if (cv) atomicAdd(&s_hcnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
+                        else s_hflag[hu] = 1u;
+                    } else {
+                        rec[2 * k] = (u << 2) | cv;
+                    }
+                    if (hv >= 0) {
+                        if (cu) atomicAdd(&s_hcnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
+                        else s_hflag[hv] = 1u;
+                    } else {
+                        rec[2 * k + 1] = (v << 2) | cu;
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (rec[2 * k + h] != 0xFFFFFFFFu) rk[2 * k + h] = atomicAdd(&s_hist[(rec[2 * k + h] >> 2) >> shift], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the batch's bin histogram (kScat2BPT bins per thread)
+        unsigned int hv[kScat2BPT], pr = 0;
+#pragma unroll
+        for (int q = 0; q < kScat2BPT; ++q) {
+            int k = kScat2BPT * t + q;
+            hv[q] = k < nbins ? s_hist[k] : 0u;
+            pr += hv[q];
+        }
+        {
+            unsigned int incl = pr;
+            for (int off = 1; off < 32; off <<= 1) {
+                unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += o;
+            }
+            if (lane == 31) s_w[wid] = incl;
+            __syncthreads();
+            if (wid == 0) {
+                unsigned int w = lane < kScat2T / 32 ? s_w[lane] : 0u, wi = w;
+                for (int off = 1; off < 32; off <<= 1) {
+                    unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
+                    if (lane >= off) wi += o;
+                }
+                s_w[lane] = wi - w;
+                if (lane == 31) s_w[32] = wi;
+            }
+            __syncthreads();
+            unsigned int ex = s_w[wid] + incl - pr;
+#pragma unroll
+            for (int q = 0; q < kScat2BPT; ++q) {
+                int k = kScat2BPT * t + q;
+                if (k < nbins) s_start[k] = ex;
+                ex += hv[q];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 2 * kScat2IPT; ++k)
+            if (rec[k] != 0xFFFFFFFFu) s_out[s_start[(rec[k] >> 2) >> shift] + rk[k]] = rec[k];
+        __syncthreads();
+        unsigned int nrec = s_w[32];
+        for (unsigned int k = t; k < nrec; k += kScat2T) {   // runs of a bin are contiguous
+            uint32_t r = s_out[k];
+            unsigned int bb = (r >> 2) >> shift;
+            recs[s_cur[bb] + (k - s_start[bb])] = r;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kScat2BPT; ++q) {
+            int k = kScat2BPT * t + q;
+            if (k < nbins) s_cur[k] += hv[q];
+        }
+    }
+    __syncthreads();
+    for (int k = t; k < kHubSlots; k += kScat2T) {
         if (s_keys[k] == kHubEmpty) continue;
         if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
         if (s_hflag[k]) hub_flag[k] = 1u;
@@ -3236,25 +3383,34 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
 
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
                               const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s) {
-    static bool attr = false;
+    static bool attr = false, attr2 = false;
     if (!attr) {
         cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatSmem);
         cudaFuncSetAttribute(k_bin_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCmpSmem);
         attr = true;
     }
     int64_t ntiles = (n + kCmpSub - 1) >> kSubShift;
-    const int G = num_sms();
+    static const bool v1 = getenv("GREM_SCATTER_V1") != nullptr;   // A/B switch: the round-1 scatter
+    if (!attr2) {
+        cudaFuncSetAttribute(k_bin_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScat2Smem);
+        attr2 = true;
+    }
+    const int G = binned_scatter_ctas();
     cudaMemsetAsync(bb.hub_cnt, 0, sizeof(unsigned long long) * kHubSlots, s);
     cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
     cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
     cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
     kmark(KM_BIN_HIST, 1, s);
-    k_bin_hist<<<G, kScatT, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
+    k_bin_hist<<<G, v1 ? kScatT : kScat2T, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
     kmark(KM_BIN_HIST, 0, s);
     exclusive_sum_i32(bb.hist, bb.offs, (int64_t)(bb.nbins + 1) * G, temp, temp_bytes, s);
     kmark(KM_BIN_SCATTER, 1, s);
-    k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
-                                               bb.hub_cnt, bb.hub_flag);
+    if (v1)
+        k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
+                                                   bb.hub_cnt, bb.hub_flag);
+    else
+        k_bin_scatter2<<<G, kScat2T, kScat2Smem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs,
+                                                      bb.recs, bb.hub_cnt, bb.hub_flag);
     kmark(KM_BIN_SCATTER, 0, s);
     kmark(KM_BIN_COMPACT, 1, s);
     k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.offs, G, bb.shift, n, b.hub_keys,
@@ -3262,7 +3418,8 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
                                                            bb.ticket, ntiles);
     kmark(KM_BIN_COMPACT, 0, s);
 }
-int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * num_sms(); }
+int binned_scatter_ctas() { return getenv("GREM_SCATTER_V1") ? num_sms() : 2 * num_sms(); }
+int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * binned_scatter_ctas(); }
 int binned_shift(int64_t n) {
     int shift = kSubShift;
     while (((n + (1LL << shift) - 1) >> shift) > kMaxBins) ++shift;

@@ -100,6 +100,7 @@ struct BinBufs {
 int binned_shift(int64_t n);
 int64_t binned_tiles(int64_t n);
 int64_t binned_hist_entries(int nbins);
+int binned_scatter_ctas();   // CTAs of the round-1 scatter (and its histogram)
 // writes nodes, meta, tlc, pos, cntc, nbrc, newb (incl. s0) for the chunk;
 // scal[0] = N_c, scal[2] = new nodes
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
