@@ -341,7 +341,7 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
-__global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __restrict__ e, int64_t m,
+__global__ void __launch_bounds__(kEdgeThreads, 3) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
                                                               const uint32_t* __restrict__ chg,
                                                               const int32_t* __restrict__ pos,
@@ -370,24 +370,46 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
             int64_t i = i0 + j * bd;
             ed[j] = i < hi ? __ldcs(&e[i]) : make_uint2(0u, 0u);   // (0,0): a self-loop, skipped
         }
+        // the per-edge chain (changed bit -> tentative label -> chunk index ->
+        // counter) is three dependent gathers; run it stage by stage across
+        // the kDeltaUnroll edges so each stage's loads are in flight together
+        // (round 2, with most lower endpoints changed, was latency bound on
+        // the chain taken one edge at a time)
+        uint32_t A[kDeltaUnroll], B[kDeltaUnroll], w[kDeltaUnroll];
+        bool act[kDeltaUnroll];
 #pragma unroll
         for (int j = 0; j < kDeltaUnroll; ++j) {
             uint32_t u = ed[j].x, v = ed[j].y;
-            if (u == v) continue;
-            uint32_t a = u < v ? u : v, b = u < v ? v : u;
-            uint32_t ca = a >> cshift;
-            if (!((s_chgc[ca >> 5] >> (ca & 31)) & 1u)) continue;   // coarse filter in shared memory
-            if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
-            uint8_t t = tl[a];
-            int cur = t & 0xF, prev = t >> 4;
+            A[j] = u < v ? u : v;
+            B[j] = u < v ? v : u;
+            uint32_t ca = A[j] >> cshift;
+            act[j] = u != v && ((s_chgc[ca >> 5] >> (ca & 31)) & 1u);   // coarse filter in shared memory
+        }
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) w[j] = act[j] ? chg[A[j] >> 5] : 0u;   // L2-resident bitmap
+        uint8_t t[kDeltaUnroll];
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) {
+            act[j] = (w[j] >> (A[j] & 31)) & 1u;
+            t[j] = act[j] ? tl[A[j]] : (uint8_t)0;
+        }
+        int hb[kDeltaUnroll];
+        int32_t pb[kDeltaUnroll];
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) {
+            hb[j] = act[j] ? hub_find(s_keys, B[j]) : -1;
+            pb[j] = (act[j] && hb[j] < 0) ? pos[B[j]] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kDeltaUnroll; ++j) {
+            if (!act[j]) continue;
+            int cur = t[j] & 0xF, prev = t[j] >> 4;
             unsigned long long d = enc_label(cur) - enc_label(prev);
-            int hb = hub_find(s_keys, b);
-            if (hb >= 0) {
-                atomicAdd(&s_cnt[hb], d);
+            if (hb[j] >= 0) {
+                atomicAdd(&s_cnt[hb[j]], d);
             } else {
-                int32_t pb = pos[b];
-                atomicAdd(&cntc[pb], d);
-                dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
+                atomicAdd(&cntc[pb[j]], d);
+                dirty[pb[j] / kRTileC] = 1;   // plain byte store: idempotent
             }
         }
     }
@@ -402,9 +424,9 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
     }
 }
 
-static inline unsigned edge_grid(int64_t m) {
+static inline unsigned edge_grid(int64_t m, int per_sm = 4) {   // per_sm: resident CTAs of the kernel
     int64_t blocks = (m + 4 * kEdgeThreads - 1) / (4 * kEdgeThreads);
-    int64_t cap = (int64_t)num_sms() * 4;
+    int64_t cap = (int64_t)num_sms() * per_sm;
     if (blocks > cap) blocks = cap;
     return (unsigned)(blocks < 1 ? 1 : blocks);
 }
@@ -413,7 +435,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
+    k_count_delta<<<edge_grid(m, 3), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 
@@ -746,7 +768,10 @@ struct RoundOut {
     long long* scal;   // [1] changed, [4] nbad, [6] first bad
 };
 
-__global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
+#ifndef GREM_RD_MINB
+#define GREM_RD_MINB 1   // A/B build knob: CTAs per SM the register budget of k_round_down allows
+#endif
+__global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
     if (a.gate && *a.gate == 0) return;
     __shared__ Clamp smem[kRT / 32];
     __shared__ long long sbad, sfirst;
@@ -784,6 +809,12 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
     int32_t xs[kRI];
     int nbad = 0, ch = 0;
     long long mybad = kInf, mybad_ch = kInf;
+    // changed bits: the thread's 8 nodes are consecutive chunk nodes (ascending
+    // ids), so their bitmap words / coarse blocks repeat; OR them into one
+    // RED per word / block instead of one per node, and never wait on a read
+    // of the coarse filter (its latency, 8 times per thread in sequence,
+    // dominated this kernel in round 1: ncu r02c)
+    uint32_t cw = 0xFFFFFFFFu, cmask = 0u, kc = 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < kRI; ++j) {
         xs[j] = (int32_t)x;
@@ -803,8 +834,18 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
                 ch++;
                 if (base + j < mybad_ch) mybad_ch = base + j;
                 out.tl[g[j]] = tc[j];
-                atomicOr(&out.chg[g[j] >> 5], 1u << (g[j] & 31));
-                mark_changed_coarse(out.chgc, out.chg_shift, g[j]);
+                uint32_t w = g[j] >> 5;
+                if (w != cw) {
+                    if (cmask) atomicOr(&out.chg[cw], cmask);
+                    cw = w;
+                    cmask = 0u;
+                }
+                cmask |= 1u << (g[j] & 31);
+                uint32_t c = g[j] >> out.chg_shift;
+                if (c != kc) {
+                    kc = c;
+                    atomicOr(&out.chgc[c >> 5], 1u << (c & 31));
+                }
             }
             // next round's tie guess: the tie rule at this x
             bool tie0 = (x - nm.o) <= (sl >> 1);
@@ -813,6 +854,7 @@ __global__ void __launch_bounds__(kRT) k_round_down(RoundArgs a, const long long
             x = clamp_apply(nm.f, x);
         }
     }
+    if (cmask) atomicOr(&out.chg[cw], cmask);
     store8_32(out.x + base, xs);
     store8_32(out.xalt + base, xs);
     store8_u8(a.meta + base, m);
@@ -2911,7 +2953,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned int s_hist[kMaxBins];
     hub_load(s_keys, hub_keys);
-    const int bd = blockDim.x;   // 1024 (GREM_SCATTER_V1) or 512: the scatter's CTA decomposition
+    const int bd = blockDim.x;   // the scatter's CTA decomposition
     for (int k = threadIdx.x; k < nbins; k += bd) s_hist[k] = 0;
     __syncthreads();
     int64_t lo, hi;
@@ -3070,146 +3112,6 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         }
     }
     for (int k = t; k < kHubSlots; k += kScatT) {
-        if (s_keys[k] == kHubEmpty) continue;
-        if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
-        if (s_hflag[k]) hub_flag[k] = 1u;
-    }
-}
-
-// ---- scatter, second form (default; GREM_SCATTER_V1=1 selects the one above):
-// 512-thread CTAs, two per SM (the block-wide sync phases of one CTA overlap
-// the other's loads), 4096-edge batches and no open-sector carry: a bin's
-// partial 32-byte sector is completed by this CTA's next run of the bin within
-// a few batches, while the line is still in L2 (the open sectors of all CTAs
-// are ~8 MB), so the carry's extra shared-memory traffic bought nothing.
-constexpr int kScat2T = 512;
-constexpr int kScat2IPT = 8;
-constexpr int kScat2Batch = kScat2T * kScat2IPT;   // edges per batch, <= 2 records each
-constexpr int kScat2BPT = kMaxBins / kScat2T;      // bins per thread in the batch scan
-constexpr size_t kScat2Smem = (size_t)kHubSlots * (8 + 4 + 4) + (size_t)kMaxBins * 4 * 3 + (size_t)2 * kScat2Batch * 4 + 64 * 4;
-static_assert(kScat2BPT * kScat2T == kMaxBins, "bins per thread");
-
-__global__ void __launch_bounds__(kScat2T, 2) k_bin_scatter2(const uint2* __restrict__ e, int64_t m,
-                                                            const uint32_t* __restrict__ lab2,
-                                                            const uint32_t* __restrict__ hub_keys, int shift, int nbins,
-                                                            const int32_t* __restrict__ offs,
-                                                            uint32_t* __restrict__ recs,
-                                                            unsigned long long* __restrict__ hub_cnt,
-                                                            uint32_t* __restrict__ hub_flag) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    unsigned long long* s_hcnt = reinterpret_cast<unsigned long long*>(smem_raw);
-    uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_hcnt + kHubSlots);
-    uint32_t* s_hflag = s_keys + kHubSlots;
-    unsigned int* s_hist = s_hflag + kHubSlots;
-    unsigned int* s_start = s_hist + kMaxBins;
-    unsigned int* s_cur = s_start + kMaxBins;
-    uint32_t* s_out = s_cur + kMaxBins;
-    unsigned int* s_w = s_out + 2 * kScat2Batch;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    hub_load(s_keys, hub_keys);
-    for (int k = t; k < kHubSlots; k += kScat2T) {
-        s_hcnt[k] = 0ULL;
-        s_hflag[k] = 0u;
-    }
-    for (int k = t; k < nbins; k += kScat2T) s_cur[k] = (unsigned int)offs[(int64_t)k * gridDim.x + blockIdx.x];
-    int64_t lo, hi;
-    cta_range(m, lo, hi);
-    for (int64_t b0 = lo; b0 < hi; b0 += kScat2Batch) {
-        for (int k = t; k < nbins; k += kScat2T) s_hist[k] = 0u;
-        uint2 ed[kScat2IPT];
-#pragma unroll
-        for (int k = 0; k < kScat2IPT; ++k) {
-            int64_t i = b0 + (int64_t)k * kScat2T + t;
-            ed[k] = i < hi ? __ldcs(e + i) : make_uint2(kHubEmpty, kHubEmpty);
-        }
-        __syncthreads();
-        uint32_t rec[2 * kScat2IPT], rk[2 * kScat2IPT];
-#pragma unroll
-        for (int k = 0; k < kScat2IPT; ++k) {
-            rec[2 * k] = 0xFFFFFFFFu;
-            rec[2 * k + 1] = 0xFFFFFFFFu;
-            uint32_t u = ed[k].x, v = ed[k].y;
-            if (u != kHubEmpty) {
-                int hu = hub_find(s_keys, u);
-                if (u == v) {   // self-loop: u is a chunk node, no count (model.py:53-55)
-                    if (hu >= 0) s_hflag[hu] = 1u;
-                    else rec[2 * k] = (u << 2) | 3u;
-                } else {
-                    int hv = hub_find(s_keys, v);
-                    uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
-                    if (hu >= 0) {
-                        if (cv) atomicAdd(&s_hcnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
-                        else s_hflag[hu] = 1u;
-                    } else {
-                        rec[2 * k] = (u << 2) | cv;
-                    }
-                    if (hv >= 0) {
-                        if (cu) atomicAdd(&s_hcnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
-                        else s_hflag[hv] = 1u;
-                    } else {
-                        rec[2 * k + 1] = (v << 2) | cu;
-                    }
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-                if (rec[2 * k + h] != 0xFFFFFFFFu) rk[2 * k + h] = atomicAdd(&s_hist[(rec[2 * k + h] >> 2) >> shift], 1u);
-        }
-        __syncthreads();
-        // exclusive scan of the batch's bin histogram (kScat2BPT bins per thread)
-        unsigned int hv[kScat2BPT], pr = 0;
-#pragma unroll
-        for (int q = 0; q < kScat2BPT; ++q) {
-            int k = kScat2BPT * t + q;
-            hv[q] = k < nbins ? s_hist[k] : 0u;
-            pr += hv[q];
-        }
-        {
-            unsigned int incl = pr;
-            for (int off = 1; off < 32; off <<= 1) {
-                unsigned int o = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += o;
-            }
-            if (lane == 31) s_w[wid] = incl;
-            __syncthreads();
-            if (wid == 0) {
-                unsigned int w = lane < kScat2T / 32 ? s_w[lane] : 0u, wi = w;
-                for (int off = 1; off < 32; off <<= 1) {
-                    unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
-                    if (lane >= off) wi += o;
-                }
-                s_w[lane] = wi - w;
-                if (lane == 31) s_w[32] = wi;
-            }
-            __syncthreads();
-            unsigned int ex = s_w[wid] + incl - pr;
-#pragma unroll
-            for (int q = 0; q < kScat2BPT; ++q) {
-                int k = kScat2BPT * t + q;
-                if (k < nbins) s_start[k] = ex;
-                ex += hv[q];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < 2 * kScat2IPT; ++k)
-            if (rec[k] != 0xFFFFFFFFu) s_out[s_start[(rec[k] >> 2) >> shift] + rk[k]] = rec[k];
-        __syncthreads();
-        unsigned int nrec = s_w[32];
-        for (unsigned int k = t; k < nrec; k += kScat2T) {   // runs of a bin are contiguous
-            uint32_t r = s_out[k];
-            unsigned int bb = (r >> 2) >> shift;
-            recs[s_cur[bb] + (k - s_start[bb])] = r;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < kScat2BPT; ++q) {
-            int k = kScat2BPT * t + q;
-            if (k < nbins) s_cur[k] += hv[q];
-        }
-    }
-    __syncthreads();
-    for (int k = t; k < kHubSlots; k += kScat2T) {
         if (s_keys[k] == kHubEmpty) continue;
         if (s_hcnt[k]) atomicAdd(&hub_cnt[k], s_hcnt[k]);
         if (s_hflag[k]) hub_flag[k] = 1u;
@@ -3383,34 +3285,25 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
 
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
                               const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s) {
-    static bool attr = false, attr2 = false;
+    static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatSmem);
         cudaFuncSetAttribute(k_bin_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCmpSmem);
         attr = true;
     }
     int64_t ntiles = (n + kCmpSub - 1) >> kSubShift;
-    static const bool v1 = getenv("GREM_SCATTER_V1") != nullptr;   // A/B switch: the round-1 scatter
-    if (!attr2) {
-        cudaFuncSetAttribute(k_bin_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScat2Smem);
-        attr2 = true;
-    }
     const int G = binned_scatter_ctas();
     cudaMemsetAsync(bb.hub_cnt, 0, sizeof(unsigned long long) * kHubSlots, s);
     cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
     cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
     cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
     kmark(KM_BIN_HIST, 1, s);
-    k_bin_hist<<<G, v1 ? kScatT : kScat2T, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
+    k_bin_hist<<<G, kScatT, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
     kmark(KM_BIN_HIST, 0, s);
     exclusive_sum_i32(bb.hist, bb.offs, (int64_t)(bb.nbins + 1) * G, temp, temp_bytes, s);
     kmark(KM_BIN_SCATTER, 1, s);
-    if (v1)
-        k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
-                                                   bb.hub_cnt, bb.hub_flag);
-    else
-        k_bin_scatter2<<<G, kScat2T, kScat2Smem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs,
-                                                      bb.recs, bb.hub_cnt, bb.hub_flag);
+    k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
+                                               bb.hub_cnt, bb.hub_flag);
     kmark(KM_BIN_SCATTER, 0, s);
     kmark(KM_BIN_COMPACT, 1, s);
     k_bin_compact<<<(unsigned)ntiles, kCmpT, kCmpSmem, s>>>(bb.recs, bb.offs, G, bb.shift, n, b.hub_keys,
@@ -3418,7 +3311,7 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
                                                            bb.ticket, ntiles);
     kmark(KM_BIN_COMPACT, 0, s);
 }
-int binned_scatter_ctas() { return getenv("GREM_SCATTER_V1") ? num_sms() : 2 * num_sms(); }
+int binned_scatter_ctas() { return num_sms(); }
 int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * binned_scatter_ctas(); }
 int binned_shift(int64_t n) {
     int shift = kSubShift;
