@@ -1722,11 +1722,45 @@ __global__ void k_seed_pairs(const uint2* __restrict__ e, int64_t m, uint2* __re
         vals[i] = make_uint2(ed.y, ed.x);
     }
 }
+// Succinct rank of the chunk-0 node set (ascending ids, the RLE runs): per
+// 32-id word {presence bits, members before the word}; rank(g) is one 8-byte
+// gather into n/4 bytes (L2-resident) plus a popcount, instead of a 4-byte
+// gather from an n x 4 B table in HBM (k_seed_map's column ranks were one
+// DRAM sector per CSR entry: 25.7 GB for a papers100M level-0 seed, ncu r02c).
+// Thread i owns the words from just after node i-1's word through node i's
+// word; the words before the first / after the last member are filled by a
+// grid-stride pass of their own (they can be long).
+__global__ void k_rank_words(const uint32_t* __restrict__ nodes, int64_t nc, int64_t nwords, uint2* __restrict__ rw) {
+    const int64_t wfirst = nodes[0] >> 5, wlast = nodes[nc - 1] >> 5;
+    GRID_STRIDE(q, nwords) {
+        if (q < wfirst) rw[q] = make_uint2(0u, 0u);
+        else if (q > wlast) rw[q] = make_uint2(0u, (uint32_t)nc);
+    }
+    GRID_STRIDE(i, nc) {
+        uint32_t g = nodes[i];
+        int64_t w = g >> 5;
+        if (i > 0)
+            for (int64_t q = (int64_t)(nodes[i - 1] >> 5) + 1; q < w; ++q) rw[q] = make_uint2(0u, (uint32_t)i);
+        if (i == 0 || (int64_t)(nodes[i - 1] >> 5) != w) {   // first member of its word: build the mask
+            uint32_t bits = 0u;
+            for (int64_t k = i; k < nc && (int64_t)(nodes[k] >> 5) == w; ++k) bits |= 1u << (nodes[k] & 31);
+            rw[w] = make_uint2(bits, (uint32_t)i);
+        }
+    }
+}
+__device__ __forceinline__ uint32_t word_rank(const uint2* __restrict__ rw, uint32_t g) {
+    uint2 q = __ldg(rw + (g >> 5));
+    return q.y + __popc(q.x & ((1u << (g & 31)) - 1u));
+}
+void launch_rank_words(const uint32_t* nodes, int64_t nc, int64_t nwords, uint2* rw, cudaStream_t s) {
+    if (nc > 0) k_rank_words<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, nwords, rw);
+}
+
 __global__ void k_seed_map(const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals, int64_t entries,
-                           const int32_t* __restrict__ rank, uint32_t* row_of, uint32_t* adj,
+                           const uint2* __restrict__ rw, uint32_t* row_of, uint32_t* adj,
                            int32_t* __restrict__ selfc) {
     GRID_STRIDE(j, entries) {
-        uint32_t r = (uint32_t)rank[skeys[j]], w = (uint32_t)rank[svals[j]];
+        uint32_t r = word_rank(rw, skeys[j]), w = word_rank(rw, svals[j]);
         row_of[j] = r;
         adj[j] = w;
         if (r == w) atomicAdd(&selfc[r], 1);
@@ -1754,9 +1788,9 @@ void launch_seed_sort(const uint2* e, int64_t m, uint32_t* keysA, uint32_t* vals
     *sorted_in_b = dk.Current() == keysB;
     cub::DeviceRunLengthEncode::Encode(temp, temp_bytes, dk.Current(), nodes, counts, d_nruns, entries, s);
 }
-void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const int32_t* rank,
+void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const uint2* rw,
                      uint32_t* row_of, uint32_t* adj, int32_t* selfc, cudaStream_t s) {
-    k_seed_map<<<grid_for(entries, 256, 16), 256, 0, s>>>(skeys, svals, entries, rank, row_of, adj, selfc);
+    k_seed_map<<<grid_for(entries, 256, 16), 256, 0, s>>>(skeys, svals, entries, rw, row_of, adj, selfc);
 }
 
 // union-find connected components (link larger root under smaller root)

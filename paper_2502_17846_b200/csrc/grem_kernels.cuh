@@ -188,7 +188,8 @@ size_t seed_csr_temp_bytes(int64_t entries);
 void launch_seed_sort(const uint2* e, int64_t m, uint32_t* keysA, uint32_t* valsA, uint32_t* keysB, uint32_t* valsB,
                       int end_bit, uint32_t* nodes, int32_t* counts, long long* d_nruns, void* temp,
                       size_t temp_bytes, bool* sorted_in_b, cudaStream_t s);
-void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const int32_t* rank,
+void launch_rank_words(const uint32_t* nodes, int64_t nc, int64_t nwords, uint2* rw, cudaStream_t s);
+void launch_seed_map(const uint32_t* skeys, const uint32_t* svals, int64_t entries, const uint2* rw,
                      uint32_t* row_of, uint32_t* adj, int32_t* selfc, cudaStream_t s);
 
 // hub detection from a sample of the level's edges

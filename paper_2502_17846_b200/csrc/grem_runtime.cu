@@ -128,6 +128,7 @@ struct grem_ctx {
     DBuf<unsigned long long> cnt{"cnt"};
     DBuf<double2> nbr{"nbr"};
     DBuf<int32_t> rank{"rank"}, scratch{"scratch"}, newid{"newid"};
+    DBuf<uint2> rankw{"rankw"};   // chunk-0 succinct rank words {bits, members before}
     // per chunk node
     DBuf<uint32_t> nodes{"nodes"};
     DBuf<uint8_t> meta{"meta"}, bad{"bad"}, want{"want"};
@@ -495,9 +496,11 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
                                   " chunk nodes");
     c->stats.visits += nc;
     exclusive_sum_i32(c->cursor.p, c->start.p, nc + 1, c->temp.p, c->temp.cap, s);
-    launch_set_rank(c->nodes.p, nc, c->rank.p, s);
+    const int64_t nwords = a.n / 32 + 1;
+    c->rankw.ensure(nwords, s);
+    launch_rank_words(c->nodes.p, nc, nwords, c->rankw.p, s);
     CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));   // now: self-loop entries per row
-    launch_seed_map(in_b ? c->sortk.p : c->row_of.p, in_b ? c->sortv.p : c->adj.p, entries, c->rank.p, c->row_of.p,
+    launch_seed_map(in_b ? c->sortk.p : c->row_of.p, in_b ? c->sortv.p : c->adj.p, entries, c->rankw.p, c->row_of.p,
                     c->adj.p, c->cursor.p, s);
     c->kernels += 4;
     SeedBufs sb = seed_bufs(c);
@@ -1841,7 +1844,7 @@ void grem_destroy(grem_ctx* c) {
     c->bin_hist.release();
     c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
     c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
-    c->rank.release(); c->scratch.release(); c->newid.release();
+    c->rank.release(); c->scratch.release(); c->newid.release(); c->rankw.release();
     c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
     c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
     c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release();
