@@ -3010,7 +3010,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
 
 constexpr int kScatIPT = 8;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
-constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8) + (size_t)2 * kScatBatch * 4 + 64 * 4;
+constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8 + 2) + (size_t)2 * kScatBatch * 4 + 64 * 4;
 
 __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
@@ -3028,7 +3028,8 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
     unsigned int* s_cur = s_start + kMaxBins;
     unsigned int* s_beg = s_cur + kMaxBins;       // first record slot of this CTA's region per bin
     uint32_t* s_carry = s_beg + kMaxBins;         // per bin: the open (incomplete) 32-byte sector
-    uint32_t* s_out = s_carry + 8 * kMaxBins;
+    uint2* s_dl = reinterpret_cast<uint2*>(s_carry + 8 * kMaxBins);   // per bin: {slot - batch offset, last full-sector slot}
+    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dl + kMaxBins);
     unsigned int* s_w = s_out + 2 * kScatBatch;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     hub_load(s_keys, hub_keys);
@@ -3102,8 +3103,16 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
             }
             __syncthreads();
             unsigned int ex = s_w[wid] + incl - pr;
-            if (2 * t < nbins) s_start[2 * t] = ex;
-            if (2 * t + 1 < nbins) s_start[2 * t + 1] = ex + v0;
+            if (2 * t < nbins) {
+                s_start[2 * t] = ex;
+                unsigned int c0 = s_cur[2 * t];
+                s_dl[2 * t] = make_uint2(c0 - ex, (c0 + v0) & ~7u);
+            }
+            if (2 * t + 1 < nbins) {
+                s_start[2 * t + 1] = ex + v0;
+                unsigned int c1 = s_cur[2 * t + 1];
+                s_dl[2 * t + 1] = make_uint2(c1 - (ex + v0), (c1 + v1) & ~7u);
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -3128,10 +3137,10 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         unsigned int nrec = s_w[32];
         for (unsigned int k = t; k < nrec; k += kScatT) {   // runs of a bin are contiguous
             uint32_t r = s_out[k];
-            unsigned int bb = (r >> 2) >> shift;
-            unsigned int p = s_cur[bb] + (k - s_start[bb]);
-            if (p < ((s_cur[bb] + s_hist[bb]) & ~7u)) recs[p] = r;
-            else s_carry[8 * bb + (p & 7u)] = r;
+            uint2 dl = s_dl[(r >> 2) >> shift];
+            unsigned int p = dl.x + k;
+            if (p < dl.y) recs[p] = r;
+            else s_carry[8 * ((r >> 2) >> shift) + (p & 7u)] = r;
         }
         __syncthreads();
         if (2 * t < nbins) s_cur[2 * t] += v0;

@@ -17,3 +17,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file $O/launches_level0.csv python tools/gpu_bisect_once.py papers100m > $O/l0.log 2>&1
 python tools/ncu_summary.py $O/launches_level0.csv > $O/launches_level0.txt 2>&1
 gzip -f $O/*.csv
+GREM_DEBUG_BUNDLE=1 python tools/gpu_subtree.py 1 > $O/subtree1_bundle.txt 2>&1
