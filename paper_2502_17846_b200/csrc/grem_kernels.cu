@@ -2901,6 +2901,26 @@ void launch_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_
     k_leaf_write<<<grid_for(n, 256), 256, 0, s>>>(lab, n, orig, leaf_base, final_lab);
 }
 
+// cut edges of one bisection (its own edge list and 0/1 labels): edges whose
+// endpoints got different sides.  partition() sums these over the leaf
+// bisections and adds the edges every extraction drops (grem_runtime.cu
+// recurse), which is the final count_cuts' cut (grem.py:235-240) without a
+// pass over the original edges after the last leaf.
+__global__ void k_bisect_cut(const uint2* __restrict__ e, int64_t m, const int8_t* __restrict__ lab,
+                             unsigned long long* out) {
+    unsigned long long c = 0;
+    GRID_STRIDE(i, m) {
+        uint2 ed = __ldcs(e + i);
+        c += __ldg(lab + ed.x) != __ldg(lab + ed.y);
+    }
+    for (int off = 16; off; off >>= 1) c += __shfl_down_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+void launch_bisect_cut(const uint2* e, int64_t m, const int8_t* lab, unsigned long long* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    if (m > 0) k_bisect_cut<<<grid_for(m, 256, 8), 256, 0, s>>>(e, m, lab, out);
+}
+
 __global__ void k_iota(int32_t* a, int64_t n) {
     GRID_STRIDE(i, n) a[i] = (int32_t)i;
 }

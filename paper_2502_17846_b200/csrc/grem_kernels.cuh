@@ -254,6 +254,7 @@ void launch_sub_orig(const int8_t* lab, int64_t n, int side, const int32_t* newi
                      int32_t* sub_orig, cudaStream_t s);
 void launch_leaf_write(const int8_t* lab, int64_t n, const int32_t* orig, int32_t leaf_base, int32_t* final_lab,
                        cudaStream_t s);
+void launch_bisect_cut(const uint2* e, int64_t m, const int8_t* lab, unsigned long long* out, cudaStream_t s);
 void launch_iota(int32_t* a, int64_t n, cudaStream_t s);
 // succinct side maps for the recursion (preferred path)
 void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wpop, uint32_t* pre, void* temp,

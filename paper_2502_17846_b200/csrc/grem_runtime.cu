@@ -21,6 +21,7 @@
 #include <unistd.h>
 #include <functional>
 #include <thread>
+#include <atomic>
 #include <cstring>
 #include <new>
 #include <utility>
@@ -1067,7 +1068,10 @@ void validate_cfg(const grem_config* cfg) {
 }
 
 // count_cuts on device edges / int32 device labels
-void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, int64_t n, grem_report* rep) {
+// known_cut >= 0: the caller already knows the cut (partition's incremental
+// count); only the sizes / max label / unlabeled checks run
+void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, int64_t n, grem_report* rep,
+                    long long known_cut = -1) {
     cudaStream_t s = c->s;
     ingest_wait_all(c);
     int64_t cap = rep && rep->sizes_cap > 0 ? rep->sizes_cap : 2;
@@ -1092,6 +1096,8 @@ void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, 
     if (neg & 4) {   // unlabeled nodes exist: exact int32 pass also checks endpoints (grem.py:238-239)
         launch_count_cuts(e, m, lab, n, d, nullptr, 0, d_max, d_neg, s);
         c->kernels += 1;
+    } else if (known_cut >= 0) {
+        h[0] = (unsigned long long)known_cut;
     } else if (m > 0) {
         int bits = 1;
         while (bits < 32 && (uint64_t)mx >= (1ULL << bits)) bits *= 2;
@@ -1101,8 +1107,10 @@ void count_cuts_dev(grem_ctx* c, const uint2* e, int64_t m, const int32_t* lab, 
         launch_count_cuts_packed(e, m, lab, n, lb, c->packed_lab.p, d, d_neg, s);
         c->kernels += 2;
     }
+    unsigned long long cut_known = h[0];
     CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * (cap + 2), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (known_cut >= 0 && !(neg & 4)) h[0] = cut_known;
     memcpy(&neg, ((char*)&h[1]) + sizeof(int), sizeof(int));
     if (neg & 1) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
     int64_t np = mx >= 0 ? (int64_t)mx + 1 : 1;
@@ -1543,6 +1551,10 @@ struct PartCtx {
     const grem_hooks* hooks;
     int32_t* final_lab;
     int shard_rank = 0;   // multi-GPU subtree sharding: this process's rank
+    // single-GPU partition: the final cut, accumulated while recursing (edges
+    // dropped by every extraction + cut edges of every leaf bisection)
+    std::atomic<long long> cut{0};
+    bool track_cut = false;
     // GREM_DEFER=1: the smaller sides split off the root context's chain run
     // after that chain (concurrently with each other) instead of alongside it
     struct Deferred {
@@ -1578,6 +1590,14 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     if (p_level == 2) {
         launch_leaf_write(c->lab.p, n, orig, (int32_t)leaf_base, pc.final_lab, s);
         c->kernels++;
+        if (pc.track_cut) {
+            ingest_wait_all(c);
+            PhaseScope ps(c, PH_CUTS);
+            launch_bisect_cut(e, m, c->lab.p, reinterpret_cast<unsigned long long*>(c->d_scal + 12), s);
+            c->kernels++;
+            scal_read(c, c->d_scal + 12, 1);
+            pc.cut += c->h_pin[0];
+        }
         return;
     }
     ingest_wait_all(c);
@@ -1613,6 +1633,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     n_off[2] = n;
     e_off[1] = c->h_pin[1];
     e_off[2] = e_off[1] + c->h_pin[2];
+    if (pc.track_cut) pc.cut += m - e_off[2];   // edges with endpoints on different sides: cut for good
     {
         PhaseScope ps(c, PH_EXTRACT);
         for (int side = 0; side < 2; ++side)
@@ -1724,6 +1745,7 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         CK(cudaEventRecord(g_dbg_t0, s));
     }
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
+    pc.track_cut = shard_world == 1 && !getenv("GREM_FINAL_CUT_PASS");   // A/B: the separate final count
     try {
         recurse(c, pc, d, m, n, orig, p, 0, 0, 0, shard_world);
         if (!pc.deferred.empty()) {   // GREM_DEFER: the split-off subtrees, concurrently
@@ -1748,8 +1770,8 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
                 if (e) std::rethrow_exception(e);
         }
         if (shard_world == 1) {
-            count_cuts_dev(c, d, m, fin, n, rep);
-            c->stats.path_bytes += 10 * m;   // final cut pass
+            count_cuts_dev(c, d, m, fin, n, rep, pc.track_cut ? (long long)pc.cut : -1);
+            c->stats.path_bytes += 10 * m;   // final cut pass (SURVEY 8(d) formula; done incrementally here)
         }
         if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, s));
         CK(cudaStreamSynchronize(s));
