@@ -341,7 +341,7 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
-__global__ void __launch_bounds__(kEdgeThreads, 3) k_count_delta(const uint2* __restrict__ e, int64_t m,
+__global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
                                                               const uint32_t* __restrict__ chg,
                                                               const int32_t* __restrict__ pos,
@@ -370,46 +370,24 @@ __global__ void __launch_bounds__(kEdgeThreads, 3) k_count_delta(const uint2* __
             int64_t i = i0 + j * bd;
             ed[j] = i < hi ? __ldcs(&e[i]) : make_uint2(0u, 0u);   // (0,0): a self-loop, skipped
         }
-        // the per-edge chain (changed bit -> tentative label -> chunk index ->
-        // counter) is three dependent gathers; run it stage by stage across
-        // the kDeltaUnroll edges so each stage's loads are in flight together
-        // (round 2, with most lower endpoints changed, was latency bound on
-        // the chain taken one edge at a time)
-        uint32_t A[kDeltaUnroll], B[kDeltaUnroll], w[kDeltaUnroll];
-        bool act[kDeltaUnroll];
 #pragma unroll
         for (int j = 0; j < kDeltaUnroll; ++j) {
             uint32_t u = ed[j].x, v = ed[j].y;
-            A[j] = u < v ? u : v;
-            B[j] = u < v ? v : u;
-            uint32_t ca = A[j] >> cshift;
-            act[j] = u != v && ((s_chgc[ca >> 5] >> (ca & 31)) & 1u);   // coarse filter in shared memory
-        }
-#pragma unroll
-        for (int j = 0; j < kDeltaUnroll; ++j) w[j] = act[j] ? chg[A[j] >> 5] : 0u;   // L2-resident bitmap
-        uint8_t t[kDeltaUnroll];
-#pragma unroll
-        for (int j = 0; j < kDeltaUnroll; ++j) {
-            act[j] = (w[j] >> (A[j] & 31)) & 1u;
-            t[j] = act[j] ? tl[A[j]] : (uint8_t)0;
-        }
-        int hb[kDeltaUnroll];
-        int32_t pb[kDeltaUnroll];
-#pragma unroll
-        for (int j = 0; j < kDeltaUnroll; ++j) {
-            hb[j] = act[j] ? hub_find(s_keys, B[j]) : -1;
-            pb[j] = (act[j] && hb[j] < 0) ? pos[B[j]] : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < kDeltaUnroll; ++j) {
-            if (!act[j]) continue;
-            int cur = t[j] & 0xF, prev = t[j] >> 4;
+            if (u == v) continue;
+            uint32_t a = u < v ? u : v, b = u < v ? v : u;
+            uint32_t ca = a >> cshift;
+            if (!((s_chgc[ca >> 5] >> (ca & 31)) & 1u)) continue;   // coarse filter in shared memory
+            if (!((chg[a >> 5] >> (a & 31)) & 1u)) continue;   // L2-resident bitmap of changed labels
+            uint8_t t = tl[a];
+            int cur = t & 0xF, prev = t >> 4;
             unsigned long long d = enc_label(cur) - enc_label(prev);
-            if (hb[j] >= 0) {
-                atomicAdd(&s_cnt[hb[j]], d);
+            int hb = hub_find(s_keys, b);
+            if (hb >= 0) {
+                atomicAdd(&s_cnt[hb], d);
             } else {
-                atomicAdd(&cntc[pb[j]], d);
-                dirty[pb[j] / kRTileC] = 1;   // plain byte store: idempotent
+                int32_t pb = pos[b];
+                atomicAdd(&cntc[pb], d);
+                dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
             }
         }
     }
@@ -435,7 +413,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m, 3), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 
@@ -769,7 +747,7 @@ struct RoundOut {
 };
 
 #ifndef GREM_RD_MINB
-#define GREM_RD_MINB 1   // A/B build knob: CTAs per SM the register budget of k_round_down allows
+#define GREM_RD_MINB 2   // CTAs per SM the register budget of k_round_down allows (2: 647 vs 664 ms/step, r02d)
 #endif
 __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
     if (a.gate && *a.gate == 0) return;
@@ -2787,13 +2765,31 @@ __global__ void __launch_bounds__(kSplitT) k_split_edges(const uint2* __restrict
     for (int k = 0; k < kSplitI; ++k) {
         if (side[k] == 2) continue;
         unsigned long long p = s_pre[side[k]] + s_c[side[k]][k][wid] + rank[k];
-        (side[k] ? out1 : out0)[p] = ed[k];
+        if (side[k]) out1[-(int64_t)p] = ed[k];   // side 1 grows down from the arena's last slot
+        else out0[p] = ed[k];
     }
 }
+
+// side 1 was written backwards from the end of the arena: restore file order
+__global__ void k_reverse_u64(unsigned long long* a, int64_t n) {
+    GRID_STRIDE(i, n / 2) {
+        unsigned long long x = a[i], y = a[n - 1 - i];
+        a[i] = y;
+        a[n - 1 - i] = x;
+    }
+}
+void launch_reverse_edges(uint2* a, int64_t n, cudaStream_t s) {
+    if (n > 1) k_reverse_u64<<<grid_for(n / 2, 256, 8), 256, 0, s>>>(reinterpret_cast<unsigned long long*>(a), n);
+}
 size_t split_edges_tiles(int64_t m) { return (size_t)((m + kSplitTile - 1) / kSplitTile); }
+// One arena of m edges holds both induced subgraphs: side 0 from the front in
+// file order, side 1 from the back in reverse file order (launch_reverse_edges
+// on its e1 edges restores the order), so extraction needs m, not 2m, slots.
 void launch_split_edges(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int64_t nw, uint2* wi,
-                        uint2* out0, uint2* out1, unsigned long long* status, unsigned int* ticket, long long* counts,
+                        uint2* arena, unsigned long long* status, unsigned int* ticket, long long* counts,
                         cudaStream_t s) {
+    uint2* out0 = arena;
+    uint2* out1 = arena + (m > 0 ? m - 1 : 0);
     int64_t ntiles = (int64_t)split_edges_tiles(m);
     k_word_info<<<grid_for(nw, 256), 256, 0, s>>>(bits, pre, nw, wi);
     cudaMemsetAsync(counts, 0, 2 * sizeof(long long), s);
@@ -3030,7 +3026,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e
 
 constexpr int kScatIPT = 8;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
-constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8 + 2) + (size_t)2 * kScatBatch * 4 + 64 * 4;
+constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8) + (size_t)2 * kScatBatch * 4 + 64 * 4;
 
 __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
@@ -3048,8 +3044,7 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
     unsigned int* s_cur = s_start + kMaxBins;
     unsigned int* s_beg = s_cur + kMaxBins;       // first record slot of this CTA's region per bin
     uint32_t* s_carry = s_beg + kMaxBins;         // per bin: the open (incomplete) 32-byte sector
-    uint2* s_dl = reinterpret_cast<uint2*>(s_carry + 8 * kMaxBins);   // per bin: {slot - batch offset, last full-sector slot}
-    uint32_t* s_out = reinterpret_cast<uint32_t*>(s_dl + kMaxBins);
+    uint32_t* s_out = s_carry + 8 * kMaxBins;
     unsigned int* s_w = s_out + 2 * kScatBatch;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     hub_load(s_keys, hub_keys);
@@ -3123,16 +3118,8 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
             }
             __syncthreads();
             unsigned int ex = s_w[wid] + incl - pr;
-            if (2 * t < nbins) {
-                s_start[2 * t] = ex;
-                unsigned int c0 = s_cur[2 * t];
-                s_dl[2 * t] = make_uint2(c0 - ex, (c0 + v0) & ~7u);
-            }
-            if (2 * t + 1 < nbins) {
-                s_start[2 * t + 1] = ex + v0;
-                unsigned int c1 = s_cur[2 * t + 1];
-                s_dl[2 * t + 1] = make_uint2(c1 - (ex + v0), (c1 + v1) & ~7u);
-            }
+            if (2 * t < nbins) s_start[2 * t] = ex;
+            if (2 * t + 1 < nbins) s_start[2 * t + 1] = ex + v0;
         }
         __syncthreads();
 #pragma unroll
@@ -3157,10 +3144,10 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
         unsigned int nrec = s_w[32];
         for (unsigned int k = t; k < nrec; k += kScatT) {   // runs of a bin are contiguous
             uint32_t r = s_out[k];
-            uint2 dl = s_dl[(r >> 2) >> shift];
-            unsigned int p = dl.x + k;
-            if (p < dl.y) recs[p] = r;
-            else s_carry[8 * ((r >> 2) >> shift) + (p & 7u)] = r;
+            unsigned int bb = (r >> 2) >> shift;
+            unsigned int p = s_cur[bb] + (k - s_start[bb]);
+            if (p < ((s_cur[bb] + s_hist[bb]) & ~7u)) recs[p] = r;
+            else s_carry[8 * bb + (p & 7u)] = r;
         }
         __syncthreads();
         if (2 * t < nbins) s_cur[2 * t] += v0;

@@ -261,8 +261,9 @@ void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wp
                       size_t temp_bytes, cudaStream_t s);
 size_t split_edges_tiles(int64_t m);
 void launch_split_edges(const uint2* e, int64_t m, const uint32_t* bits, const uint32_t* pre, int64_t nw, uint2* wi,
-                        uint2* out0, uint2* out1, unsigned long long* status, unsigned int* ticket, long long* counts,
+                        uint2* arena, unsigned long long* status, unsigned int* ticket, long long* counts,
                         cudaStream_t s);
+void launch_reverse_edges(uint2* a, int64_t n, cudaStream_t s);
 void launch_sub_orig_bits(const int8_t* lab, int64_t n, int side, const uint32_t* bits, const uint32_t* pre,
                           const int32_t* orig, int32_t* sub, cudaStream_t s);
 // cut count with labels packed to 2^lb bits (d_neg gets bit 1 on negative labels)

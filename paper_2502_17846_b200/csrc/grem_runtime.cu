@@ -211,7 +211,7 @@ struct grem_ctx {
     DBuf<int32_t> lab32;
     DBuf<uint32_t> packed_lab{"packed_lab"}, side_bits{"side_bits"}, side_pop{"side_pop"}, side_pre{"side_pre"};
     // recursion arena: per-level induced-subgraph buffers (reused across calls)
-    DBuf<uint2> rec_e[40], rec_e1[40];
+    DBuf<uint2> rec_e[40];   // per recursion level: both induced subgraphs of the level's bisection
     DBuf<uint2> word_info{"word_info"};
     DBuf<unsigned long long> lb_status{"lb_status"};
     DBuf<unsigned int> lb_ticket{"lb_ticket"};
@@ -1602,10 +1602,9 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     }
     ingest_wait_all(c);
     // extract both sides: one pass over the edges writes both induced subgraphs
-    c->rec_e[level].ensure(m > 0 ? m : 1, s);
-    c->rec_e1[level].ensure(m > 0 ? m : 1, s);
+    c->rec_e[level].ensure(m > 0 ? m : 1, s);   // both sides in one arena (launch_split_edges)
     c->rec_o[level].ensure(n, s);
-    uint2* side_e[2] = {c->rec_e[level].p, c->rec_e1[level].p};
+    uint2* side_e[2] = {c->rec_e[level].p, nullptr};
     int32_t* sub_o = c->rec_o[level].p;
     int64_t e_off[3] = {0, 0, 0}, n_off[3] = {0, 0, 0};
     int64_t nw = (n + 31) / 32;
@@ -1620,7 +1619,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         PhaseScope ps(c, PH_EXTRACT);
         CK(cudaMemsetAsync(c->side_pop.p + nw, 0, sizeof(uint32_t), s));
         launch_side_bits(c->lab.p, n, c->side_bits.p, c->side_pop.p, c->side_pre.p, c->temp.p, c->temp.cap, s);
-        launch_split_edges(e, m, c->side_bits.p, c->side_pre.p, nw, c->word_info.p, side_e[0], side_e[1],
+        launch_split_edges(e, m, c->side_bits.p, c->side_pre.p, nw, c->word_info.p, side_e[0],
                            c->lb_status.p, c->lb_ticket.p, c->d_scal + 6, s);
         CK(cudaMemcpyAsync(&c->h_pin[0], c->side_pre.p + nw, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&c->h_pin[1], c->d_scal + 6, 2 * sizeof(long long), cudaMemcpyDeviceToHost, s));
@@ -1633,12 +1632,14 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     n_off[2] = n;
     e_off[1] = c->h_pin[1];
     e_off[2] = e_off[1] + c->h_pin[2];
+    side_e[1] = side_e[0] + (m - c->h_pin[2]);   // side 1 occupies the arena's last e1 slots
     if (pc.track_cut) pc.cut += m - e_off[2];   // edges with endpoints on different sides: cut for good
     {
         PhaseScope ps(c, PH_EXTRACT);
+        launch_reverse_edges(side_e[1], e_off[2] - e_off[1], s);
         for (int side = 0; side < 2; ++side)
             launch_sub_orig_bits(c->lab.p, n, side, c->side_bits.p, c->side_pre.p, orig, sub_o + n_off[side], s);
-        c->kernels += 2;
+        c->kernels += 3;
     }
     c->stats.path_bytes += 10 * m + 8 * e_off[2];   // extraction: read, gather, write kept edges
     // split the owning ranks between the sides in proportion to their edges
@@ -1882,7 +1883,6 @@ void grem_destroy(grem_ctx* c) {
     c->side_pre.release();
     for (int l = 0; l < 40; ++l) {
         c->rec_e[l].release();
-        c->rec_e1[l].release();
         c->rec_o[l].release();
     }
     c->part_fin.release();
