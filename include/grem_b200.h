@@ -114,6 +114,9 @@ int grem_get_phase_bytes(grem_ctx* ctx, double* bytes_out, int cap);
  * default pool); reset != 0 restarts them.  Buffers the caller allocated with
  * grem_device_alloc (plain cudaMalloc) are not included. */
 int grem_mem_high_water(grem_ctx* ctx, int64_t* used_high, int64_t* reserved_high, int reset);
+/* Release every device workspace of the context and its child contexts (the
+ * next call re-allocates them) and trim the memory pool. */
+int grem_trim(grem_ctx* ctx);
 
 /* --------------------------------------------------------------- the path */
 

@@ -222,6 +222,8 @@ struct grem_ctx {
     grem_stats stats{};
     long long kernels = 0;
 };
+void ctx_trim_buffers(grem_ctx* c);   // every device workspace of one context (defined below)
+
 
 namespace {
 
@@ -1492,6 +1494,15 @@ void init_ctx(grem_ctx* c, int device, bool child = false) {
 
 // A subtree position (level, leaf base) always gets the same child context,
 // so its workspaces are sized once and reused by later calls.
+// free device memory below `frac` of the device: deep recursions (k >= 64 on
+// the 1.8B-edge Friendster shape) then stop opening concurrent child contexts
+// and hand finished children's workspaces back to the pool
+bool mem_low(double frac) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) return false;
+    return (double)free_b < frac * (double)total_b;
+}
+
 grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
     grem_ctx* ch = nullptr;
     {
@@ -1669,7 +1680,8 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     bool mine0 = pc.shard_rank >= sr0[0] && pc.shard_rank < sr1[0];
     bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
     bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
-    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
+    static const double kSpawnFree = getenv("GREM_SPAWN_FREE") ? atof(getenv("GREM_SPAWN_FREE")) : 0.30;
+    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS") && !mem_low(kSpawnFree);
     static const bool defer = getenv("GREM_DEFER") && atoi(getenv("GREM_DEFER")) > 0;
     if (par && defer && c == c->root) {
         cudaEvent_t ready;
@@ -1720,6 +1732,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         th.join();
         cudaEventDestroy(ready);
         ctx_release(c, ch);
+        if (mem_low(kSpawnFree + 0.1)) ctx_trim_buffers(ch);   // (its stream is synchronised)
         if (err0) std::rethrow_exception(err0);
         if (err) std::rethrow_exception(err);
     } else {
@@ -1828,6 +1841,39 @@ int guarded(grem_ctx* c, F f) {
 
 }  // namespace
 
+// every device workspace of one context (stream-ordered frees on its stream)
+void ctx_trim_buffers(grem_ctx* c) {
+    c->lab.release();
+    c->lab2.release();
+    c->bin_recs.release();
+    c->bin_hist.release();
+    c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
+    c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
+    c->rank.release(); c->scratch.release(); c->newid.release(); c->rankw.release();
+    c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
+    c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
+    c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release();
+    c->sortk.release(); c->sortv.release(); c->parent.release();
+    c->csize.release(); c->roots.release(); c->rvals.release(); c->rvals2.release(); c->cpos.release();
+    c->disc.release(); c->frontier.release(); c->ckey.release(); c->rkeys.release(); c->rkeys2.release();
+    c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
+    c->fdeg.release(); c->cum.release(); c->temp.release(); c->edges_owned.release(); c->cc_sizes.release();
+    c->lab32.release();
+    c->packed_lab.release();
+    c->side_bits.release();
+    c->side_pop.release();
+    c->side_pre.release();
+    for (int l = 0; l < 40; ++l) {
+        c->rec_e[l].release();
+        c->rec_o[l].release();
+    }
+    c->part_fin.release();
+    c->part_orig.release();
+    c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
+    c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release(); c->ns_pack.release();
+    c->sh_keys.release(); c->sh_vals.release();
+}
+
 // =============================================================== C ABI
 
 extern "C" {
@@ -1861,35 +1907,7 @@ void grem_destroy(grem_ctx* c) {
     cudaStreamSynchronize(c->s);
     if (c->round_exec) cudaGraphExecDestroy(c->round_exec);
     c->round_exec = nullptr;
-    c->lab.release();
-    c->lab2.release();
-    c->bin_recs.release();
-    c->bin_hist.release();
-    c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
-    c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
-    c->rank.release(); c->scratch.release(); c->newid.release(); c->rankw.release();
-    c->nodes.release(); c->meta.release(); c->bad.release(); c->want.release(); c->newb.release(); c->x.release();
-    c->tile_agg.release(); c->tile_x.release(); c->tile_bad.release();
-    c->start.release(); c->cursor.release(); c->adj.release(); c->row_of.release();
-    c->sortk.release(); c->sortv.release(); c->parent.release();
-    c->csize.release(); c->roots.release(); c->rvals.release(); c->rvals2.release(); c->cpos.release();
-    c->disc.release(); c->frontier.release(); c->ckey.release(); c->rkeys.release(); c->rkeys2.release();
-    c->cand.release(); c->cand2.release(); c->pair.release(); c->slab.release(); c->slab2.release();
-    c->fdeg.release(); c->cum.release(); c->temp.release(); c->edges_owned.release(); c->cc_sizes.release();
-    c->lab32.release();
-    c->packed_lab.release();
-    c->side_bits.release();
-    c->side_pop.release();
-    c->side_pre.release();
-    for (int l = 0; l < 40; ++l) {
-        c->rec_e[l].release();
-        c->rec_o[l].release();
-    }
-    c->part_fin.release();
-    c->part_orig.release();
-    c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
-    c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release(); c->ns_pack.release();
-    c->sh_keys.release(); c->sh_vals.release();
+    ctx_trim_buffers(c);
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -1926,6 +1944,23 @@ int grem_get_phase_times(grem_ctx* c, double* ms_out, int64_t* count_out, int ca
         if (names_out) names_out[k] = kPhaseNames[k];
     }
     return PH_N;
+}
+
+int grem_trim(grem_ctx* c) {
+    if (!c) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(c->device));
+        for (grem_ctx* ch : c->pool_all) {
+            CK(cudaStreamSynchronize(ch->s));
+            ctx_trim_buffers(ch);
+        }
+        CK(cudaStreamSynchronize(c->s));
+        ctx_trim_buffers(c);
+        CK(cudaDeviceSynchronize());
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+        CK(cudaMemPoolTrimTo(pool, 0));
+    });
 }
 
 int grem_mem_high_water(grem_ctx* c, int64_t* used_high, int64_t* reserved_high, int reset) {

@@ -42,6 +42,7 @@ def _device_edges(shape):
     if shape not in _dev:
         for k in list(_dev):
             _abi.lib().grem_device_free(grem.context(), _dev.pop(k))
+        assert _abi.lib().grem_trim(grem.context()) == 0   # the previous shape's workspaces
         s = synth.SHAPES[shape]
         ptr = ctypes.c_void_p()
         L = _abi.lib()
