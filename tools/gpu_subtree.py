@@ -26,7 +26,9 @@ for side in path:
     n = int(sel.sum())
     del ei, keep, newid, sel, lab
     print(f"side {side}: n {n} m {e.shape[0]}", flush=True)
-grem.set_profiling(True)
+import os
+prof = os.environ.get('SUBTREE_PROFILE', '1') == '1'
+grem.set_profiling(prof)
 m = e.shape[0]
 for r in range(3):
     t = time.perf_counter()
