@@ -744,6 +744,8 @@ struct RoundOut {
     uint32_t* chgc;    // coarse changed filter
     int chg_shift;
     long long* scal;   // [1] changed, [4] nbad, [6] first bad
+    uint8_t* segbad;   // per bundle segment of segL nodes: a mis-speculated tie (nullptr: not tracked)
+    int64_t segL;
 };
 
 #ifndef GREM_RD_MINB
@@ -804,6 +806,7 @@ __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, c
             if (meta_pref(mm) == 2 && tie_misspeculated(mm, x, nm)) {   // mis-speculated tie
                 nbad++;
                 if (base + j < mybad) mybad = base + j;
+                if (out.segbad) out.segbad[(base + j) / out.segL] = 1;
             }
             // speculative decision (exact unless a repair follows) and tentative label update
             int cur = tc[j] & 0xF, code = b + 1;
@@ -1041,8 +1044,9 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
     RoundArgs a{b.nodes, b.meta, b.newb, b.cntc, b.nbrc, b.sizes, cap, nc, first_round ? nullptr : b.gate,
                 b.dcur, b.dnext, incremental};
     int64_t ntiles = (nc + 1 + kRTile - 1) / kRTile;   // x[nc] falls in a tile too
-    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.chgc, b.chg_shift, b.scal};
     static const bool fused = getenv("GREM_ROUND_FUSED") != nullptr;   // measured: no gain over 3 launches
+    RoundOut o{b.x, b.xnext, b.tlc, b.tl, b.chg, b.chgc, b.chg_shift, b.scal,
+               (fused || b.bseg_len <= 0) ? nullptr : b.segbad, b.bseg_len};
     if (fused && b.tflag) {
         cudaMemsetAsync(b.tflag, 0, sizeof(unsigned) * (ntiles + 1), s);   // flags + ticket (last word)
         FusedBufs fb{b.tile_inc, b.tflag, b.tflag + ntiles};
@@ -1203,12 +1207,17 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
                                                                  const int32_t* __restrict__ xalt, int64_t nc,
                                                                  int64_t L, int32_t* __restrict__ ends,
                                                                  int32_t* __restrict__ ckpt, const long long* nbad,
-                                                                 const long long* first_bad) {
+                                                                 const long long* first_bad,
+                                                                 const uint8_t* __restrict__ segbad) {
     constexpr int NT = kBundleWin * NWIN;
     constexpr int IPT = (kBundleBatch + NT - 1) / NT;
     if (*nbad == 0) return;
     int64_t seg = blockIdx.x;
     if (seg < bundle_seg0(first_bad, L)) return;
+    // only segments holding a mis-speculated tie and the segment after each
+    // need tables: elsewhere the exact trajectory is the speculative one as
+    // long as it enters on it (the chain checks, a miss replays exactly)
+    if (segbad && !segbad[seg] && !(seg > 0 && segbad[seg - 1])) return;
     __shared__ int32_t sK[kBundleBatch];
     __shared__ int32_t sO[kBundleBatch / kCkpt + 1];
     __shared__ int32_t swarp[NT / 32 + 1];
@@ -1295,12 +1304,15 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
                                                      const int32_t* __restrict__ xalt, const int32_t* __restrict__ ends,
                                                      int64_t nseg, int64_t nc, int64_t L, int32_t* __restrict__ xin,
                                                      int32_t* __restrict__ hit_out, const long long* nbad,
-                                                     const long long* first_bad, long long* misses) {
+                                                     const long long* first_bad, long long* misses,
+                                                     const uint8_t* __restrict__ segbad) {
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     const int lane = threadIdx.x;
     __shared__ __align__(16) int32_t tab[2][kChainSB * NT];
     __shared__ int32_t cen[2][kChainSB][NWIN];
+    __shared__ int32_t sxe[2][kChainSB];   // speculative x at the segment's end
+    __shared__ int32_t sflag[2][kChainSB];   // bit 0: mis-speculated tie inside, bit 1: simulated
     int64_t seg0 = bundle_seg0(first_bad, L);
     auto stage = [&](int buf, int64_t s0) {
         int cnt = (int)(nseg - s0 < kChainSB ? nseg - s0 : kChainSB);
@@ -1312,6 +1324,11 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
             cp_async4(&cen[buf][lane][0], xspec + lo);
             if (NWIN > 1) cp_async4(&cen[buf][lane][1], xalt + lo);
             if (NWIN > 2) cp_async4(&cen[buf][lane][NWIN > 2 ? 2 : 0], newb + lo);   // balance point: (s + 1) / 2
+            if (segbad) {
+                int64_t sg = s0 + lane;
+                cp_async4(&sxe[buf][lane], xspec + (lo + L < nc ? lo + L : nc));
+                sflag[buf][lane] = (segbad[sg] ? 1 : 0) | ((segbad[sg] || (sg > 0 && segbad[sg - 1])) ? 2 : 0);
+            }
         }
         cp_async_commit();
     };
@@ -1331,11 +1348,24 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
         for (int j = 0; j < cnt; ++j) {
             int64_t seg = s0 + j;
             int hit = -1;
+            int fl = segbad ? sflag[buf][j] : 3;   // no flags: every segment may hold a bad tie, all simulated
+            if (!(fl & 1) && cur == (long long)cen[buf][j][0]) {
+                // no mis-speculated tie and entered on the speculative trajectory:
+                // the speculative decisions are exact here (final / fix skip it)
+                if (lane == 0) {
+                    xin[seg] = (int32_t)cur;
+                    hit_out[seg] = -2;
+                }
+                cur = sxe[buf][j];
+                continue;
+            }
+            if (fl & 2) {
 #pragma unroll
-            for (int w = 0; w < NWIN; ++w) {
-                long long cw = w == 2 ? ((long long)cen[buf][j][w] + 1) / 2 : (long long)cen[buf][j][w];
-                long long d = cur - cw + kBundleWin / 2;
-                if (hit < 0 && d >= 0 && d < kBundleWin) hit = w * kBundleWin + (int)d;
+                for (int w = 0; w < NWIN; ++w) {
+                    long long cw = w == 2 ? ((long long)cen[buf][j][w] + 1) / 2 : (long long)cen[buf][j][w];
+                    long long d = cur - cw + kBundleWin / 2;
+                    if (hit < 0 && d >= 0 && d < kBundleWin) hit = w * kBundleWin + (int)d;
+                }
             }
             if (lane == 0) {
                 xin[seg] = (int32_t)cur;
@@ -1391,6 +1421,7 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
         if (seg < seg0) continue;
         int64_t lo = seg * L, hi = lo + L < nc ? lo + L : nc;
         int h = hit[seg];
+        if (h == -2) continue;   // exact speculative trajectory (k_bundle_chain)
         long long cur;
         int64_t a, e;
         if (h >= 0) {
@@ -1441,12 +1472,14 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
 
 // the repaired suffix re-decided from its exact x, one thread per node
 __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __restrict__ x, int64_t nc, int64_t L,
-                             const long long* nbad, const long long* first_bad, BundleFix fx) {
+                             const long long* nbad, const long long* first_bad, BundleFix fx,
+                             const int32_t* __restrict__ hit) {
     if (*nbad == 0) return;
     int64_t lo = bundle_seg0(first_bad, L) * L;
     long long dch = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc;
          i += (int64_t)gridDim.x * blockDim.x) {
+        if (hit[i / L] == -2) continue;   // decided exactly by k_round_down already
         int32_t pk = bp[i];
         int o = pk & 3;
         if (o == 2) continue;
@@ -1464,7 +1497,8 @@ __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __re
                 fx.tl[g] = nt;
                 if (!was) {
                     atomicOr(&fx.chg[g >> 5], 1u << (g & 31));
-                    mark_changed_coarse(fx.chgc, fx.chg_shift, g);
+                    uint32_t cc = g >> fx.chg_shift;
+                    atomicOr(&fx.chgc[cc >> 5], 1u << (cc & 31));   // RED: no dependent read of the filter
                 }
             } else if (was) {
                 atomicAnd(&fx.chg[g >> 5], ~(1u << (g & 31)));
@@ -1500,6 +1534,11 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     int64_t L = bundle_segment_len(nc);
     int64_t nseg = (nc + L - 1) / L;
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
+    // per-segment mis-speculation flags from k_round_down (same L); without
+    // them (fused round kernel, debug entry points) every segment is simulated
+    static const bool fused = getenv("GREM_ROUND_FUSED") != nullptr;
+    static const bool no_skip = getenv("GREM_BUNDLE_NO_SKIP") != nullptr;   // A/B switch
+    const uint8_t* segbad = (!fused && !no_skip && fix_decisions && b.bseg_len == L) ? b.segbad : nullptr;
     const long long* nbad = b.scal + 4;
     const long long* first_bad = b.scal + 6;
     BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
@@ -1509,20 +1548,20 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;
     if (nwin == 3) {
         k_bundle_sim<3><<<(unsigned)nseg, kBundleWin * 3, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
-                                                                 nbad, first_bad);
+                                                                 nbad, first_bad, segbad);
         k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
-                                           first_bad, b.scal + 3);
+                                           first_bad, b.scal + 3, segbad);
         k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     } else {
         k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
-                                                                 nbad, first_bad);
+                                                                 nbad, first_bad, segbad);
         k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
-                                           first_bad, b.scal + 3);
+                                           first_bad, b.scal + 3, segbad);
         k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     }
-    if (fix_decisions) k_bundle_fix<<<grid_for(nc, 256), 256, 0, s>>>(bb.params, b.x, nc, L, nbad, first_bad, fx);
+    if (fix_decisions) k_bundle_fix<<<grid_for(nc, 256), 256, 0, s>>>(bb.params, b.x, nc, L, nbad, first_bad, fx, bb.hit);
 }
 
 
@@ -1556,7 +1595,8 @@ void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
 // runs iff round r-1 changed a label) and clears this round's changed-label
 // bitmaps (double buffered: round r writes chg[r&1], count_delta(r+1) reads it).
 __global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all, int64_t nt, int first_round,
-                              uint32_t* chg, int64_t nchg, uint32_t* chgc, int64_t nchgc) {
+                              uint32_t* chg, int64_t nchg, uint32_t* chgc, int64_t nchgc, uint8_t* segbad,
+                              int64_t nseg) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (!first_round) {
             if (scal[7]) scal[8] += 1;
@@ -1574,12 +1614,16 @@ __global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all
     }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nchg; i += stride) chg[i] = 0u;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nchgc; i += stride) chgc[i] = 0u;
+    if (segbad)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseg; i += stride) segbad[i] = 0;
 }
 void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, int64_t nchg_words, cudaStream_t s) {
     int64_t work = nt > nchg_words ? nt : nchg_words;
+    int64_t nseg = b.bseg_len > 0 ? (nt * kRTileC + b.bseg_len - 1) / b.bseg_len + 1 : 0;
     k_round_start<<<grid_for(work, 256), 256, 0, s>>>(b.scal, b.dnext, first_round ? b.dcur : nullptr, nt,
                                                        first_round ? 1 : 0, b.chg, nchg_words, b.chgc,
-                                                       kChgCoarseBits / 32);
+                                                       kChgCoarseBits / 32, b.bseg_len > 0 ? b.segbad : nullptr,
+                                                       nseg);
 }
 
 // end of a round: the next round runs only if this one changed a label;

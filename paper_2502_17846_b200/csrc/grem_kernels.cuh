@@ -54,6 +54,8 @@ struct ChunkBufs {
     uint32_t* chg;              // n bits: tentative label changed in the last round (tl[g] valid)
     uint32_t* chgc;             // kChgCoarseBits bits: some node of the 2^chg_shift-id block changed
     int chg_shift;
+    uint8_t* segbad;            // per bundle segment (bseg_len nodes): a tie of this round was mis-speculated
+    int64_t bseg_len;
     // per scan tile
     Clamp* tile_agg;
     Clamp* tile_inc;            // single-pass round: inclusive look-back prefixes

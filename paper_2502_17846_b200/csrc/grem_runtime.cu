@@ -141,6 +141,7 @@ struct grem_ctx {
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
+    DBuf<uint8_t> bsegbad{"bsegbad"};   // per bundle segment: mis-speculated tie this round
     DBuf<Clamp> tile_agg{"tile_agg"}, tile_inc{"tile_inc"};
     DBuf<unsigned> tflag{"tflag"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
@@ -345,6 +346,7 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->bends.ensure(nseg * 192, c->s);
     c->bxin.ensure(nseg, c->s);
     c->bhit.ensure(nseg, c->s);
+    c->bsegbad.ensure(nseg + 1, c->s);
     c->bparams.ensure(nc_cap + 1, c->s);
     c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192, c->s);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
@@ -420,6 +422,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.gate = nullptr;
     b.dcur = c->dirty0.p;
     b.dnext = c->dirty1.p;
+    b.segbad = c->bsegbad.p;
+    b.bseg_len = 0;   // set per chunk (process_chunk: bundle_segment_len(nc))
     return b;
 }
 
@@ -694,6 +698,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         launch_add_base(c->newb.p, nc, c->d_sizes, s);
         c->kernels += 3;
     }
+    b.bseg_len = bundle_segment_len(nc);
     // identity padding up to whole round tiles (inactive nodes, meta 0)
     {
         int64_t padded = (nc + 1 + kScanTile - 1) / kScanTile * kScanTile;
@@ -1845,6 +1850,7 @@ int guarded(grem_ctx* c, F f) {
 void ctx_trim_buffers(grem_ctx* c) {
     c->lab.release();
     c->lab2.release();
+    c->bsegbad.release();
     c->bin_recs.release();
     c->bin_hist.release();
     c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
