@@ -1937,14 +1937,29 @@ __global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __
         int64_t i = base + (threadIdx.x & 31);
         bool valid = i < nc;
         uint32_t r = valid ? parent[i] : 0xFFFFFFFFu;
+        unsigned long long key = ~0ULL;
         if (valid) {
             uint32_t d = (uint32_t)(start[i + 1] - start[i] - selfc[i]);
-            unsigned long long key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
-            if (key < ((volatile unsigned long long*)ckey)[r]) atomicMin(&ckey[r], key);
+            key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
         }
-        unsigned peers = __match_any_sync(0xffffffffu, r);   // aggregate the giant component's size
+        unsigned peers = __match_any_sync(0xffffffffu, r);   // aggregate per component (the giant: whole warps)
         int leader = __ffs(peers) - 1;
-        if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&csize[r], (uint32_t)__popc(peers));
+        if (peers == 0xffffffffu) {
+            // one component for the whole warp: min of the keys by shuffles, one
+            // atomic per warp (every lane's read-then-atomic on the giant root's
+            // key serialised on one L2 address)
+            for (int off = 16; off; off >>= 1) {
+                unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
+                key = o < key ? o : key;
+            }
+            if (valid && (threadIdx.x & 31) == 0) {
+                atomicMin(&ckey[r], key);
+                atomicAdd(&csize[r], 32u);
+            }
+        } else if (valid) {
+            atomicMin(&ckey[r], key);
+            if ((int)(threadIdx.x & 31) == leader) atomicAdd(&csize[r], (uint32_t)__popc(peers));
+        }
     }
 }
 void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
