@@ -352,7 +352,8 @@ def _golden_full_run(workload, k):
     try:
         gs = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_shapes.json")))
         g = gs.get(f"{workload}_k{k}") or {}
-        sec = g.get("oracle_seconds") or g.get("reference_seconds") or g.get("seconds")
+        sec = g.get("oracle_seconds") or g.get("reference_seconds") or (None if g.get("derived_from") else
+                                                                           g.get("seconds"))
         if not sec or g.get("chunk_frac", 0.1) != 0.1:
             return None
         who = ("streamcut itself (pure Python)" if "reference_seconds" in g else
