@@ -333,6 +333,11 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
     }
 }
 
+__device__ __forceinline__ uint32_t word_rank(const uint2* __restrict__ rw, uint32_t g) {
+    uint2 q = __ldg(rw + (g >> 5));
+    return q.y + __popc(q.x & ((1u << (g & 31)) - 1u));
+}
+
 __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, uint32_t g) {
     uint32_t c = g >> shift;
     uint32_t bit = 1u << (c & 31);
@@ -344,7 +349,7 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
                                                               const uint32_t* __restrict__ chg,
-                                                              const int32_t* __restrict__ pos,
+                                                              const uint2* __restrict__ rankw,
                                                               unsigned long long* __restrict__ cntc,
                                                               const uint32_t* __restrict__ hub_keys,
                                                               const long long* __restrict__ gate,
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
             if (hb >= 0) {
                 atomicAdd(&s_cnt[hb], d);
             } else {
-                int32_t pb = pos[b];
+                int32_t pb = (int32_t)word_rank(rankw, b);   // L2-resident succinct map
                 atomicAdd(&cntc[pb], d);
                 dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
             }
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
         uint32_t key = s_keys[k];
         if (key != kHubEmpty && s_cnt[k]) {
-            int32_t pk = pos[key];
+            int32_t pk = (int32_t)word_rank(rankw, key);
             atomicAdd(&cntc[pk], s_cnt[k]);
             dirty[pk / kRTileC] = 1;
         }
@@ -413,7 +418,7 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.pos, b.cntc, b.hub_keys, b.gate, b.dcur,
+    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 
@@ -505,7 +510,6 @@ __global__ void k_node_init(const uint32_t* __restrict__ nodes, int64_t nc, cons
         bool active = isnew || refine;
         meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
         b.tlc[i] = (uint8_t)(code | (code << 4));
-        b.pos[g] = (int32_t)i;
         b.cntc[i] = b.cnt[g];
         b.cnt[g] = 0ULL;
         b.flag[g] = 0;
@@ -1769,10 +1773,6 @@ __global__ void k_rank_words(const uint32_t* __restrict__ nodes, int64_t nc, int
             rw[w] = make_uint2(bits, (uint32_t)i);
         }
     }
-}
-__device__ __forceinline__ uint32_t word_rank(const uint2* __restrict__ rw, uint32_t g) {
-    uint2 q = __ldg(rw + (g >> 5));
-    return q.y + __popc(q.x & ((1u << (g & 31)) - 1u));
 }
 void launch_rank_words(const uint32_t* nodes, int64_t nc, int64_t nwords, uint2* rw, cudaStream_t s) {
     if (nc > 0) k_rank_words<<<grid_for(nc, 256), 256, 0, s>>>(nodes, nc, nwords, rw);
@@ -3356,9 +3356,11 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         }
     }
     __syncthreads();
+    int kfirst;   // this thread's first member's index inside the tile
     {   // members of this thread in tile order
         unsigned long long ex = s_w[wid] + incl - mine;
         int k = (int)(ex & 0x7FFFFFFFULL), nw = (int)(ex >> 31);
+        kfirst = k;
 #pragma unroll
         for (int j = 0; j < kCmpIPT; ++j) {
             if (!((pmask >> j) & 1u)) continue;
@@ -3374,6 +3376,10 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
     const int64_t i0 = (int64_t)(pre & 0x7FFFFFFFULL);
     const long long nb0 = b.sizes[0] + b.sizes[1] + (long long)(pre >> 31);
     const int cnt = (int)(s_w[33] & 0x7FFFFFFFULL);
+    {   // succinct id -> chunk index map: this tile's 512 rank words {bits, members before}
+        uint32_t hi = __shfl_down_sync(0xffffffffu, pmask, 1);
+        if (!(t & 1)) b.rankw[(g0 >> 5) + (t >> 1)] = make_uint2(pmask | (hi << 16), (uint32_t)(i0 + kfirst));
+    }
     for (int k = t; k < cnt; k += kCmpT) {
         uint32_t v = s_idx[k];
         uint32_t l = v & (kCmpSub - 1);
@@ -3385,7 +3391,6 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         b.nodes[i] = g;
         b.meta[i] = (uint8_t)(code | (active ? M_ACTIVE : 0) | (isnew ? M_NEW : 0));
         b.tlc[i] = (uint8_t)(code | (code << 4));
-        b.pos[g] = (int32_t)i;
         b.cntc[i] = s_cnt[l];
         b.nbrc[i] = isnew ? make_double2(0.0, 0.0) : b.nbr[g];
         b.newb[i] = (int32_t)(nb0 + s_nwx[k]);   // s0 + active new nodes before i (new nodes are always active)

@@ -50,7 +50,8 @@ struct ChunkBufs {
     unsigned long long* cntc;   // packed counts (c0 | c1 << 32) of chunk node i
     double2* nbrc;              // running estimates of chunk node i (old nodes; 0 for new)
     uint8_t* tlc;               // tentative label codes (cur | prev << 4) of chunk node i
-    int32_t* pos;               // n: chunk index of node g (valid for this chunk's nodes)
+    int32_t* pos;               // (unused by the chunk rounds; see rankw)
+    uint2* rankw;               // n/32 words {presence bits, chunk members before}: chunk index of node g
     uint32_t* chg;              // n bits: tentative label changed in the last round (tl[g] valid)
     uint32_t* chgc;             // kChgCoarseBits bits: some node of the 2^chg_shift-id block changed
     int chg_shift;

@@ -318,7 +318,9 @@ void ensure_nodes(grem_ctx* c, int64_t n) {
     c->flag.ensure(n, c->s);
     c->cnt.ensure(n, c->s);
     c->nbr.ensure(n, c->s);
-    c->rank.ensure(n, c->s);
+    // succinct id -> chunk index map of the current chunk (rank words of 32
+    // ids, whole 16K-node compact tiles); replaces an n x 4 B index table
+    c->rankw.ensure(((n + 16383) / 16384) * 512 + 2, c->s);
     c->chg.ensure(n / 32 + 2, c->s);
     c->chgc.ensure(kChgCoarseBits / 32, c->s);
     c->chg2.ensure(n / 32 + 2, c->s);
@@ -406,7 +408,8 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.cntc = c->cntc.p;
     b.nbrc = c->nbrc.p;
     b.tlc = c->tlc.p;
-    b.pos = c->rank.p;   // the seed's rank array (chunk 0 only) doubles as the chunk index map
+    b.pos = nullptr;
+    b.rankw = c->rankw.p;
     b.chg = c->chg.p;
     b.chgc = c->chgc.p;
     b.chg_shift = chg_coarse_shift(c->live_n);
@@ -429,7 +432,7 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
 
 SeedBufs seed_bufs(grem_ctx* c) {
     SeedBufs sb;
-    sb.rank = c->rank.p;
+    sb.rank = nullptr;   // (the seed ranks through rankw)
     sb.start = c->start.p;
     sb.cursor = c->cursor.p;
     sb.adj = c->adj.p;
@@ -504,7 +507,6 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
     c->stats.visits += nc;
     exclusive_sum_i32(c->cursor.p, c->start.p, nc + 1, c->temp.p, c->temp.cap, s);
     const int64_t nwords = a.n / 32 + 1;
-    c->rankw.ensure(nwords, s);
     launch_rank_words(c->nodes.p, nc, nwords, c->rankw.p, s);
     CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * (nc + 1), s));   // now: self-loop entries per row
     launch_seed_map(in_b ? c->sortk.p : c->row_of.p, in_b ? c->sortv.p : c->adj.p, entries, c->rankw.p, c->row_of.p,
@@ -691,8 +693,9 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         kbytes(c, KM_BIN_SCATTER, 16.0 * mc);          // edge read + two 4-byte records out
         kbytes(c, KM_BIN_COMPACT, 8.0 * mc + 38.0 * nc + 16.0 * refined + (double)a.n);   // records in, state out, nbr + lab in
     }
-    if (!binned) {   // (the binned path wrote the compact state and newb already)
+    if (!binned) {   // (the binned path wrote the compact state, newb and the rank words already)
         PhaseScope ps(c, PH_NODE);
+        launch_rank_words(c->nodes.p, nc, a.n / 32 + 1, c->rankw.p, s);
         launch_node_init(b, nc, a.refine, s);
         exclusive_sum_i32(c->x.p, c->newb.p, nc, c->temp.p, c->temp.cap, s);
         launch_add_base(c->newb.p, nc, c->d_sizes, s);
