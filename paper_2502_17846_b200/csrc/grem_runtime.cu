@@ -1020,9 +1020,19 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     CK(cudaMemsetAsync(c->lab2.p, 0, sizeof(uint32_t) * (a.n / 16 + 2), s));
     CK(cudaMemsetAsync(c->chg.p, 0, sizeof(uint32_t) * (a.n / 32 + 2), s));
     CK(cudaMemsetAsync(c->chgc.p, 0, kChgCoarseBits / 8, s));
-    CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
-    CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
-    CK(cudaMemsetAsync(c->nbr.p, 0, sizeof(double2) * a.n, s));
+    // id-indexed counters / flags are only used by the unbinned (small-chunk)
+    // count path, which leaves them zero behind itself; the estimates nbr[g]
+    // are read only for nodes that already have a label, i.e. after a commit
+    // wrote them, so they need no clearing at all (1.8 GB at papers100M)
+    {
+        int64_t last = a.m ? a.m - (a.m - 1) / a.chunk * a.chunk : 0;
+        bool all_binned = !getenv("GREM_NO_BINNING") && a.n * 9 > (48LL << 20) && a.chunk >= (1 << 20) &&
+                          last >= (1 << 20) && a.passes == 1;
+        if (!all_binned) {
+            CK(cudaMemsetAsync(c->flag.p, 0, a.n, s));
+            CK(cudaMemsetAsync(c->cnt.p, 0, sizeof(unsigned long long) * a.n, s));
+        }
+    }
     CK(cudaMemsetAsync(c->d_sizes, 0, sizeof(long long) * 2, s));
     c->live_n = a.n;
     detect_hubs(c, a);
@@ -1505,10 +1515,38 @@ void init_ctx(grem_ctx* c, int device, bool child = false) {
 // free device memory below `frac` of the device: deep recursions (k >= 64 on
 // the 1.8B-edge Friendster shape) then stop opening concurrent child contexts
 // and hand finished children's workspaces back to the pool
-bool mem_low(double frac) {
+// cudaMemGetInfo is not free (it stalled the concurrent subtrees when called
+// per recursion node): the partition entry samples it once (mem_sample), and
+// recursion nodes only read the pool's reserved size, a host-side query
+struct MemModel {
+    int device = -1;
+    double total = 0, other = 0;   // device bytes; bytes held outside the stream-ordered pool
+};
+MemModel g_mem;
+std::mutex g_mem_mu;
+double pool_reserved(int device) {
+    cudaMemPool_t pool;
+    unsigned long long r = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r) != cudaSuccess) return 0;
+    return (double)r;
+}
+void mem_sample(int device) {
     size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || total_b == 0) return false;
-    return (double)free_b < frac * (double)total_b;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    g_mem.device = device;
+    g_mem.total = (double)total_b;
+    g_mem.other = (double)total_b - (double)free_b - pool_reserved(device);
+}
+bool mem_low(double frac, int device) {
+    MemModel m;
+    {
+        std::lock_guard<std::mutex> lk(g_mem_mu);
+        m = g_mem;
+    }
+    if (m.device != device || m.total <= 0) return false;
+    return m.total - m.other - pool_reserved(device) < frac * m.total;
 }
 
 grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
@@ -1689,7 +1727,8 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
     bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
     static const double kSpawnFree = getenv("GREM_SPAWN_FREE") ? atof(getenv("GREM_SPAWN_FREE")) : 0.30;
-    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS") && !mem_low(kSpawnFree);
+    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS") &&
+               !mem_low(kSpawnFree, c->device);
     static const bool defer = getenv("GREM_DEFER") && atoi(getenv("GREM_DEFER")) > 0;
     if (par && defer && c == c->root) {
         cudaEvent_t ready;
@@ -1740,7 +1779,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         th.join();
         cudaEventDestroy(ready);
         ctx_release(c, ch);
-        if (mem_low(kSpawnFree + 0.1)) ctx_trim_buffers(ch);   // (its stream is synchronised)
+        if (mem_low(kSpawnFree + 0.1, c->device)) ctx_trim_buffers(ch);   // (its stream is synchronised)
         if (err0) std::rethrow_exception(err0);
         if (err) std::rethrow_exception(err);
     } else {
@@ -1766,6 +1805,7 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         if (!g_dbg_t0) CK(cudaEventCreate(&g_dbg_t0));
         CK(cudaEventRecord(g_dbg_t0, s));
     }
+    mem_sample(c->device);
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
     pc.track_cut = shard_world == 1 && !getenv("GREM_FINAL_CUT_PASS");   // A/B: the separate final count
     try {
