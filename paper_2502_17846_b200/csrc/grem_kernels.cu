@@ -3055,8 +3055,16 @@ void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, ui
 // Per-CTA record histogram (the scatter CTA c covers the same contiguous
 // edge range): hist[bin * G + c]; its exclusive scan gives every CTA a private,
 // deterministic cursor per bin (no global atomics in the scatter).
-constexpr int kScatT = 1024;
-__global__ void __launch_bounds__(kScatT) k_bin_hist(const uint2* __restrict__ e, int64_t m,
+// Scatter shape (A/B build knobs): GREM_SCAT_T threads per CTA and
+// 1024 / GREM_SCAT_T CTAs per SM; the bin count limit kMaxBins (grem_kernels.cuh)
+// must be <= 2 * GREM_SCAT_T (two bins per thread in the batch scan).
+#ifndef GREM_SCAT_T
+#define GREM_SCAT_T 1024
+#endif
+constexpr int kScatT = GREM_SCAT_T;
+constexpr int kScatPerSM = 1024 / kScatT;   // the 64-register budget: 1024 resident threads
+static_assert(kMaxBins <= 2 * kScatT, "two bins per thread in the batch scan");
+__global__ void __launch_bounds__(1024) k_bin_hist(const uint2* __restrict__ e, int64_t m,
                                                      const uint32_t* __restrict__ hub_keys, int shift, int nbins,
                                                      int32_t* __restrict__ hist) {
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
@@ -3087,7 +3095,7 @@ constexpr int kScatIPT = 8;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
 constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8) + (size_t)2 * kScatBatch * 4 + 64 * 4;
 
-__global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
+__global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
                                                         const uint32_t* __restrict__ hub_keys, int shift, int nbins,
                                                         const int32_t* __restrict__ offs,
@@ -3167,12 +3175,12 @@ __global__ void __launch_bounds__(kScatT) k_bin_scatter(const uint2* __restrict_
             if (lane == 31) s_w[wid] = incl;
             __syncthreads();
             if (wid == 0) {
-                unsigned int w = s_w[lane], wi = w;
+                unsigned int w = lane < kScatT / 32 ? s_w[lane] : 0u, wi = w;
                 for (int off = 1; off < 32; off <<= 1) {
                     unsigned int o = __shfl_up_sync(0xffffffffu, wi, off);
                     if (lane >= off) wi += o;
                 }
-                s_w[lane] = wi - w;
+                if (lane < kScatT / 32) s_w[lane] = wi - w;
                 if (lane == 31) s_w[32] = wi;
             }
             __syncthreads();
@@ -3425,7 +3433,7 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
                                                            bb.ticket, ntiles);
     kmark(KM_BIN_COMPACT, 0, s);
 }
-int binned_scatter_ctas() { return num_sms(); }
+int binned_scatter_ctas() { return num_sms() * kScatPerSM; }
 int64_t binned_hist_entries(int nbins) { return (int64_t)(nbins + 1) * binned_scatter_ctas(); }
 int binned_shift(int64_t n) {
     int shift = kSubShift;

@@ -85,7 +85,10 @@ constexpr int kRTileC = 4096;   // nodes per round tile (kRT * kRI in grem_kerne
 // (node, label code) records binned by coarse node range (2^shift ids,
 // <= kMaxBins bins); one CTA per 2^kSubShift-node tile then accumulates its
 // records in shared memory and writes the compact chunk state directly.
-constexpr int kMaxBins = 2048;
+#ifndef GREM_MAX_BINS
+#define GREM_MAX_BINS 2048
+#endif
+constexpr int kMaxBins = GREM_MAX_BINS;
 #ifndef GREM_SUB_SHIFT
 #define GREM_SUB_SHIFT 14
 #endif
