@@ -1192,9 +1192,18 @@ __device__ __forceinline__ int64_t bundle_seg0(const long long* first_bad, int64
 
 __global__ void k_bundle_params(const uint8_t* __restrict__ meta, const int32_t* __restrict__ newb, int64_t nc,
                                 int64_t L, long long cap, int32_t* __restrict__ bp, const long long* nbad,
-                                const long long* first_bad) {
+                                const long long* first_bad, const uint8_t* __restrict__ segbad,
+                                int32_t* __restrict__ segflag) {
     if (*nbad == 0) return;
     int64_t lo = bundle_seg0(first_bad, L) * L;   // from the start of the first repaired segment
+    if (segbad) {   // per segment: bit 0 a mis-speculated tie inside, bit 1 simulate (it or its predecessor)
+        int64_t nseg = (nc + L - 1) / L;
+        for (int64_t sg = lo / L + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sg < nseg;
+             sg += (int64_t)gridDim.x * blockDim.x) {
+            bool b0 = segbad[sg], bp1 = sg > 0 && segbad[sg - 1];
+            segflag[sg] = (b0 ? 1 : 0) | ((b0 || bp1) ? 2 : 0);
+        }
+    }
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x)
         bp[i] = bundle_pack(meta[i], newb[i], cap);
 }
@@ -1212,7 +1221,7 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
                                                                  int64_t L, int32_t* __restrict__ ends,
                                                                  int32_t* __restrict__ ckpt, const long long* nbad,
                                                                  const long long* first_bad,
-                                                                 const uint8_t* __restrict__ segbad) {
+                                                                 const int32_t* __restrict__ segflag) {
     constexpr int NT = kBundleWin * NWIN;
     constexpr int IPT = (kBundleBatch + NT - 1) / NT;
     if (*nbad == 0) return;
@@ -1221,7 +1230,7 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
     // only segments holding a mis-speculated tie and the segment after each
     // need tables: elsewhere the exact trajectory is the speculative one as
     // long as it enters on it (the chain checks, a miss replays exactly)
-    if (segbad && !segbad[seg] && !(seg > 0 && segbad[seg - 1])) return;
+    if (segflag && !(segflag[seg] & 2)) return;
     __shared__ int32_t sK[kBundleBatch];
     __shared__ int32_t sO[kBundleBatch / kCkpt + 1];
     __shared__ int32_t swarp[NT / 32 + 1];
@@ -1309,7 +1318,7 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
                                                      int64_t nseg, int64_t nc, int64_t L, int32_t* __restrict__ xin,
                                                      int32_t* __restrict__ hit_out, const long long* nbad,
                                                      const long long* first_bad, long long* misses,
-                                                     const uint8_t* __restrict__ segbad) {
+                                                     const int32_t* __restrict__ segflag) {
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     const int lane = threadIdx.x;
@@ -1328,10 +1337,9 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
             cp_async4(&cen[buf][lane][0], xspec + lo);
             if (NWIN > 1) cp_async4(&cen[buf][lane][1], xalt + lo);
             if (NWIN > 2) cp_async4(&cen[buf][lane][NWIN > 2 ? 2 : 0], newb + lo);   // balance point: (s + 1) / 2
-            if (segbad) {
-                int64_t sg = s0 + lane;
+            if (segflag) {
                 cp_async4(&sxe[buf][lane], xspec + (lo + L < nc ? lo + L : nc));
-                sflag[buf][lane] = (segbad[sg] ? 1 : 0) | ((segbad[sg] || (sg > 0 && segbad[sg - 1])) ? 2 : 0);
+                cp_async4(&sflag[buf][lane], segflag + s0 + lane);
             }
         }
         cp_async_commit();
@@ -1352,7 +1360,7 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
         for (int j = 0; j < cnt; ++j) {
             int64_t seg = s0 + j;
             int hit = -1;
-            int fl = segbad ? sflag[buf][j] : 3;   // no flags: every segment may hold a bad tie, all simulated
+            int fl = segflag ? sflag[buf][j] : 3;   // no flags: every segment may hold a bad tie, all simulated
             if (!(fl & 1) && cur == (long long)cen[buf][j][0]) {
                 // no mis-speculated tie and entered on the speculative trajectory:
                 // the speculative decisions are exact here (final / fix skip it)
@@ -1547,21 +1555,23 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     const long long* first_bad = b.scal + 6;
     BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
                  fix_decisions ? b.scal + 1 : nullptr, b.dnext, b.chgc, b.chg_shift};
-    k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad);
+    int32_t* segflag = segbad ? bb.segflag : nullptr;
+    k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad, segbad,
+                                                      segflag);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
     int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;
     if (nwin == 3) {
         k_bundle_sim<3><<<(unsigned)nseg, kBundleWin * 3, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
-                                                                 nbad, first_bad, segbad);
+                                                                 nbad, first_bad, segflag);
         k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
-                                           first_bad, b.scal + 3, segbad);
+                                           first_bad, b.scal + 3, segflag);
         k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     } else {
         k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
-                                                                 nbad, first_bad, segbad);
+                                                                 nbad, first_bad, segflag);
         k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
-                                           first_bad, b.scal + 3, segbad);
+                                           first_bad, b.scal + 3, segflag);
         k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     }
@@ -1942,23 +1952,17 @@ __global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __
             uint32_t d = (uint32_t)(start[i + 1] - start[i] - selfc[i]);
             key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
         }
-        unsigned peers = __match_any_sync(0xffffffffu, r);   // aggregate per component (the giant: whole warps)
+        // one atomic per (warp, component): the lanes of a component (the giant
+        // fills most warps) reduce their keys first -- min of the degree part,
+        // then of the index among the lanes holding it -- instead of each lane
+        // racing a read-then-atomic on the root's key (one L2 address)
+        unsigned peers = __match_any_sync(0xffffffffu, r);
         int leader = __ffs(peers) - 1;
-        if (peers == 0xffffffffu) {
-            // one component for the whole warp: min of the keys by shuffles, one
-            // atomic per warp (every lane's read-then-atomic on the giant root's
-            // key serialised on one L2 address)
-            for (int off = 16; off; off >>= 1) {
-                unsigned long long o = __shfl_xor_sync(0xffffffffu, key, off);
-                key = o < key ? o : key;
-            }
-            if (valid && (threadIdx.x & 31) == 0) {
-                atomicMin(&ckey[r], key);
-                atomicAdd(&csize[r], 32u);
-            }
-        } else if (valid) {
-            atomicMin(&ckey[r], key);
-            if ((int)(threadIdx.x & 31) == leader) atomicAdd(&csize[r], (uint32_t)__popc(peers));
+        uint32_t khi = __reduce_min_sync(peers, (uint32_t)(key >> 32));
+        uint32_t klo = __reduce_min_sync(peers, (uint32_t)(key >> 32) == khi ? (uint32_t)key : 0xFFFFFFFFu);
+        if (valid && (int)(threadIdx.x & 31) == leader) {
+            atomicMin(&ckey[r], ((unsigned long long)khi << 32) | klo);
+            atomicAdd(&csize[r], (uint32_t)__popc(peers));
         }
     }
 }

@@ -132,6 +132,7 @@ struct BundleBufs {
     int32_t* ckpt;     // bundle_ckpt_ints(nc)
     int32_t* xin;      // nseg
     int32_t* hit;      // nseg
+    int32_t* segflag;  // nseg: bit 0 mis-speculated tie inside, bit 1 simulated (k_bundle_params)
 };
 int64_t bundle_segment_len(int64_t nc);
 int64_t bundle_ckpt_ints(int64_t nc);

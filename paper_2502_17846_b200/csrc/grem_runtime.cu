@@ -142,6 +142,7 @@ struct grem_ctx {
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
     DBuf<uint8_t> bsegbad{"bsegbad"};   // per bundle segment: mis-speculated tie this round
+    DBuf<int32_t> bsegflag{"bsegflag"};   // per bundle segment: flags for the sim / chain
     DBuf<Clamp> tile_agg{"tile_agg"}, tile_inc{"tile_inc"};
     DBuf<unsigned> tflag{"tflag"};
     DBuf<long long> tile_x{"tile_x"}, tile_bad{"tile_bad"};
@@ -349,6 +350,7 @@ void ensure_chunk(grem_ctx* c, int64_t nc_cap, int64_t entries_cap) {
     c->bxin.ensure(nseg, c->s);
     c->bhit.ensure(nseg, c->s);
     c->bsegbad.ensure(nseg + 1, c->s);
+    c->bsegflag.ensure(nseg + 1, c->s);
     c->bparams.ensure(nc_cap + 1, c->s);
     c->bckpt.ensure(bundle_ckpt_ints(nc_cap) + 192, c->s);
     int64_t tiles = (nc_cap + kScanTile - 1) / kScanTile + 1;
@@ -759,7 +761,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
                 launch_half_predictor(b, nc, a.cap, c->xalt.p, s);
                 c->kernels += 4;
             }
-            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
+            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p, c->bsegflag.p};
             launch_bundle(b, nc, a.cap, c->xalt.p, bb, r == 1 ? 3 : 2, s, true);
             c->kernels += 5;
         }
@@ -1894,6 +1896,7 @@ void ctx_trim_buffers(grem_ctx* c) {
     c->lab.release();
     c->lab2.release();
     c->bsegbad.release();
+    c->bsegflag.release();
     c->bin_recs.release();
     c->bin_hist.release();
     c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
@@ -2501,7 +2504,7 @@ extern "C" int grem_debug_chunk_scan(grem_ctx* c, const uint8_t* meta, const int
         if (do_walk == 1) launch_walk(b, nc, cap, c->s);
         if (do_walk >= 2) {   // production repair: half-step predictor + trajectory bundles (2 or 3 windows)
             launch_half_predictor(b, nc, cap, c->xalt.p, c->s);
-            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p};
+            BundleBufs bb{c->bparams.p, c->bends.p, c->bckpt.p, c->bxin.p, c->bhit.p, c->bsegflag.p};
             launch_bundle(b, nc, cap, c->xalt.p, bb, do_walk == 2 ? 3 : 2, c->s, false);
         }
         CK(cudaMemcpyAsync(x_out, c->x.p, sizeof(int32_t) * (nc + 1), cudaMemcpyDeviceToHost, c->s));
