@@ -1809,7 +1809,10 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
     }
     mem_sample(c->device);
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
-    pc.track_cut = shard_world == 1 && !getenv("GREM_FINAL_CUT_PASS");   // A/B: the separate final count
+    // incremental cut (extraction drops + per-leaf cut passes) only on request:
+    // measured slower and noisier than one final pass (the leaf passes compete
+    // with the concurrent sibling leaves; 652 vs 655-700 ms, r02k)
+    pc.track_cut = shard_world == 1 && getenv("GREM_INCREMENTAL_CUT");
     try {
         recurse(c, pc, d, m, n, orig, p, 0, 0, 0, shard_world);
         if (!pc.deferred.empty()) {   // GREM_DEFER: the split-off subtrees, concurrently
