@@ -117,6 +117,10 @@ int grem_mem_high_water(grem_ctx* ctx, int64_t* used_high, int64_t* reserved_hig
 /* Release every device workspace of the context and its child contexts (the
  * next call re-allocates them) and trim the memory pool. */
 int grem_trim(grem_ctx* ctx);
+/* write_buckets with out_edges == NULL (out_on_device 0) keeps the
+ * bucket-ordered edges on the device; this copies edges [first, first+count)
+ * of them to host memory, so a caller streams the store file in bounded pieces. */
+int grem_bucket_edges(grem_ctx* ctx, uint32_t* dst, int64_t first, int64_t count);
 
 /* --------------------------------------------------------------- the path */
 

@@ -54,7 +54,7 @@ class GremStatsC(ctypes.Structure):
 # every exported symbol of include/grem_b200.h (tests check they all resolve)
 EXPORTS = [
     "grem_create", "grem_destroy", "grem_last_error", "grem_get_stats", "grem_set_profiling",
-    "grem_get_phase_times", "grem_get_phase_bytes", "grem_mem_high_water", "grem_trim",
+    "grem_get_phase_times", "grem_get_phase_bytes", "grem_mem_high_water", "grem_trim", "grem_bucket_edges",
     "grem_bisect_u32", "grem_partition_u32", "grem_partition_shard_u32", "grem_staged_edges", "grem_count_cuts_u32",
     "grem_write_buckets_u32", "grem_write_buckets_file", "grem_reorder_records", "grem_node_stats_u32", "grem_shuffle_u32", "grem_shuffle_file", "grem_node_stats_file",
     "grem_bisect_file", "grem_partition_file", "grem_count_cuts_file", "grem_state_parts",
@@ -98,6 +98,7 @@ def _declare(L):
     L.grem_get_phase_bytes.argtypes = [c_vp, c_vp, c_int]
     L.grem_mem_high_water.argtypes = [c_vp, c_vp, c_vp, c_int]
     L.grem_trim.argtypes = [c_vp]
+    L.grem_bucket_edges.argtypes = [c_vp, c_vp, c_i64, c_i64]
     L.grem_bisect_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, P(GremConfigC), c_i64,
                                   P(GremHooksC), c_vp, P(GremReportC)]
     L.grem_partition_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, c_i64, P(GremConfigC),

@@ -10,6 +10,7 @@
 // O(n) device arrays (grem_core.cuh).  The host only reads a handful of
 // scalars per chunk round (N_c, labels changed).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -223,6 +224,7 @@ struct grem_ctx {
     int64_t live_n = 0;
     grem_stats stats{};
     long long kernels = 0;
+    int64_t bk_out_m = -1;   // edges of the last write_buckets kept in bk_out (-1: none)
 };
 void ctx_trim_buffers(grem_ctx* c);   // every device workspace of one context (defined below)
 
@@ -252,11 +254,14 @@ cudaEvent_t prof_event(grem_ctx* c) {
     return c->ev_pool[c->ev_used++];
 }
 
+// NVTX ranges mirror the phases (header-only nvtx3; free when no tool is
+// attached), so an nsys / ncu --nvtx timeline names every launch group
 struct PhaseScope {
     grem_ctx* c;
     int ph;
     cudaEvent_t a = nullptr, b = nullptr;
     PhaseScope(grem_ctx* c_, int ph_) : c(c_), ph(ph_) {
+        nvtxRangePushA(kPhaseNames[ph]);
         if (c->profiling) {
             a = prof_event(c);
             b = prof_event(c);
@@ -268,6 +273,7 @@ struct PhaseScope {
             cudaEventRecord(b, c->s);
             c->prof_open.push_back({ph, {a, b}});
         }
+        nvtxRangePop();
     }
 };
 
@@ -275,10 +281,19 @@ struct PhaseScope {
 struct PhaseSeq {
     grem_ctx* c;
     int ph = -1;
+    bool nvtx_open = false;
     cudaEvent_t a = nullptr;
     explicit PhaseSeq(grem_ctx* c_) : c(c_) {}
     void to(int nph) {
-        if (!c->profiling) return;
+        if (ph >= 0 || nph >= 0) {   // NVTX: close the open sub-phase, open the next
+            if (nvtx_open) nvtxRangePop();
+            nvtx_open = nph >= 0;
+            if (nvtx_open) nvtxRangePushA(kPhaseNames[nph]);
+        }
+        if (!c->profiling) {
+            ph = nph;
+            return;
+        }
         cudaEvent_t e = prof_event(c);
         cudaEventRecord(e, c->s);
         if (ph >= 0) c->prof_open.push_back({ph, {a, e}});
@@ -958,6 +973,14 @@ cudaEvent_t g_dbg_t0 = nullptr;   // GREM_DEBUG_LEVELS timeline origin
 void bisect_core(grem_ctx* c, const BisectArgs& a) {
     cudaStream_t s = c->s;
     CtxBind bind(c);
+    struct NvtxBisect {
+        explicit NvtxBisect(const BisectArgs& a) {
+            char buf[96];
+            snprintf(buf, sizeof buf, "bisect n=%lld m=%lld", (long long)a.n, (long long)a.m);
+            nvtxRangePushA(buf);
+        }
+        ~NvtxBisect() { nvtxRangePop(); }
+    } nvtx_bisect(a);
     static const char* dbg_levels = getenv("GREM_DEBUG_LEVELS");
     cudaEvent_t lv0 = nullptr, lv1 = nullptr;
     int64_t r0 = c->stats.rounds, v0 = c->stats.visits, b0 = c->stats.walk_steps;
@@ -2018,6 +2041,18 @@ int grem_trim(grem_ctx* c) {
     });
 }
 
+int grem_bucket_edges(grem_ctx* c, uint32_t* dst, int64_t first, int64_t count) {
+    if (!c || !dst || first < 0 || count < 0) return GREM_E_FORMAT;
+    return guarded(nullptr, [&] {
+        if (c->bk_out_m < 0 || first + count > c->bk_out_m)
+            fail(GREM_E_FORMAT, "no bucket-ordered edges of that range on the device");
+        CK(cudaSetDevice(c->device));
+        if (count)
+            CK(cudaMemcpyAsync(dst, c->bk_out.p + first, sizeof(uint2) * count, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
 int grem_mem_high_water(grem_ctx* c, int64_t* used_high, int64_t* reserved_high, int reset) {
     if (!c) return GREM_E_FORMAT;
     return guarded(nullptr, [&] {   // (no per-call stats reset)
@@ -2124,15 +2159,16 @@ static void write_buckets_dev(grem_ctx* c, const uint2* d, int64_t m, int64_t n,
     memcpy(&bad, &c->h_pin[1], sizeof(int));
     if (bad) fail(GREM_E_FORMAT, "unlabeled endpoint encountered");
     CK(cudaMemcpyAsync(counts_out, c->bk_counts.p, sizeof(uint64_t) * nb, cudaMemcpyDeviceToHost, s));
-    if (!out_on_device && m > 0)
+    if (!out_on_device && out_edges && m > 0)   // (out_edges NULL: kept on the device, grem_bucket_edges)
         CK(cudaMemcpyAsync(out_edges, out, sizeof(uint2) * m, cudaMemcpyDeviceToHost, s));
+    c->bk_out_m = out_on_device ? -1 : m;
     CK(cudaStreamSynchronize(s));
 }
 
 int grem_write_buckets_u32(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t n, int edges_on_device,
                            const int32_t* labels, int labels_on_device, uint32_t* out_edges, int out_on_device,
                            uint64_t* counts_out, int64_t counts_cap, int64_t* p_out) {
-    if (!c || !labels || !counts_out || (m > 0 && !out_edges)) return GREM_E_FORMAT;
+    if (!c || !labels || !counts_out || (m > 0 && !out_edges && out_on_device)) return GREM_E_FORMAT;
     return guarded(c, [&] {
         const uint2* d = stage_edges(c, edges, m, n, edges_on_device);
         write_buckets_dev(c, d, m, n, stage_labels(c, labels, n, labels_on_device), out_edges, out_on_device,
@@ -2146,7 +2182,7 @@ int grem_write_buckets_file(grem_ctx* c, const char* path, const int32_t* labels
     if (!c || !path || !labels || !counts_out) return GREM_E_FORMAT;
     return guarded(c, [&] {
         GrpeHeader hd = read_grpe_header(path);
-        if (hd.m > 0 && !out_edges) fail(GREM_E_FORMAT, "out_edges is NULL");
+        if (hd.m > 0 && !out_edges && out_on_device) fail(GREM_E_FORMAT, "out_edges is NULL");
         const uint2* d = load_grpe(c, path, &hd);
         write_buckets_dev(c, d, hd.m, hd.n, stage_labels(c, labels, hd.n, labels_on_device), out_edges,
                           out_on_device, counts_out, counts_cap, p_out);

@@ -98,6 +98,9 @@ def _offsets(counts: np.ndarray, pair: int) -> np.ndarray:
     return _BUCKET_HEADER.size + starts * pair
 
 
+_BUCKET_PIECE_EDGES = 16 << 20   # 128 MB of u32 pairs per host piece
+
+
 def write_buckets(efile, labels, out_path: str):
     """store.py:55-104 on the GPU (same file bytes as the reference)."""
     labels = np.asarray(labels)
@@ -110,27 +113,31 @@ def write_buckets(efile, labels, out_path: str):
     p_guess = int(assigned.max()) + 1 if assigned.size else 1
     counts = np.zeros(p_guess * p_guess, dtype=np.uint64)
     p_out = ctypes.c_int64()
+    # the bucket-ordered edges stay on the device and are written in bounded
+    # pieces (the reference streams blocks too, store.py:86-101)
     if is_native_binary(efile):   # GRPE u32: the overlapped native reader
         m = int(efile.meta.num_edges)
-        out = np.empty((m, 2), dtype=np.uint32)
         rc = _abi.lib().grem_write_buckets_file(context(), os.fsencode(efile.path), lab.ctypes.data, 0,
-                                                out.ctypes.data, 0, counts.ctypes.data, counts.size,
-                                                ctypes.byref(p_out))
+                                                None, 0, counts.ctypes.data, counts.size, ctypes.byref(p_out))
     else:
         edges = edges_u32(efile)
         m = int(edges.shape[0])
-        out = np.empty((m, 2), dtype=np.uint32)
         rc = _abi.lib().grem_write_buckets_u32(context(), edges.ctypes.data, m, n, 0, lab.ctypes.data, 0,
-                                               out.ctypes.data, 0, counts.ctypes.data, counts.size,
-                                               ctypes.byref(p_out))
+                                               None, 0, counts.ctypes.data, counts.size, ctypes.byref(p_out))
+        del edges
     _raise(rc)
     p = int(p_out.value)
     pair = 2 * (width // 8)
     cnt = counts.astype(np.int64)
     offsets = _offsets(cnt, pair)
+    piece = max(1, _BUCKET_PIECE_EDGES)
+    buf = np.empty((min(piece, max(m, 1)), 2), dtype=np.uint32)
     with open(out_path, "wb") as fh:
         fh.write(_BUCKET_HEADER.pack(BUCKET_MAGIC, 1, p, FLAG_WIDE_IDS if width == 64 else 0, m))
-        out.astype("<u8" if width == 64 else "<u4", copy=False).tofile(fh)
+        for lo in range(0, m, piece):
+            k = min(piece, m - lo)
+            _raise(_abi.lib().grem_bucket_edges(context(), buf.ctypes.data, lo, k))
+            buf[:k].astype("<u8" if width == 64 else "<u4", copy=False).tofile(fh)
     side = np.empty((p * p, 2), dtype="<u8")
     side[:, 0] = offsets
     side[:, 1] = cnt
