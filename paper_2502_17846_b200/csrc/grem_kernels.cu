@@ -1640,6 +1640,17 @@ void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, int64_
                                                        nseg);
 }
 
+// body tail of the device-side round loop (a conditional WHILE graph node,
+// grem_runtime.cu process_chunk): iterate again while the pair's last round
+// changed a label, within the round budget the host loop also enforced
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long* scal, long long max_rounds) {
+    bool again = scal[1] != 0 && scal[8] + 2 < max_rounds;
+    cudaGraphSetConditional(h, again ? 1u : 0u);
+}
+void launch_loop_cond(cudaGraphConditionalHandle h, const long long* scal, long long max_rounds, cudaStream_t s) {
+    k_loop_cond<<<1, 1, 0, s>>>(h, scal, max_rounds);
+}
+
 // end of a round: the next round runs only if this one changed a label;
 // scal[8] counts the rounds that actually ran
 __global__ void k_round_gate(long long* scal) {

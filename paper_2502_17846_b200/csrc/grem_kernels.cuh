@@ -249,6 +249,7 @@ void launch_labels_to_i32(const int8_t* lab, int64_t n, int32_t* out, cudaStream
 void launch_count_cuts(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* d_cut,
                        unsigned long long* d_sizes, int64_t sizes_cap, int* d_max, int* d_neg, cudaStream_t s);
 void launch_count_cuts_i8(const uint2* e, int64_t m, const int8_t* lab, unsigned long long* d_cut, cudaStream_t s);
+void launch_loop_cond(cudaGraphConditionalHandle h, const long long* scal, long long max_rounds, cudaStream_t s);
 void launch_check_piece(uint2* e, int64_t m, uint32_t n, unsigned long long* bad_max, cudaStream_t s);
 void launch_check_ids(const uint2* e, int64_t m, uint32_t* d_max_id, cudaStream_t s);
 

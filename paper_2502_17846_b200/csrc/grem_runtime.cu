@@ -139,6 +139,7 @@ struct grem_ctx {
     DBuf<uint8_t> tlc{"tlc"};
     DBuf<uint32_t> chg{"chg"}, chgc{"chgc"}, chg2{"chg2"}, chgc2{"chgc2"};
     cudaGraphExec_t round_exec = nullptr;   // replayed pair of rounds (process_chunk)
+    cudaGraphExec_t loop_exec = nullptr;    // device-side round loop (conditional WHILE node)
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
@@ -800,7 +801,51 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     const bool use_graph = graphs_on && batch == 2 && !c->profiling;
     bool graph_ready = false;
     long long pair_kernels = 0;
+    // Device-side convergence: rounds >= 3 run as a conditional WHILE graph
+    // node whose body is one round pair plus k_loop_cond, which sets the
+    // condition from the pair's last changed count -- one host round trip
+    // per chunk (after round 2) instead of one per pair.  The graph is built
+    // while rounds 1-2 run (GREM_NO_DEVICE_LOOP=1: one launch + host check per pair).
+    static const bool dev_loop_on = !getenv("GREM_NO_DEVICE_LOOP");
+    const bool dev_loop = use_graph && dev_loop_on;
+    const long long max_rounds = nc + 6;
+    bool looped = false;
     for (int r = 1;;) {
+        if (dev_loop && r == 3) {
+            cudaGraph_t parent = nullptr;
+            CK(cudaGraphCreate(&parent, 0));
+            cudaGraphConditionalHandle h;
+            CK(cudaGraphConditionalHandleCreate(&h, parent, 1, cudaGraphCondAssignDefault));
+            cudaGraphNodeParams np = {};   // (a union with no default constructor: value-initialise)
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = h;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            CK(cudaGraphAddNode(&node, parent, nullptr, 0, &np));
+            cudaGraph_t body = np.conditional.phGraph_out[0];
+            long long k0 = c->kernels;
+            CK(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            issue(r);
+            issue(r + 1);
+            launch_loop_cond(h, c->d_scal, max_rounds, s);
+            cudaGraph_t captured = nullptr;
+            CK(cudaStreamEndCapture(s, &captured));
+            pair_kernels = c->kernels - k0 + 1;
+            c->kernels = k0;
+            if (c->loop_exec) {
+                cudaGraphExecDestroy(c->loop_exec);   // a graph with conditionals: one instance at a time
+                c->loop_exec = nullptr;
+            }
+            CK(cudaGraphInstantiate(&c->loop_exec, parent, 0));
+            CK(cudaGraphDestroy(parent));
+            // the host check of round 2 (rounds 1-2 ran while the graph was built)
+            scal_read(c, c->d_scal + 1, 1);
+            if (c->h_pin[0] == 0) break;
+            CK(cudaGraphLaunch(c->loop_exec, s));
+            looped = true;
+            break;
+        }
         if (use_graph && r >= 3) {
             if (!graph_ready) {
                 long long k0 = c->kernels;
@@ -832,11 +877,17 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             issue(r);
             r += 1;
         }
-        if ((r - 1) % batch == 0) {
+        if ((r - 1) % batch == 0 && !(dev_loop && r == 3)) {   // (the device loop checks round 2 itself)
             scal_read(c, c->d_scal + 1, 1);   // the last round's changed count (the next round's gate)
             if (c->h_pin[0] == 0) break;
         }
         if (r > nc + 4 + batch) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
+    }
+    if (looped) {
+        scal_read(c, c->d_scal + 1, 8);   // [0] the last round's changed count, [7] rounds run
+        if (c->h_pin[0] != 0) fail(GREM_E_FORMAT, "internal: chunk rounds did not converge");
+        long long ran = c->h_pin[7];
+        c->kernels += pair_kernels * std::max(1LL, (ran - 1) / 2);
     }
     launch_round_gate(b, s);   // closes the last launched round's gate
     c->kernels++;
@@ -1549,13 +1600,14 @@ struct MemModel {
 };
 MemModel g_mem;
 std::mutex g_mem_mu;
-double pool_reserved(int device) {
+double pool_attr(int device, cudaMemPoolAttr attr) {
     cudaMemPool_t pool;
     unsigned long long r = 0;
     if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return 0;
-    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r) != cudaSuccess) return 0;
+    if (cudaMemPoolGetAttribute(pool, attr, &r) != cudaSuccess) return 0;
     return (double)r;
 }
+double pool_reserved(int device) { return pool_attr(device, cudaMemPoolAttrReservedMemCurrent); }
 void mem_sample(int device) {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
@@ -1571,7 +1623,15 @@ bool mem_low(double frac, int device) {
         m = g_mem;
     }
     if (m.device != device || m.total <= 0) return false;
-    return m.total - m.other - pool_reserved(device) < frac * m.total;
+    // memory in use by live allocations (the pool may also hold freed blocks
+    // it has not released yet: those are reusable, so they count as free)
+    double used = pool_attr(device, cudaMemPoolAttrUsedMemCurrent);
+    bool low = m.total - m.other - used < frac * m.total;
+    static const bool dbg = getenv("GREM_DEBUG_MEM") != nullptr;
+    if (low && dbg)
+        fprintf(stderr, "[mem] low: %.1f GB free of %.1f (other %.1f, pool used %.1f)\n",
+                (m.total - m.other - used) / 1e9, m.total / 1e9, m.other / 1e9, used / 1e9);
+    return low;
 }
 
 grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
@@ -1985,6 +2045,8 @@ void grem_destroy(grem_ctx* c) {
     cudaStreamSynchronize(c->s);
     if (c->round_exec) cudaGraphExecDestroy(c->round_exec);
     c->round_exec = nullptr;
+    if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
+    c->loop_exec = nullptr;
     ctx_trim_buffers(c);
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
