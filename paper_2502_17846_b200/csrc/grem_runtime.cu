@@ -805,8 +805,10 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
     // node whose body is one round pair plus k_loop_cond, which sets the
     // condition from the pair's last changed count -- one host round trip
     // per chunk (after round 2) instead of one per pair.  The graph is built
-    // while rounds 1-2 run (GREM_NO_DEVICE_LOOP=1: one launch + host check per pair).
-    static const bool dev_loop_on = !getenv("GREM_NO_DEVICE_LOOP");
+    // while rounds 1-2 run.  Off by default (GREM_DEVICE_LOOP=1): instantiating
+    // a graph with a conditional node per chunk cost more than the host round
+    // trips it saves (papers100M k=16: 664 vs 608 ms, profiles/r02_ab_devloop.txt).
+    static const bool dev_loop_on = getenv("GREM_DEVICE_LOOP") != nullptr;
     const bool dev_loop = use_graph && dev_loop_on;
     const long long max_rounds = nc + 6;
     bool looped = false;
