@@ -25,3 +25,4 @@ for spec in k_count_delta:46:cd_r2 k_round_down:55:rd_r2 k_bundle_sim:1:sim_r2 k
     ncu -i $O/sparse_full_$name.ncu-rep --page source --csv 2>/dev/null | gzip > $O/sparse_full_$name.source.csv.gz
     rm -f $O/sparse_full_$name.ncu-rep
 done
+GREM_DEBUG_LEVELS=1 python tools/gpu_levels_e2e.py papers100m 16 > $O/e2e_timeline.txt 2>&1
