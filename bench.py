@@ -275,14 +275,16 @@ def main():
     for kk, (ms_l0, cnt_l0) in ph_l0.items():
         if not kk.startswith("k.") or cnt_l0 <= 0 or ms_l0 <= 0 or by_l0.get(kk, 0) <= 0:
             continue
-        kname = "k_" + kk[2:]
+        base = kk[:-5] if kk.endswith("_full") else kk   # round kernels: bytes from full rounds,
+        kname = "k_" + base[2:]                            # share from all their launches
         ach = by_l0[kk] / (ms_l0 / 1e3) / 1e9
         tr = traffic.get(kname, {})
+        share = (phases.get(base, (0.0, 0))[0] + (phases.get(kk, (0.0, 0))[0] if kk != base else 0.0)) / step_ms_sum
         rows.append({"kernel": kname, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                      "algorithmic_bytes_per_launch": by_l0[kk] / cnt_l0, "avg_launch_ms": ms_l0 / cnt_l0,
-                     "launches_timed": cnt_l0,
+                     "launches_timed": cnt_l0, "timed_launches": "full rounds" if kk != base else "all",
                      "traffic": tr.get("dram_bytes_per_launch"), "traffic_source": tr.get("source"),
-                     "share_of_step": phases.get(kk, (0.0, 0))[0] / step_ms_sum})
+                     "share_of_step": share})
     rows.sort(key=lambda r: -r["share_of_step"])
     path_bytes = st.get("path_bytes")
     roof = None

@@ -1059,13 +1059,13 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
     }
     // kernel marks on full rounds only (incremental rounds skip clean tiles,
     // so their per-launch bytes are not the per-node figure)
-    if (!incremental) kmark(KM_ROUND_REDUCE, 1, s);
+    kmark(incremental ? KM_ROUND_REDUCE_ALL : KM_ROUND_REDUCE, 1, s);
     k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
-    if (!incremental) kmark(KM_ROUND_REDUCE, 0, s);
+    kmark(incremental ? KM_ROUND_REDUCE_ALL : KM_ROUND_REDUCE, 0, s);
     k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
-    if (!incremental) kmark(KM_ROUND_DOWN, 1, s);
+    kmark(incremental ? KM_ROUND_DOWN_ALL : KM_ROUND_DOWN, 1, s);
     k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
-    if (!incremental) kmark(KM_ROUND_DOWN, 0, s);
+    kmark(incremental ? KM_ROUND_DOWN_ALL : KM_ROUND_DOWN, 0, s);
 }
 
 // ------------------------------------------------------- trajectory bundles

@@ -13,7 +13,8 @@ namespace grem {
 // CUDA event pair around the marked launches when kernel profiling is on
 // (grem_set_profiling(ctx, 2)); a no-op otherwise.  Ids index the runtime's
 // kernel phases (KM_* -> "k.<name>").
-enum KMark { KM_BIN_HIST = 0, KM_BIN_SCATTER, KM_BIN_COMPACT, KM_ROUND_REDUCE, KM_ROUND_DOWN, KM_COUNT_DELTA, KM_N };
+enum KMark { KM_BIN_HIST = 0, KM_BIN_SCATTER, KM_BIN_COMPACT, KM_ROUND_REDUCE, KM_ROUND_DOWN, KM_COUNT_DELTA,
+             KM_ROUND_REDUCE_ALL, KM_ROUND_DOWN_ALL, KM_N };   // *_ALL: every launch (share of the step)
 void kmark(int km, int begin, cudaStream_t s);
 
 // Hub privatisation (power-law hubs would serialise the counter atomics):

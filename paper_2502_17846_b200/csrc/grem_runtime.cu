@@ -98,8 +98,8 @@ enum Phase {
 static const char* kPhaseNames[PH_N] = {"count_init", "select", "node_init", "count_delta", "scan", "bundle",
                                         "commit", "seed", "fill", "extract", "count_cuts", "ingest", "hubs",
                                         "seed.csr", "seed.cc", "seed.bfs", "seed.refine", "seed.commit",
-                                        "k.bin_hist", "k.bin_scatter", "k.bin_compact", "k.round_reduce",
-                                        "k.round_down", "k.count_delta"};
+                                        "k.bin_hist", "k.bin_scatter", "k.bin_compact", "k.round_reduce_full",
+                                        "k.round_down_full", "k.count_delta", "k.round_reduce", "k.round_down"};
 
 struct grem_ctx {
     int device = 0;
