@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, c
     // RED per word / block instead of one per node, and never wait on a read
     // of the coarse filter (its latency, 8 times per thread in sequence,
     // dominated this kernel in round 1: ncu r02c)
-    uint32_t cw = 0xFFFFFFFFu, cmask = 0u, kc = 0xFFFFFFFFu;
+    uint32_t cw = 0xFFFFFFFFu, cmask = 0u, kc = 0xFFFFFFFFu, kc0 = 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < kRI; ++j) {
         xs[j] = (int32_t)x;
@@ -827,9 +827,10 @@ __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, c
                 }
                 cmask |= 1u << (g[j] & 31);
                 uint32_t c = g[j] >> out.chg_shift;
-                if (c != kc) {
+                if (c != kc) {   // coarse blocks: the first is OR-ed warp-wide below, later ones directly
+                    if (kc0 == 0xFFFFFFFFu) kc0 = c;
+                    else atomicOr(&out.chgc[c >> 5], 1u << (c & 31));
                     kc = c;
-                    atomicOr(&out.chgc[c >> 5], 1u << (c & 31));
                 }
             }
             // next round's tie guess: the tie rule at this x
@@ -840,6 +841,17 @@ __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, c
         }
     }
     if (cmask) atomicOr(&out.chg[cw], cmask);
+    {   // the warp's lanes mostly share one coarse-filter word (a warp spans ~500
+        // ids): one RED per distinct word instead of up to 32 on one address
+        const bool has = kc0 != 0xFFFFFFFFu;
+        const unsigned act = __ballot_sync(0xffffffffu, has);
+        if (has) {
+            const uint32_t wi = kc0 >> 5;
+            const unsigned peers = __match_any_sync(act, wi);
+            const uint32_t bits = __reduce_or_sync(peers, 1u << (kc0 & 31));
+            if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(&out.chgc[wi], bits);
+        }
+    }
     store8_32(out.x + base, xs);
     store8_32(out.xalt + base, xs);
     store8_u8(a.meta + base, m);
