@@ -346,7 +346,16 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 
 // rounds >= 2: the higher endpoint of every edge sees the lower endpoint's
 // tentative label; apply the change since the previous round.
-__global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __restrict__ e, int64_t m,
+// STAGED (the first delta round of a chunk, where most lower endpoints
+// changed): the per-edge chain of dependent gathers (changed bit -> label ->
+// chunk index) runs stage by stage across the unrolled edges so each stage's
+// loads are in flight together; later rounds (few active edges) keep the
+// plain form, which has fewer registers and stays at 4 CTAs per SM.
+#ifndef GREM_CD_MINB
+#define GREM_CD_MINB 4   // CTAs per SM the plain delta kernel's register budget allows (A/B build knob)
+#endif
+template <bool STAGED>
+__global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
                                                               const uint32_t* __restrict__ chg,
                                                               const uint2* __restrict__ rankw,
@@ -375,6 +384,46 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
             int64_t i = i0 + j * bd;
             ed[j] = i < hi ? __ldcs(&e[i]) : make_uint2(0u, 0u);   // (0,0): a self-loop, skipped
         }
+        if constexpr (STAGED) {
+            uint32_t A[kDeltaUnroll], B[kDeltaUnroll], w[kDeltaUnroll];
+            bool act[kDeltaUnroll];
+#pragma unroll
+            for (int j = 0; j < kDeltaUnroll; ++j) {
+                uint32_t u = ed[j].x, v = ed[j].y;
+                A[j] = u < v ? u : v;
+                B[j] = u < v ? v : u;
+                uint32_t ca = A[j] >> cshift;
+                act[j] = u != v && ((s_chgc[ca >> 5] >> (ca & 31)) & 1u);
+            }
+#pragma unroll
+            for (int j = 0; j < kDeltaUnroll; ++j) w[j] = act[j] ? chg[A[j] >> 5] : 0u;
+            uint8_t t[kDeltaUnroll];
+#pragma unroll
+            for (int j = 0; j < kDeltaUnroll; ++j) {
+                act[j] = (w[j] >> (A[j] & 31)) & 1u;
+                t[j] = act[j] ? tl[A[j]] : (uint8_t)0;
+            }
+            int hb[kDeltaUnroll];
+            uint2 q[kDeltaUnroll];
+#pragma unroll
+            for (int j = 0; j < kDeltaUnroll; ++j) {
+                hb[j] = act[j] ? hub_find(s_keys, B[j]) : -1;
+                q[j] = (act[j] && hb[j] < 0) ? __ldg(rankw + (B[j] >> 5)) : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int j = 0; j < kDeltaUnroll; ++j) {
+                if (!act[j]) continue;
+                int cur = t[j] & 0xF, prev = t[j] >> 4;
+                unsigned long long d = enc_label(cur) - enc_label(prev);
+                if (hb[j] >= 0) {
+                    atomicAdd(&s_cnt[hb[j]], d);
+                } else {
+                    int32_t pb = (int32_t)(q[j].y + __popc(q[j].x & ((1u << (B[j] & 31)) - 1u)));
+                    atomicAdd(&cntc[pb], d);
+                    dirty[pb / kRTileC] = 1;
+                }
+            }
+        } else {
 #pragma unroll
         for (int j = 0; j < kDeltaUnroll; ++j) {
             uint32_t u = ed[j].x, v = ed[j].y;
@@ -394,6 +443,7 @@ __global__ void __launch_bounds__(kEdgeThreads, 4) k_count_delta(const uint2* __
                 atomicAdd(&cntc[pb], d);
                 dirty[pb / kRTileC] = 1;   // plain byte store: idempotent
             }
+        }
         }
     }
     __syncthreads();
@@ -417,8 +467,13 @@ static inline unsigned edge_grid(int64_t m, int per_sm = 4) {   // per_sm: resid
 void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
-void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
-    k_count_delta<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
+void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s, bool staged) {
+    if (staged) {
+        k_count_delta<true><<<edge_grid(m, 3), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys,
+                                                                     b.gate, b.dcur, b.chgc, b.chg_shift);
+        return;
+    }
+    k_count_delta<false><<<edge_grid(m, GREM_CD_MINB), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 

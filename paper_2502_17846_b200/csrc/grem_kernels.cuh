@@ -121,7 +121,7 @@ int num_sms();
 
 // --- non-seed chunk (process_chunk, grem.py:119-155) ---
 void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
-void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s);
+void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s, bool staged = false);
 void launch_node_init(const ChunkBufs& b, int64_t nc, int refine, cudaStream_t s);
 void launch_add_base(int32_t* a, int64_t n, const long long* sizes, cudaStream_t s);
 void launch_chunk_scan(const ChunkBufs& b, int64_t nc, long long cap, cudaStream_t s);

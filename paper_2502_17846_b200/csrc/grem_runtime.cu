@@ -753,7 +753,8 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
             bd.chg = chgbuf[(r - 1) & 1];
             bd.chgc = chgcbuf[(r - 1) & 1];
             kmark(KM_COUNT_DELTA, 1, s);
-            launch_count_delta(e, mc, bd, s);
+            static const bool staged_on = !getenv("GREM_NO_STAGED_DELTA");   // A/B switch
+            launch_count_delta(e, mc, bd, s, staged_on && r == 2);   // round 2: most lower endpoints changed
             kmark(KM_COUNT_DELTA, 0, s);
             kbytes(c, KM_COUNT_DELTA, 9.0 * mc);   // 8 B edge read + 1 B lower-endpoint label
             c->kernels++;
