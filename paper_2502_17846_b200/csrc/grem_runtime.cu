@@ -109,6 +109,7 @@ struct grem_ctx {
     grem_ctx* root = nullptr;
     std::mutex pool_mu;
     std::vector<grem_ctx*> pool_all, pool_idle;
+    bool busy = false;   // child context: a subtree is running on it (guarded by the root's pool_mu)
     std::vector<std::pair<long long, grem_ctx*>> pool_keyed;   // subtree position -> context
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_open;
     std::vector<cudaEvent_t> ev_pool;
@@ -1650,6 +1651,7 @@ grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
             root->pool_all.push_back(ch);
             root->pool_keyed.push_back({key, ch});
         }
+        ch->busy = true;
     }
     memset(&ch->stats, 0, sizeof(ch->stats));
     ch->kernels = 0;
@@ -1665,8 +1667,25 @@ grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
 }
 
 // fold a finished child's counters into its parent (stream already synchronised)
+// Workspaces of child contexts that are not running a subtree go back to the
+// pool (a deep recursion leaves one context per subtree position holding its
+// buffers: Friendster k=256 otherwise ran its next call with siblings
+// serialised for lack of memory, 4.5 s instead of 2.1 s)
+void trim_idle_children(grem_ctx* root) {
+    std::lock_guard<std::mutex> lk(root->pool_mu);
+    for (grem_ctx* ch : root->pool_all) {
+        if (ch->busy) continue;
+        cudaStreamSynchronize(ch->s);
+        ctx_trim_buffers(ch);
+    }
+}
+
 void ctx_release(grem_ctx* parent, grem_ctx* ch) {
     prof_collect(ch);
+    {
+        std::lock_guard<std::mutex> lk(parent->root->pool_mu);
+        ch->busy = false;
+    }
     grem_ctx* root = parent->root;
     (void)root;
     parent->stats.chunks += ch->stats.chunks;
@@ -1815,8 +1834,11 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
     bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
     static const double kSpawnFree = getenv("GREM_SPAWN_FREE") ? atof(getenv("GREM_SPAWN_FREE")) : 0.30;
-    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS") &&
-               !mem_low(kSpawnFree, c->device);
+    bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
+    if (par && mem_low(kSpawnFree, c->device)) {   // reclaim idle children first, then decide
+        trim_idle_children(c->root);
+        par = !mem_low(kSpawnFree, c->device);
+    }
     static const bool defer = getenv("GREM_DEFER") && atoi(getenv("GREM_DEFER")) > 0;
     if (par && defer && c == c->root) {
         cudaEvent_t ready;
