@@ -51,6 +51,39 @@ static inline unsigned grid_for(int64_t work, int threads, int per_sm = 8) {
 #define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); \
                                i += (int64_t)gridDim.x * blockDim.x)
 
+// Programmatic dependent launch for the round kernels: each is launched with
+// programmatic stream serialization (its CTAs may be scheduled while the
+// previous kernel drains) and waits at entry (griddepcontrol.wait) until that
+// kernel has completed and its writes are visible -- same semantics as a
+// plain stream order, minus the launch gap.  GREM_NO_PDL=1: plain launches.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    cudaGridDependencySynchronize();
+#endif
+}
+static bool pdl_on() {
+    static const bool on = getenv("GREM_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    if (!pdl_on()) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 // ------------------------------------------------------------------ scan core
 
 __device__ __forceinline__ Clamp shfl_up_clamp(const Clamp& v, int off) {
@@ -364,6 +397,7 @@ __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_cou
                                                               const long long* __restrict__ gate,
                                                               uint8_t* __restrict__ dirty,
                                                               const uint32_t* __restrict__ chgc, int cshift) {
+    pdl_wait();
     if (gate && *gate == 0) return;   // previous round changed nothing (converged)
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
     __shared__ unsigned long long s_cnt[kHubSlots];
@@ -469,11 +503,11 @@ void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s, bool staged) {
     if (staged) {
-        k_count_delta<true><<<edge_grid(m, 3), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys,
+        launch_pdl(k_count_delta<true>, dim3(edge_grid(m, 3)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys,
                                                                      b.gate, b.dcur, b.chgc, b.chg_shift);
         return;
     }
-    k_count_delta<false><<<edge_grid(m, GREM_CD_MINB), kEdgeThreads, 0, s>>>(e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
+    launch_pdl(k_count_delta<false>, dim3(edge_grid(m, GREM_CD_MINB)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 
@@ -755,6 +789,7 @@ __device__ __forceinline__ long long node_sl(uint8_t m, int32_t nb) {
 }
 
 __global__ void __launch_bounds__(kRT) k_round_reduce(RoundArgs a, Clamp* tile_agg, int first_round) {
+    pdl_wait();
     if (a.gate && *a.gate == 0) return;
     // a clean tile (no count change, no tie-guess change) keeps its preferences
     // and its aggregate from the previous round
@@ -811,6 +846,7 @@ struct RoundOut {
 #define GREM_RD_MINB 2   // CTAs per SM the register budget of k_round_down allows (2: 647 vs 664 ms/step, r02d)
 #endif
 __global__ void __launch_bounds__(kRT, GREM_RD_MINB) k_round_down(RoundArgs a, const long long* tile_x, RoundOut out) {
+    pdl_wait();
     if (a.gate && *a.gate == 0) return;
     __shared__ Clamp smem[kRT / 32];
     __shared__ long long sbad, sfirst;
@@ -1127,11 +1163,11 @@ void launch_round_scan(const ChunkBufs& b, int64_t nc, long long cap, int first_
     // kernel marks on full rounds only (incremental rounds skip clean tiles,
     // so their per-launch bytes are not the per-node figure)
     kmark(incremental ? KM_ROUND_REDUCE_ALL : KM_ROUND_REDUCE, 1, s);
-    k_round_reduce<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_agg, first_round);
+    launch_pdl(k_round_reduce, dim3((unsigned)ntiles), dim3(kRT), 0, s, a, b.tile_agg, first_round);
     kmark(incremental ? KM_ROUND_REDUCE_ALL : KM_ROUND_REDUCE, 0, s);
-    k_scan_top_gated<<<1, 1024, 0, s>>>(b.tile_agg, ntiles, b.sizes, b.tile_x, b.gate);
+    launch_pdl(k_scan_top_gated, dim3(1), dim3(1024), 0, s, (const Clamp*)b.tile_agg, ntiles, (const long long*)b.sizes, b.tile_x, b.gate);
     kmark(incremental ? KM_ROUND_DOWN_ALL : KM_ROUND_DOWN, 1, s);
-    k_round_down<<<(unsigned)ntiles, kRT, 0, s>>>(a, b.tile_x, o);
+    launch_pdl(k_round_down, dim3((unsigned)ntiles), dim3(kRT), 0, s, a, b.tile_x, o);
     kmark(incremental ? KM_ROUND_DOWN_ALL : KM_ROUND_DOWN, 0, s);
 }
 
@@ -1189,6 +1225,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce_gated(Src src, int
 }
 __global__ void __launch_bounds__(1024) k_scan_top_gated(const Clamp* tile_agg, int64_t ntiles, const long long* x0p,
                                                          long long* tile_x, const long long* gate) {
+    pdl_wait();
     if (gate && *gate == 0) return;
     __shared__ Clamp smem[32];
     int64_t per = (ntiles + 1023) / 1024;
@@ -1261,6 +1298,7 @@ __global__ void k_bundle_params(const uint8_t* __restrict__ meta, const int32_t*
                                 int64_t L, long long cap, int32_t* __restrict__ bp, const long long* nbad,
                                 const long long* first_bad, const uint8_t* __restrict__ segbad,
                                 int32_t* __restrict__ segflag) {
+    pdl_wait();
     if (*nbad == 0) return;
     int64_t lo = bundle_seg0(first_bad, L) * L;   // from the start of the first repaired segment
     if (segbad) {   // per segment: bit 0 a mis-speculated tie inside, bit 1 simulate (it or its predecessor)
@@ -1289,6 +1327,7 @@ __global__ void __launch_bounds__(kBundleWin * NWIN) k_bundle_sim(const int32_t*
                                                                  int32_t* __restrict__ ckpt, const long long* nbad,
                                                                  const long long* first_bad,
                                                                  const int32_t* __restrict__ segflag) {
+    pdl_wait();
     constexpr int NT = kBundleWin * NWIN;
     constexpr int IPT = (kBundleBatch + NT - 1) / NT;
     if (*nbad == 0) return;
@@ -1386,6 +1425,7 @@ __global__ void __launch_bounds__(32) k_bundle_chain(const int32_t* __restrict__
                                                      int32_t* __restrict__ hit_out, const long long* nbad,
                                                      const long long* first_bad, long long* misses,
                                                      const int32_t* __restrict__ segflag) {
+    pdl_wait();
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     const int lane = threadIdx.x;
@@ -1490,6 +1530,7 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
                                const int32_t* __restrict__ hit, const int32_t* __restrict__ ckpt, int64_t nseg,
                                int64_t nc, int64_t L, int32_t* __restrict__ x, int32_t* __restrict__ xalt,
                                const long long* nbad, const long long* first_bad) {
+    pdl_wait();
     constexpr int NT = kBundleWin * NWIN;
     if (*nbad == 0) return;
     int64_t ncp = (L + kCkpt - 1) / kCkpt;
@@ -1553,6 +1594,7 @@ __global__ void k_bundle_final(const int32_t* __restrict__ bp, const int32_t* __
 __global__ void k_bundle_fix(const int32_t* __restrict__ bp, const int32_t* __restrict__ x, int64_t nc, int64_t L,
                              const long long* nbad, const long long* first_bad, BundleFix fx,
                              const int32_t* __restrict__ hit) {
+    pdl_wait();
     if (*nbad == 0) return;
     int64_t lo = bundle_seg0(first_bad, L) * L;
     long long dch = 0;
@@ -1623,26 +1665,26 @@ void launch_bundle(const ChunkBufs& b, int64_t nc, long long cap, const int32_t*
     BundleFix fx{b.nodes, b.meta,  b.newb, b.tlc, b.tl, b.chg, fix_decisions ? b.xnext : nullptr,
                  fix_decisions ? b.scal + 1 : nullptr, b.dnext, b.chgc, b.chg_shift};
     int32_t* segflag = segbad ? bb.segflag : nullptr;
-    k_bundle_params<<<grid_for(nc, 256), 256, 0, s>>>(b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad, segbad,
+    launch_pdl(k_bundle_params, dim3(grid_for(nc, 256)), dim3(256), 0, s, b.meta, b.newb, nc, L, cap, bb.params, nbad, first_bad, segbad,
                                                       segflag);
     unsigned fgrid = (unsigned)((nseg * ncp + 255) / 256);
     int32_t* xalt_out = fix_decisions ? b.xnext : nullptr;
     if (nwin == 3) {
-        k_bundle_sim<3><<<(unsigned)nseg, kBundleWin * 3, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
+        launch_pdl(k_bundle_sim<3>, dim3((unsigned)nseg), dim3(kBundleWin * 3), 0, s, bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
                                                                  nbad, first_bad, segflag);
-        k_bundle_chain<3><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
+        launch_pdl(k_bundle_chain<3>, dim3(1), dim3(32), 0, s, bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3, segflag);
-        k_bundle_final<3><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
+        launch_pdl(k_bundle_final<3>, dim3(fgrid), dim3(256), 0, s, bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     } else {
-        k_bundle_sim<2><<<(unsigned)nseg, kBundleWin * 2, 0, s>>>(bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
+        launch_pdl(k_bundle_sim<2>, dim3((unsigned)nseg), dim3(kBundleWin * 2), 0, s, bb.params, b.newb, b.x, xalt, nc, L, bb.ends, bb.ckpt,
                                                                  nbad, first_bad, segflag);
-        k_bundle_chain<2><<<1, 32, 0, s>>>(bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
+        launch_pdl(k_bundle_chain<2>, dim3(1), dim3(32), 0, s, bb.params, b.newb, b.x, xalt, bb.ends, nseg, nc, L, bb.xin, bb.hit, nbad,
                                            first_bad, b.scal + 3, segflag);
-        k_bundle_final<2><<<fgrid, 256, 0, s>>>(bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
+        launch_pdl(k_bundle_final<2>, dim3(fgrid), dim3(256), 0, s, bb.params, bb.xin, bb.hit, bb.ckpt, nseg, nc, L, b.x, xalt_out, nbad,
                                                first_bad);
     }
-    if (fix_decisions) k_bundle_fix<<<grid_for(nc, 256), 256, 0, s>>>(bb.params, b.x, nc, L, nbad, first_bad, fx, bb.hit);
+    if (fix_decisions) launch_pdl(k_bundle_fix, dim3(grid_for(nc, 256)), dim3(256), 0, s, bb.params, b.x, nc, L, nbad, first_bad, fx, bb.hit);
 }
 
 
@@ -1678,6 +1720,7 @@ void launch_commit(const ChunkBufs& b, int64_t nc, cudaStream_t s) {
 __global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all, int64_t nt, int first_round,
                               uint32_t* chg, int64_t nchg, uint32_t* chgc, int64_t nchgc, uint8_t* segbad,
                               int64_t nseg) {
+    pdl_wait();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (!first_round) {
             if (scal[7]) scal[8] += 1;
@@ -1701,7 +1744,7 @@ __global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all
 void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, int64_t nchg_words, cudaStream_t s) {
     int64_t work = nt > nchg_words ? nt : nchg_words;
     int64_t nseg = b.bseg_len > 0 ? (nt * kRTileC + b.bseg_len - 1) / b.bseg_len + 1 : 0;
-    k_round_start<<<grid_for(work, 256), 256, 0, s>>>(b.scal, b.dnext, first_round ? b.dcur : nullptr, nt,
+    launch_pdl(k_round_start, dim3(grid_for(work, 256)), dim3(256), 0, s, b.scal, b.dnext, first_round ? b.dcur : nullptr, nt,
                                                        first_round ? 1 : 0, b.chg, nchg_words, b.chgc,
                                                        kChgCoarseBits / 32, b.bseg_len > 0 ? b.segbad : nullptr,
                                                        nseg);
