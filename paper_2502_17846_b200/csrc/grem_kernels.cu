@@ -3530,8 +3530,21 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
     }
 }
 
+// the state-independent half of round 1: per-(bin, CTA) record counts of a
+// chunk's edges and their scan (the scatter's private cursors).  Depends only
+// on the edges and the hub table, so the runtime computes it for chunk i+1 on
+// a side stream while chunk i's rounds run.
+void launch_bin_offsets(const uint2* e, int64_t m, const uint32_t* hub_keys, int shift, int nbins, int32_t* hist,
+                        int32_t* offs, void* temp, size_t temp_bytes, cudaStream_t s) {
+    const int G = binned_scatter_ctas();
+    kmark(KM_BIN_HIST, 1, s);
+    k_bin_hist<<<G, kScatT, 0, s>>>(e, m, hub_keys, shift, nbins, hist);
+    kmark(KM_BIN_HIST, 0, s);
+    exclusive_sum_i32(hist, offs, (int64_t)(nbins + 1) * G, temp, temp_bytes, s);
+}
+
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
-                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s) {
+                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s, bool have_offs) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_bin_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatSmem);
@@ -3544,10 +3557,7 @@ void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, 
     cudaMemsetAsync(bb.hub_flag, 0, sizeof(uint32_t) * kHubSlots, s);
     cudaMemsetAsync(bb.status, 0, sizeof(unsigned long long) * ntiles, s);
     cudaMemsetAsync(bb.ticket, 0, sizeof(unsigned int), s);
-    kmark(KM_BIN_HIST, 1, s);
-    k_bin_hist<<<G, kScatT, 0, s>>>(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist);
-    kmark(KM_BIN_HIST, 0, s);
-    exclusive_sum_i32(bb.hist, bb.offs, (int64_t)(bb.nbins + 1) * G, temp, temp_bytes, s);
+    if (!have_offs) launch_bin_offsets(e, m, b.hub_keys, bb.shift, bb.nbins, bb.hist, bb.offs, temp, temp_bytes, s);
     kmark(KM_BIN_SCATTER, 1, s);
     k_bin_scatter<<<G, kScatT, kScatSmem, s>>>(e, m, b.lab2, b.hub_keys, bb.shift, bb.nbins, bb.offs, bb.recs,
                                                bb.hub_cnt, bb.hub_flag);

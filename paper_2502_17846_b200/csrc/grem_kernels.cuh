@@ -110,8 +110,11 @@ int64_t binned_hist_entries(int nbins);
 int binned_scatter_ctas();   // CTAs of the round-1 scatter (and its histogram)
 // writes nodes, meta, tlc, pos, cntc, nbrc, newb (incl. s0) for the chunk;
 // scal[0] = N_c, scal[2] = new nodes
+void launch_bin_offsets(const uint2* e, int64_t m, const uint32_t* hub_keys, int shift, int nbins, int32_t* hist,
+                        int32_t* offs, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_count_init_binned(const uint2* e, int64_t m, int64_t n, int refine, const ChunkBufs& b,
-                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s);
+                              const BinBufs& bb, void* temp, size_t temp_bytes, cudaStream_t s,
+                              bool have_offs = false);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;

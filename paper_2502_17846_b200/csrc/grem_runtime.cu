@@ -181,6 +181,15 @@ struct grem_ctx {
     long long* h_pin = nullptr;     // [32] pinned mirror
     // cub temp
     DBuf<unsigned char> temp{"temp"};
+    // next-chunk bin offsets computed on aux_s while this chunk's rounds run
+    DBuf<int32_t> bin_hist2{"bin_hist2"}, bin_offs2{"bin_offs2"};
+    DBuf<unsigned char> aux_temp{"aux_temp"};
+    cudaStream_t aux_s = nullptr;
+    cudaEvent_t pref_go = nullptr, pref_done = nullptr;
+    const uint2* pref_e = nullptr;   // chunk whose offsets are pending in buffer pref_buf
+    int64_t pref_m = 0;
+    int pref_buf = 0, pref_nbins = 0;
+    bool pref_pending = false;       // pref_done not yet waited on by c->s
     // ingest
     void* pin_buf[2] = {nullptr, nullptr};
     size_t pin_bytes = 0;
@@ -661,7 +670,56 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
 }
 
 // ------------------------------------------------------------ process_chunk
-void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
+bool chunk_binned(const BisectArgs& a, int64_t mc) {
+    if (getenv("GREM_NO_BINNING")) return false;
+    return getenv("GREM_FORCE_BINNING") || (a.n * 9 > (48LL << 20) && mc >= (1 << 20));
+}
+
+// make c->s wait for any offsets prefetch still in flight (its buffer is about to be reused)
+void prefetch_join(grem_ctx* c) {
+    if (c->pref_pending) {
+        CK(cudaStreamWaitEvent(c->s, c->pref_done, 0));
+        c->pref_pending = false;
+    }
+}
+
+// queue the next chunk's bin offsets on aux_s (into the buffer the current
+// chunk does not use), ordered after everything queued on c->s so far
+void prefetch_offsets(grem_ctx* c, const BisectArgs& a, const uint2* ne, int64_t nm, int cur_buf) {
+    static const bool on = !getenv("GREM_NO_PREFETCH");
+    c->pref_e = nullptr;
+    if (!on || !ne || nm <= 0 || c->ingest_base || !chunk_binned(a, nm)) return;
+    int shift = binned_shift(a.n);
+    int nbins = (int)((a.n + (1LL << shift) - 1) >> shift);
+    int64_t hent = binned_hist_entries(nbins);
+    int nb = cur_buf ^ 1;
+    DBuf<int32_t>& hist = nb ? c->bin_hist2 : c->bin_hist;
+    DBuf<int32_t>& offs = nb ? c->bin_offs2 : c->bin_offs;
+    hist.ensure(hent, c->s);
+    offs.ensure(hent, c->s);
+    c->aux_temp.ensure(scan_temp_bytes(hent), c->s);
+    if (!c->aux_s) {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->aux_s, cudaStreamNonBlocking, lo));
+        CK(cudaEventCreateWithFlags(&c->pref_go, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->pref_done, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->pref_go, c->s));
+    CK(cudaStreamWaitEvent(c->aux_s, c->pref_go, 0));
+    launch_bin_offsets(ne, nm, c->hubs_on ? c->hub_table.p : nullptr, shift, nbins, hist.p, offs.p, c->aux_temp.p,
+                       c->aux_temp.cap, c->aux_s);
+    CK(cudaEventRecord(c->pref_done, c->aux_s));
+    c->kernels += 3;
+    c->pref_e = ne;
+    c->pref_m = nm;
+    c->pref_buf = nb;
+    c->pref_nbins = nbins;
+    c->pref_pending = true;
+}
+
+void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc, const uint2* next_e = nullptr,
+                   int64_t next_mc = 0) {
     cudaStream_t s = c->s;
     ChunkBufs b = chunk_bufs(c);
     CK(cudaMemsetAsync(c->d_scal, 0, sizeof(long long) * 16, s));
@@ -673,25 +731,34 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc)
         // propagation blocking when the per-node counters do not fit in L2
         const char* nb_env = getenv("GREM_NO_BINNING");
         const char* fb_env = getenv("GREM_FORCE_BINNING");   // tests: exercise the binned path on small graphs
-        binned = !nb_env && (fb_env || (a.n * 9 > (48LL << 20) && mc >= (1 << 20)));
+        (void)nb_env;
+        (void)fb_env;
+        binned = chunk_binned(a, mc);
         if (binned) {
             int shift = binned_shift(a.n);
             int nbins = (int)((a.n + (1LL << shift) - 1) >> shift);
             int64_t ntiles = binned_tiles(a.n);
+            bool have = c->pref_e == e && c->pref_m == mc && c->pref_nbins == nbins;
+            int buf = have ? c->pref_buf : 0;
+            prefetch_join(c);
+            DBuf<int32_t>& hist = buf ? c->bin_hist2 : c->bin_hist;
+            DBuf<int32_t>& offs = buf ? c->bin_offs2 : c->bin_offs;
             c->bin_recs.ensure(2 * mc + 16, s);
             int64_t hent = binned_hist_entries(nbins);
-            c->bin_hist.ensure(hent, s);
-            c->bin_offs.ensure(hent, s);
+            hist.ensure(hent, s);
+            offs.ensure(hent, s);
             ensure_temp(c, scan_temp_bytes(hent));
             c->bin_hcnt.ensure(kHubSlots, s);
             c->bin_hflag.ensure(kHubSlots, s);
             c->bin_status.ensure(ntiles + 1, s);
             c->bin_ticket.ensure(4, s);
-            BinBufs bb{c->bin_recs.p, c->bin_hist.p, c->bin_offs.p, c->bin_hcnt.p, c->bin_hflag.p, c->bin_status.p,
+            BinBufs bb{c->bin_recs.p, hist.p, offs.p, c->bin_hcnt.p, c->bin_hflag.p, c->bin_status.p,
                        c->bin_ticket.p, shift, nbins};
-            launch_count_init_binned(e, mc, a.n, a.refine, b, bb, c->temp.p, c->temp.cap, s);
-            c->kernels += 9;
+            launch_count_init_binned(e, mc, a.n, a.refine, b, bb, c->temp.p, c->temp.cap, s, have);
+            c->kernels += have ? 6 : 9;
+            prefetch_offsets(c, a, next_e, next_mc, buf);   // overlaps this chunk's rounds
         } else {
+            prefetch_join(c);
             launch_count_init(e, mc, b, s);
         }
     }
@@ -1125,11 +1192,15 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
             meter.on_chunk(mc);
             const uint2* e = a.e + lo;
             ingest_wait(c, e + mc);
+            const uint2* ne = ci + 1 < num_chunks ? e + mc : nullptr;   // next chunk of this pass
+            int64_t nm = ne ? (a.m - (lo + mc) < a.chunk ? a.m - (lo + mc) : a.chunk) : 0;
             if (pass == 0 && ci == 0) {
                 PhaseScope ps(c, PH_SEED);
+                prefetch_join(c);
+                prefetch_offsets(c, a, ne, nm, 1);   // chunk 1's offsets during the seed (into buffer 0)
                 seed_chunk(c, a, e, mc);
             } else {
-                process_chunk(c, a, e, mc);
+                process_chunk(c, a, e, mc, ne, nm);
             }
             c->stats.chunks++;
             if (a.hooks && a.hooks->on_chunk) {
@@ -1676,6 +1747,7 @@ void trim_idle_children(grem_ctx* root) {
     for (grem_ctx* ch : root->pool_all) {
         if (ch->busy) continue;
         cudaStreamSynchronize(ch->s);
+        if (ch->aux_s) cudaStreamSynchronize(ch->aux_s);
         ctx_trim_buffers(ch);
     }
 }
@@ -2010,6 +2082,9 @@ void ctx_trim_buffers(grem_ctx* c) {
     c->bsegflag.release();
     c->bin_recs.release();
     c->bin_hist.release();
+    c->bin_hist2.release();
+    c->bin_offs2.release();
+    c->aux_temp.release();
     c->bin_offs.release(); c->bin_ticket.release(); c->bin_hcnt.release(); c->bin_status.release();
     c->bin_hflag.release(); c->tl.release(); c->flag.release(); c->cnt.release(); c->nbr.release();
     c->rank.release(); c->scratch.release(); c->newid.release(); c->rankw.release();
@@ -2072,7 +2147,11 @@ void grem_destroy(grem_ctx* c) {
     c->round_exec = nullptr;
     if (c->loop_exec) cudaGraphExecDestroy(c->loop_exec);
     c->loop_exec = nullptr;
+    if (c->aux_s) cudaStreamSynchronize(c->aux_s);
     ctx_trim_buffers(c);
+    if (c->aux_s) cudaStreamDestroy(c->aux_s);
+    if (c->pref_go) cudaEventDestroy(c->pref_go);
+    if (c->pref_done) cudaEventDestroy(c->pref_done);
     for (int i = 0; i < 2; ++i) {
         if (c->pin_buf[i]) cudaFreeHost(c->pin_buf[i]);
         if (c->pin_ev[i]) cudaEventDestroy(c->pin_ev[i]);
@@ -2117,9 +2196,11 @@ int grem_trim(grem_ctx* c) {
         CK(cudaSetDevice(c->device));
         for (grem_ctx* ch : c->pool_all) {
             CK(cudaStreamSynchronize(ch->s));
+            if (ch->aux_s) CK(cudaStreamSynchronize(ch->aux_s));
             ctx_trim_buffers(ch);
         }
         CK(cudaStreamSynchronize(c->s));
+        if (c->aux_s) CK(cudaStreamSynchronize(c->aux_s));
         ctx_trim_buffers(c);
         CK(cudaDeviceSynchronize());
         cudaMemPool_t pool;
