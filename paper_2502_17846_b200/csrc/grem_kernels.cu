@@ -2082,7 +2082,10 @@ __global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __
         uint32_t khi = __reduce_min_sync(peers, (uint32_t)(key >> 32));
         uint32_t klo = __reduce_min_sync(peers, (uint32_t)(key >> 32) == khi ? (uint32_t)key : 0xFFFFFFFFu);
         if (valid && (int)(threadIdx.x & 31) == leader) {
-            atomicMin(&ckey[r], ((unsigned long long)khi << 32) | klo);
+            // the giant root's key is hit by every warp: skip the atomic when it
+            // cannot lower the key (one read per warp, not per lane)
+            unsigned long long kk = ((unsigned long long)khi << 32) | klo;
+            if (kk < ((volatile unsigned long long*)ckey)[r]) atomicMin(&ckey[r], kk);
             atomicAdd(&csize[r], (uint32_t)__popc(peers));
         }
     }

@@ -2022,6 +2022,12 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         }
         if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, s));
         CK(cudaStreamSynchronize(s));
+        // every child context is idle now: if the recursion filled most of the
+        // device, hand their workspaces back to the pool (it keeps the memory
+        // reserved, so the next call re-allocates without the OS), otherwise a
+        // repeated deep partition (Friendster k=256) starts with the children's
+        // buffers of the last one and serialises its siblings for lack of room
+        if (mem_low(0.5, c->device)) trim_idle_children(c);
     } catch (...) {
         cudaStreamSynchronize(s);
         throw;
