@@ -48,8 +48,11 @@ for name, (n, us, b) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:30]:
 if "--traffic" in sys.argv:
     out = sys.argv[sys.argv.index("--traffic") + 1]
     src = sys.argv[sys.argv.index("--source") + 1] if "--source" in sys.argv else path
-    js = {"step": {"dram_bytes": totb, "kernel_ms": tot / 1e3, "launches": sum(v[0] for v in agg.values()),
-                   "source": src}}
+    step = {k: v for k, v in agg.items() if "k_gen" not in k}   # input generation is not part of the step
+    js = {"step": {"dram_bytes": sum(v[2] for v in step.values()), "kernel_ms": sum(v[1] for v in step.values()) / 1e3,
+                   "launches": sum(v[0] for v in step.values()), "source": src,
+                   "note": "ncu launch list of one partition (GREM_NO_GRAPH=1 so every launch is listed), "
+                           "cold caches, serialised; k_gen (input generation) excluded"}}
     for name, (n, us, b) in agg.items():
         js[name.split("::")[-1]] = {"dram_bytes_per_launch": b / n, "launches": n, "avg_launch_us_cold": us / n,
                                     "source": src}
