@@ -1709,19 +1709,39 @@ bool mem_low(double frac, int device) {
     return low;
 }
 
+// A bounded pool of child contexts (GREM_MAX_CTX, default 24): an idle one
+// that last ran the same subtree position is preferred (its workspaces have
+// the right sizes), else any idle one, else a new one below the cap; at the
+// cap the caller runs the sibling on its own context.  One context per subtree
+// position (round 1) held k-1 sets of workspaces across calls, which at
+// Friendster k=256 filled the device and serialised later calls.
 grem_ctx* ctx_acquire(grem_ctx* root, long long key) {
+    static const size_t kMaxCtx = getenv("GREM_MAX_CTX") ? (size_t)atoi(getenv("GREM_MAX_CTX")) : 24;
     grem_ctx* ch = nullptr;
     {
         std::lock_guard<std::mutex> lk(root->pool_mu);
         for (auto& kv : root->pool_keyed)
-            if (kv.first == key) ch = kv.second;
+            if (kv.first == key && !kv.second->busy) ch = kv.second;
+        if (!ch)
+            for (grem_ctx* c2 : root->pool_all)
+                if (!c2->busy) {
+                    ch = c2;
+                    break;
+                }
         if (!ch) {
+            if (root->pool_all.size() >= kMaxCtx) return nullptr;
             ch = new grem_ctx();
             ch->root = root;
             init_ctx(ch, root->device, true);
             root->pool_all.push_back(ch);
-            root->pool_keyed.push_back({key, ch});
         }
+        bool keyed = false;
+        for (auto& kv : root->pool_keyed)
+            if (kv.second == ch) {
+                kv.first = key;
+                keyed = true;
+            }
+        if (!keyed) root->pool_keyed.push_back({key, ch});
         ch->busy = true;
     }
     memset(&ch->stats, 0, sizeof(ch->stats));
@@ -1912,13 +1932,18 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         par = !mem_low(kSpawnFree, c->device);
     }
     static const bool defer = getenv("GREM_DEFER") && atoi(getenv("GREM_DEFER")) > 0;
+    int big = (e_off[1] - e_off[0]) >= (e_off[2] - e_off[1]) ? 0 : 1;   // stays on this context
+    grem_ctx* dch = nullptr;
+    if (par && defer && c == c->root) {
+        dch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
+        if (!dch) par = false;
+    }
     if (par && defer && c == c->root) {
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, s));
-        int big = (e_off[1] - e_off[0]) >= (e_off[2] - e_off[1]) ? 0 : 1;
         int sm = 1 - big;
-        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + sm * (p_level / 2)));
+        grem_ctx* ch = dch;
         const uint2* se = side_e[sm];
         int64_t sm_m = e_off[sm + 1] - e_off[sm], sm_n = n_off[sm + 1] - n_off[sm];
         const int32_t* so = sub_o + n_off[sm];
@@ -1934,12 +1959,15 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         side_call(c, big);
         return;
     }
+    grem_ctx* ch = nullptr;
+    if (par && !(defer && c == c->root)) {
+        ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
+        par = ch != nullptr;   // context pool at its cap: siblings in sequence
+    }
     if (par) {
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, s));
-        int big = (e_off[1] - e_off[0]) >= (e_off[2] - e_off[1]) ? 0 : 1;   // stays on this context
-        grem_ctx* ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
         std::exception_ptr err = nullptr;
         std::thread th([&] {
             try {
@@ -2022,12 +2050,6 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         }
         if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, s));
         CK(cudaStreamSynchronize(s));
-        // every child context is idle now: if the recursion filled most of the
-        // device, hand their workspaces back to the pool (it keeps the memory
-        // reserved, so the next call re-allocates without the OS), otherwise a
-        // repeated deep partition (Friendster k=256) starts with the children's
-        // buffers of the last one and serialises its siblings for lack of room
-        if (mem_low(0.5, c->device)) trim_idle_children(c);
     } catch (...) {
         cudaStreamSynchronize(s);
         throw;
