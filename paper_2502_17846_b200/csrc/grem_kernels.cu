@@ -497,17 +497,26 @@ static inline unsigned edge_grid(int64_t m, int per_sm = 4) {   // per_sm: resid
     if (blocks > cap) blocks = cap;
     return (unsigned)(blocks < 1 ? 1 : blocks);
 }
+// the delta pass loads a 24 KB shared-memory prologue per CTA (hub table,
+// coarse filter): small chunks get >= 16 edges per thread so that prologue
+// does not outweigh their edges (a 2.75M-edge chunk read 14 MB of prologue)
+static inline unsigned delta_grid(int64_t m, int per_sm) {
+    int64_t blocks = (m + 16 * kEdgeThreads - 1) / (16 * kEdgeThreads);
+    int64_t lo = num_sms(), cap = (int64_t)num_sms() * per_sm;
+    blocks = blocks < lo ? lo : (blocks > cap ? cap : blocks);
+    return (unsigned)blocks;
+}
 
 void launch_count_init(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s) {
     k_count_init<<<edge_grid(m), kEdgeThreads, 0, s>>>(e, m, b.lab, b.cnt, b.flag, b.hub_keys);
 }
 void launch_count_delta(const uint2* e, int64_t m, const ChunkBufs& b, cudaStream_t s, bool staged) {
     if (staged) {
-        launch_pdl(k_count_delta<true>, dim3(edge_grid(m, 3)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys,
+        launch_pdl(k_count_delta<true>, dim3(delta_grid(m, 3)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys,
                                                                      b.gate, b.dcur, b.chgc, b.chg_shift);
         return;
     }
-    launch_pdl(k_count_delta<false>, dim3(edge_grid(m, GREM_CD_MINB)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
+    launch_pdl(k_count_delta<false>, dim3(delta_grid(m, GREM_CD_MINB)), dim3(kEdgeThreads), 0, s, e, m, b.tl, b.chg, b.rankw, b.cntc, b.hub_keys, b.gate, b.dcur,
                                                               b.chgc, b.chg_shift);
 }
 
