@@ -110,6 +110,7 @@ struct grem_ctx {
     std::mutex pool_mu;
     std::vector<grem_ctx*> pool_all, pool_idle;
     bool busy = false;   // child context: a subtree is running on it (guarded by the root's pool_mu)
+    int64_t ws_m = 0;    // child context: edges of the largest subtree its workspaces were sized for
     std::vector<std::pair<long long, grem_ctx*>> pool_keyed;   // subtree position -> context
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_open;
     std::vector<cudaEvent_t> ev_pool;
@@ -1769,6 +1770,7 @@ void trim_idle_children(grem_ctx* root) {
         cudaStreamSynchronize(ch->s);
         if (ch->aux_s) cudaStreamSynchronize(ch->aux_s);
         ctx_trim_buffers(ch);
+        ch->ws_m = 0;
     }
 }
 
@@ -1963,6 +1965,16 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     if (par && !(defer && c == c->root)) {
         ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
         par = ch != nullptr;   // context pool at its cap: siblings in sequence
+        if (ch) {   // a context sized for a far bigger subtree first gives its workspaces back
+            int64_t ms = e_off[(1 - big) + 1] - e_off[1 - big];
+            if (ch->ws_m > 8 * ms + (1 << 22)) {
+                CK(cudaStreamSynchronize(ch->s));
+                if (ch->aux_s) CK(cudaStreamSynchronize(ch->aux_s));
+                ctx_trim_buffers(ch);
+                ch->ws_m = 0;
+            }
+            if (ms > ch->ws_m) ch->ws_m = ms;
+        }
     }
     if (par) {
         cudaEvent_t ready;
