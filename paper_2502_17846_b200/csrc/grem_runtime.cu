@@ -1927,7 +1927,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
     bool mine0 = pc.shard_rank >= sr0[0] && pc.shard_rank < sr1[0];
     bool mine1 = pc.shard_rank >= sr0[1] && pc.shard_rank < sr1[1];
     bool both = (n_off[1] > 0) && (n_off[2] - n_off[1] > 0) && mine0 && mine1;
-    static const double kSpawnFree = getenv("GREM_SPAWN_FREE") ? atof(getenv("GREM_SPAWN_FREE")) : 0.30;
+    static const double kSpawnFree = getenv("GREM_SPAWN_FREE") ? atof(getenv("GREM_SPAWN_FREE")) : 0.15;
     bool par = both && !(pc.hooks && pc.hooks->meter) && !getenv("GREM_SERIAL_SIBLINGS");
     if (par && mem_low(kSpawnFree, c->device)) {   // reclaim idle children first, then decide
         trim_idle_children(c->root);
