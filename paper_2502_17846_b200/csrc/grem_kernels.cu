@@ -1752,7 +1752,7 @@ __global__ void k_round_start(long long* scal, uint8_t* dnext, uint8_t* dcur_all
 }
 void launch_round_start(const ChunkBufs& b, int64_t nt, bool first_round, int64_t nchg_words, cudaStream_t s) {
     int64_t work = nt > nchg_words ? nt : nchg_words;
-    int64_t nseg = b.bseg_len > 0 ? (nt * kRTileC + b.bseg_len - 1) / b.bseg_len + 1 : 0;
+    int64_t nseg = b.bseg_len > 0 ? b.bseg_n + 1 : 0;   // (the buffer holds bseg_n + 2 flags)
     launch_pdl(k_round_start, dim3(grid_for(work, 256)), dim3(256), 0, s, b.scal, b.dnext, first_round ? b.dcur : nullptr, nt,
                                                        first_round ? 1 : 0, b.chg, nchg_words, b.chgc,
                                                        kChgCoarseBits / 32, b.bseg_len > 0 ? b.segbad : nullptr,

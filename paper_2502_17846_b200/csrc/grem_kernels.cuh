@@ -58,6 +58,7 @@ struct ChunkBufs {
     int chg_shift;
     uint8_t* segbad;            // per bundle segment (bseg_len nodes): a tie of this round was mis-speculated
     int64_t bseg_len;
+    int64_t bseg_n;             // segments of this chunk: ceil(N_c / bseg_len)
     // per scan tile
     Clamp* tile_agg;
     Clamp* tile_inc;            // single-pass round: inclusive look-back prefixes

@@ -456,6 +456,7 @@ ChunkBufs chunk_bufs(grem_ctx* c) {
     b.dnext = c->dirty1.p;
     b.segbad = c->bsegbad.p;
     b.bseg_len = 0;   // set per chunk (process_chunk: bundle_segment_len(nc))
+    b.bseg_n = 0;
     return b;
 }
 
@@ -789,6 +790,10 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc,
         c->kernels += 3;
     }
     b.bseg_len = bundle_segment_len(nc);
+    b.bseg_n = (nc + b.bseg_len - 1) / b.bseg_len;
+    c->bsegbad.ensure(b.bseg_n + 2, s);   // (sized from the chunk-node capacity already; never less than this chunk)
+    c->bsegflag.ensure(b.bseg_n + 2, s);
+    b.segbad = c->bsegbad.p;
     // identity padding up to whole round tiles (inactive nodes, meta 0)
     {
         int64_t padded = (nc + 1 + kScanTile - 1) / kScanTile * kScanTile;
