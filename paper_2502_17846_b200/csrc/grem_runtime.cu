@@ -81,6 +81,11 @@ struct DBuf {
         p = nullptr;
         cap = 0;
     }
+    void release_async(cudaStream_t s) {   // stream-ordered: no device-wide synchronisation
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        cap = 0;
+    }
 };
 
 }  // namespace
@@ -1781,6 +1786,15 @@ void trim_idle_children(grem_ctx* root) {
 
 void ctx_release(grem_ctx* parent, grem_ctx* ch) {
     prof_collect(ch);
+    // the finished subtree's induced subgraphs are dead: hand the level arenas
+    // back to the pool (stream-ordered; the pool keeps the memory, so the next
+    // subtree re-allocates without the OS).  A pooled context otherwise keeps
+    // the union of every subtree's arenas it ever ran (Friendster k=256 repeat
+    // calls crept into low-memory serialisation).
+    for (int l = 0; l < 40; ++l) {
+        ch->rec_e[l].release_async(ch->s);
+        ch->rec_o[l].release_async(ch->s);
+    }
     {
         std::lock_guard<std::mutex> lk(parent->root->pool_mu);
         ch->busy = false;
