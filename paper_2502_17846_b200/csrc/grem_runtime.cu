@@ -1986,7 +1986,7 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         par = ch != nullptr;   // context pool at its cap: siblings in sequence
         if (ch) {   // a context sized for a far bigger subtree first gives its workspaces back
             int64_t ms = e_off[(1 - big) + 1] - e_off[1 - big];
-            if (ch->ws_m > 8 * ms + (1 << 22)) {
+            if (ch->ws_m > 2 * ms + (1 << 22)) {
                 CK(cudaStreamSynchronize(ch->s));
                 if (ch->aux_s) CK(cudaStreamSynchronize(ch->aux_s));
                 ctx_trim_buffers(ch);
