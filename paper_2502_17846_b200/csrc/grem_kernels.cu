@@ -2071,7 +2071,18 @@ void launch_cc_csr(const int32_t* start, const uint32_t* adj, int64_t nc, uint32
 // highest-degree, lowest-index node; key = (~degree << 32) | index, min wins.
 __global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __restrict__ selfc,
                             const uint32_t* __restrict__ parent, int64_t nc, unsigned long long* ckey,
-                            uint32_t* csize) {
+                            uint32_t* csize, const unsigned long long* giant) {
+    // the giant component's key and size are accumulated per block in shared
+    // memory (one atomic per block instead of one per warp on two L2 words:
+    // 1.9M same-address atomics per papers100M level-0 seed)
+    __shared__ unsigned int s_gcnt;
+    __shared__ unsigned long long s_gkey;
+    const uint32_t g = giant ? (uint32_t)*giant : 0xFFFFFFFFu;
+    if (threadIdx.x == 0) {
+        s_gcnt = 0u;
+        s_gkey = ~0ULL;
+    }
+    __syncthreads();
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nc; base += stride) {
         int64_t i = base + (threadIdx.x & 31);
@@ -2082,27 +2093,33 @@ __global__ void k_comp_keys(const int32_t* __restrict__ start, const int32_t* __
             uint32_t d = (uint32_t)(start[i + 1] - start[i] - selfc[i]);
             key = ((unsigned long long)(0xFFFFFFFFu - d) << 32) | (unsigned long long)i;
         }
-        // one atomic per (warp, component): the lanes of a component (the giant
-        // fills most warps) reduce their keys first -- min of the degree part,
-        // then of the index among the lanes holding it -- instead of each lane
-        // racing a read-then-atomic on the root's key (one L2 address)
+        // one update per (warp, component): min of the degree part, then of
+        // the index among the lanes holding it
         unsigned peers = __match_any_sync(0xffffffffu, r);
         int leader = __ffs(peers) - 1;
         uint32_t khi = __reduce_min_sync(peers, (uint32_t)(key >> 32));
         uint32_t klo = __reduce_min_sync(peers, (uint32_t)(key >> 32) == khi ? (uint32_t)key : 0xFFFFFFFFu);
         if (valid && (int)(threadIdx.x & 31) == leader) {
-            // the giant root's key is hit by every warp: skip the atomic when it
-            // cannot lower the key (one read per warp, not per lane)
             unsigned long long kk = ((unsigned long long)khi << 32) | klo;
-            if (kk < ((volatile unsigned long long*)ckey)[r]) atomicMin(&ckey[r], kk);
-            atomicAdd(&csize[r], (uint32_t)__popc(peers));
+            if (r == g) {
+                atomicAdd(&s_gcnt, (unsigned int)__popc(peers));
+                if (kk < s_gkey) atomicMin(&s_gkey, kk);
+            } else {
+                atomicMin(&ckey[r], kk);
+                atomicAdd(&csize[r], (uint32_t)__popc(peers));
+            }
         }
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_gcnt) {
+        atomicAdd(&csize[g], s_gcnt);
+        atomicMin(&ckey[g], s_gkey);
+    }
 }
-void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s) {
+void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s, const unsigned long long* giant) {
     cudaMemsetAsync(sb.ckey, 0xFF, sizeof(unsigned long long) * nc, s);
     cudaMemsetAsync(sb.csize, 0, sizeof(uint32_t) * nc, s);
-    k_comp_keys<<<grid_for(nc, 256), 256, 0, s>>>(sb.start, sb.cursor, sb.parent, nc, sb.ckey, sb.csize);
+    k_comp_keys<<<grid_for(nc, 256), 256, 0, s>>>(sb.start, sb.cursor, sb.parent, nc, sb.ckey, sb.csize, giant);
 }
 
 struct RootPred {

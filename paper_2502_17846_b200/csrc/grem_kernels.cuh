@@ -217,7 +217,7 @@ void launch_cc(const uint2* e, int64_t m, const int32_t* rank, uint32_t* parent,
                cudaStream_t s);
 void launch_cc_csr(const int32_t* start, const uint32_t* adj, int64_t nc, uint32_t* parent, uint32_t* scratch,
                    unsigned long long* d_giant, cudaStream_t s);
-void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s);
+void launch_comp_keys(const SeedBufs& sb, int64_t nc, cudaStream_t s, const unsigned long long* giant = nullptr);
 void launch_select_roots(const SeedBufs& sb, int64_t nc, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_root_keys(const SeedBufs& sb, int64_t nroots, cudaStream_t s);
 void launch_boundary(const SeedBufs& sb, int64_t nroots, long long target, void* temp, size_t temp_bytes,

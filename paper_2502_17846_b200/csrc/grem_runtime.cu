@@ -563,7 +563,7 @@ void seed_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc) {
         seq.to(PH_SEED_CC);
         launch_cc_csr(c->start.p, c->adj.p, nc, c->parent.p, c->roots.p,
                       reinterpret_cast<unsigned long long*>(c->d_sscal + 13), s);
-        launch_comp_keys(sb, nc, s);
+        launch_comp_keys(sb, nc, s, reinterpret_cast<unsigned long long*>(c->d_sscal + 13));
         ensure_temp(c, select_nodes_temp_bytes(nc));
         launch_select_roots(sb, nc, c->temp.p, c->temp.cap, s);
         c->kernels += 8;
