@@ -1193,6 +1193,8 @@ void bisect_core(grem_ctx* c, const BisectArgs& a) {
     }
     CK(cudaMemsetAsync(c->d_sizes, 0, sizeof(long long) * 2, s));
     c->live_n = a.n;
+    prefetch_join(c);      // a prefetch is only ever consumed within its own bisection
+    c->pref_e = nullptr;
     detect_hubs(c, a);
     int64_t num_chunks = a.m ? (a.m + a.chunk - 1) / a.chunk : 0;
     for (int pass = 0; pass < a.passes; ++pass) {
