@@ -1,0 +1,5 @@
+#!/bin/bash
+O=gpurun_out/r02_2gpu
+mkdir -p $O
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus 2 --steps 5 --warmup 3 > $O/bench_2gpu.json 2> $O/bench_2gpu.err
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 bench.py --gpus 2 --steps 5 --warmup 3 --workload friendster --k 256 > $O/bench_2gpu_f256.json 2> $O/bench_2gpu_f256.err
