@@ -9,6 +9,7 @@
 // All edge data stays resident in HBM for the whole call; per-node state is
 // O(n) device arrays (grem_core.cuh).  The host only reads a handful of
 // scalars per chunk round (N_c, labels changed).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 
@@ -147,6 +148,9 @@ struct grem_ctx {
     DBuf<uint32_t> chg{"chg"}, chgc{"chgc"}, chg2{"chg2"}, chgc2{"chgc2"};
     cudaGraphExec_t round_exec = nullptr;   // replayed pair of rounds (process_chunk)
     cudaGraphExec_t loop_exec = nullptr;    // device-side round loop (conditional WHILE node)
+    // root context: its stream on the dense SM partition (green context) and
+    // the full-GPU stream it started on (see green_parts / recurse)
+    cudaStream_t s_full = nullptr, s_dense = nullptr;
     DBuf<uint8_t> dirty0{"dirty0"}, dirty1{"dirty1"};
     DBuf<int32_t> newb{"newb"}, x{"x"}, xalt{"xalt"}, xnext{"xnext"}, bends{"bends"}, bxin{"bxin"}, bhit{"bhit"}, bparams{"bparams"},
         bckpt{"bckpt"};
@@ -1657,6 +1661,46 @@ void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_
 // Stream priorities: the root context carries the dense chain of the
 // recursion (the larger side always stays on it), child contexts the smaller
 // subtrees.  GREM_PRIO: 0 = none, 1 = root high, 2 = children high.
+// SM partitions (green contexts, driver API): once a recursion has split into
+// the dense chain and its sibling subtrees, the chain runs on a "dense"
+// partition and every child context on a "sparse" one, so the
+// latency-bound rounds of the sparse subtrees stop queueing behind the
+// chain's SM-filling kernels (and vice versa).  GREM_GREEN_SPARSE_SMS (default
+// 32, a multiple of 8; 0 disables): the sparse partition's SM count.  Streams
+// of both partitions share the device's memory pool with the primary context
+// (checked by tools/micro/green_test.cu on a B200).
+struct GreenParts {
+    bool ok = false;
+    CUgreenCtx dense = nullptr, sparse = nullptr;
+};
+GreenParts* green_parts(int device) {
+    static std::mutex mu;
+    static GreenParts parts[16];
+    static bool tried[16] = {false};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 16) return nullptr;
+    GreenParts& g = parts[device];
+    if (!tried[device]) {
+        tried[device] = true;
+        int want = getenv("GREM_GREEN_SPARSE_SMS") ? atoi(getenv("GREM_GREEN_SPARSE_SMS")) : 32;
+        CUdevice dev;
+        CUdevResource res, grp[1], rest;
+        unsigned nb = 1;
+        CUdevResourceDesc dd, ds;
+        if (want > 0 && cuDeviceGet(&dev, device) == CUDA_SUCCESS &&
+            cuDeviceGetDevResource(dev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+            (int)res.sm.smCount > 2 * want &&
+            cuDevSmResourceSplitByCount(grp, &nb, &res, &rest, 0, (unsigned)want) == CUDA_SUCCESS && nb == 1 &&
+            cuDevResourceGenerateDesc(&ds, grp, 1) == CUDA_SUCCESS &&
+            cuDevResourceGenerateDesc(&dd, &rest, 1) == CUDA_SUCCESS &&
+            cuGreenCtxCreate(&g.sparse, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+            cuGreenCtxCreate(&g.dense, dd, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS)
+            g.ok = true;
+        cudaGetLastError();
+    }
+    return g.ok ? &g : nullptr;
+}
+
 void init_ctx(grem_ctx* c, int device, bool child = false) {
     c->device = device;
     CK(cudaSetDevice(device));
@@ -1664,7 +1708,16 @@ void init_ctx(grem_ctx* c, int device, bool child = false) {
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     bool high = (prio_mode == 1 && !child) || (prio_mode == 2 && child);
-    CK(cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, (prio_mode && high) ? hi : lo));
+    GreenParts* gp = green_parts(device);
+    CUstream cs = nullptr;
+    if (child && gp && cuGreenCtxStreamCreate(&cs, gp->sparse, CU_STREAM_NON_BLOCKING,
+                                              (prio_mode && high) ? hi : lo) == CUDA_SUCCESS)
+        c->s = (cudaStream_t)cs;
+    else
+        CK(cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, (prio_mode && high) ? hi : lo));
+    if (!child && gp && cuGreenCtxStreamCreate(&cs, gp->dense, CU_STREAM_NON_BLOCKING,
+                                               prio_mode == 1 ? hi : lo) == CUDA_SUCCESS)
+        c->s_dense = (cudaStream_t)cs;
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
     CK(cudaMalloc(&c->d_sizes, sizeof(long long) * 2));
@@ -1987,6 +2040,17 @@ void recurse(grem_ctx* c, PartCtx& pc, const uint2* e, int64_t m, int64_t n, con
         return;
     }
     grem_ctx* ch = nullptr;
+    if (par && !(defer && c == c->root) && c == c->root && c->s_dense && c->s != c->s_dense) {
+        // first split of the recursion: from here on the chain runs on the
+        // dense SM partition and the spawned subtrees on the sparse one
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(ev, c->s));
+        CK(cudaStreamWaitEvent(c->s_dense, ev, 0));
+        CK(cudaEventDestroy(ev));
+        c->s_full = c->s;
+        c->s = c->s_dense;
+    }
     if (par && !(defer && c == c->root)) {
         ch = ctx_acquire(c->root, ((long long)(level + 1) << 40) | (leaf_base + (1 - big) * (p_level / 2)));
         par = ch != nullptr;   // context pool at its cap: siblings in sequence
@@ -2053,6 +2117,22 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
         CK(cudaEventRecord(g_dbg_t0, s));
     }
     mem_sample(c->device);
+    struct BackToFull {   // the root context leaves the call on its full-GPU stream again
+        grem_ctx* c;
+        ~BackToFull() {
+            if (!c->s_full) return;
+            cudaEvent_t ev;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(ev, c->s);
+                cudaStreamWaitEvent(c->s_full, ev, 0);
+                cudaEventDestroy(ev);
+            } else {
+                cudaStreamSynchronize(c->s);
+            }
+            c->s = c->s_full;
+            c->s_full = nullptr;
+        }
+    } back_to_full{c};
     PartCtx pc{n, cfg, hooks, fin, shard_rank};
     // incremental cut (extraction drops + per-leaf cut passes) only on request:
     // measured slower and noisier than one final pass (the leaf passes compete
@@ -2085,13 +2165,14 @@ void partition_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, int64_t 
             count_cuts_dev(c, d, m, fin, n, rep, pc.track_cut ? (long long)pc.cut : -1);
             c->stats.path_bytes += 10 * m;   // final cut pass (SURVEY 8(d) formula; done incrementally here)
         }
-        if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, s));
-        CK(cudaStreamSynchronize(s));
+        // (c->s: the root may have moved to its dense-partition stream)
+        if (labels_out) CK(cudaMemcpyAsync(labels_out, fin, sizeof(int32_t) * n, cudaMemcpyDefault, c->s));
+        CK(cudaStreamSynchronize(c->s));
     } catch (...) {
-        cudaStreamSynchronize(s);
+        cudaStreamSynchronize(c->s);
         throw;
     }
-    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(c->s));
 }
 
 template <class F>

@@ -331,6 +331,7 @@ def test_pinned_host_edges_overlapped_ingest():
                                  {"GREM_ROUND_BATCH": "1"}, {"GREM_ROUND_BATCH": "3", "GREM_PRIO": "2"},
                                  {"GREM_BUNDLE_K": "3"}, {"GREM_INCREMENTAL_CUT": "1"}, {"GREM_BUNDLE_NO_SKIP": "1"},
                                  {"GREM_SPAWN_FREE": "0.99"}, {"GREM_DEVICE_LOOP": "1"}, {"GREM_NO_PDL": "1"}, {"GREM_NO_PREFETCH": "1"}, {"GREM_MAX_CTX": "2"},
+                                 {"GREM_GREEN_SPARSE_SMS": "0"}, {"GREM_GREEN_SPARSE_SMS": "64"},
                                  {"GREM_NO_STAGED_DELTA": "1"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_alternative_schedules_are_exact(golden_dir, env):
