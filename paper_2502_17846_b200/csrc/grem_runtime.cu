@@ -893,7 +893,7 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc,
     // a graph with a conditional node per chunk cost more than the host round
     // trips it saves (papers100M k=16: 664 vs 608 ms, profiles/r02_ab_devloop.txt).
     static const bool dev_loop_on = getenv("GREM_DEVICE_LOOP") != nullptr;
-    const bool dev_loop = use_graph && dev_loop_on;
+    const bool dev_loop = use_graph && dev_loop_on && !c->root->s_dense;   // (not with green-context streams)
     const long long max_rounds = nc + 6;
     bool looped = false;
     for (int r = 1;;) {
@@ -1665,10 +1665,13 @@ void bisect_entry(grem_ctx* c, const uint2* d, int64_t m, int64_t n, const grem_
 // the dense chain and its sibling subtrees, the chain runs on a "dense"
 // partition and every child context on a "sparse" one, so the
 // latency-bound rounds of the sparse subtrees stop queueing behind the
-// chain's SM-filling kernels (and vice versa).  GREM_GREEN_SPARSE_SMS (default
-// 32, a multiple of 8; 0 disables): the sparse partition's SM count.  Streams
+// chain's SM-filling kernels (and vice versa).  GREM_GREEN_SPARSE_SMS (a
+// multiple of 8; default 0 = off): the sparse partition's SM count.  Streams
 // of both partitions share the device's memory pool with the primary context
-// (checked by tools/micro/green_test.cu on a B200).
+// (checked by tools/micro/green_test.cu on a B200).  Measured slower than
+// sharing the whole GPU (papers100M k=16: 16 / 32 / 48 SMs -> 1050 / 672 /
+// 610 ms vs 588 ms, profiles/r02_ab_green.txt): the sparse subtrees need more
+// than a slice, and the chain loses the SMs it would have borrowed.
 struct GreenParts {
     bool ok = false;
     CUgreenCtx dense = nullptr, sparse = nullptr;
@@ -1682,7 +1685,7 @@ GreenParts* green_parts(int device) {
     GreenParts& g = parts[device];
     if (!tried[device]) {
         tried[device] = true;
-        int want = getenv("GREM_GREEN_SPARSE_SMS") ? atoi(getenv("GREM_GREEN_SPARSE_SMS")) : 32;
+        int want = getenv("GREM_GREEN_SPARSE_SMS") ? atoi(getenv("GREM_GREEN_SPARSE_SMS")) : 0;
         CUdevice dev;
         CUdevResource res, grp[1], rest;
         unsigned nb = 1;
