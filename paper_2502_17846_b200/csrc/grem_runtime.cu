@@ -956,9 +956,14 @@ void process_chunk(grem_ctx* c, const BisectArgs& a, const uint2* e, int64_t mc,
                 CK(cudaGraphDestroy(g));
                 graph_ready = true;
             }
-            CK(cudaGraphLaunch(c->round_exec, s));
-            c->kernels += pair_kernels;
-            r += 2;
+            // GREM_GRAPH_REPLAYS pairs per host check (A/B knob, default 1):
+            // rounds past the fixpoint are gated no-ops
+            static const int replays = getenv("GREM_GRAPH_REPLAYS") ? std::max(1, atoi(getenv("GREM_GRAPH_REPLAYS"))) : 1;
+            for (int q = 0; q < replays; ++q) {
+                CK(cudaGraphLaunch(c->round_exec, s));
+                c->kernels += pair_kernels;
+                r += 2;
+            }
         } else {
             issue(r);
             r += 1;
