@@ -9,10 +9,10 @@ s = synth.SHAPES[name]
 L = _abi.lib(); ctx = grem.context(); ptr = ctypes.c_void_p()
 assert L.grem_device_alloc(ctx, s.num_edges * 8, ctypes.byref(ptr)) == 0
 assert L.grem_gen_edges_device(ctx, s.num_nodes, s.beta, s.seed, 0, s.num_edges, ptr) == 0
-grem.set_profiling(True)
+grem.set_profiling(2 if os.environ.get("PHASE_K") else True)
 for r in range(3):
     lab, rep = grem.partition_edges(None, s.num_nodes, k, GremConfig(chunk_frac=0.1), on_device_ptr=ptr.value,
                                     num_edges=s.num_edges)
 st = grem.last_stats(); ph = grem.phase_times()
 print(f"[{os.environ.get('GREM_LIB', 'default').split('/')[-1]}] total {st['ms_total']:.1f} ms  " +
-      " ".join(f"{kk}={v[0]:.1f}" for kk, v in sorted(ph.items()) if v[1] and not kk.startswith("k.")), flush=True)
+      " ".join(f"{kk}={v[0]:.1f}" for kk, v in sorted(ph.items()) if v[1] and (os.environ.get("PHASE_K") or not kk.startswith("k."))), flush=True)
