@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
         int lu = lab[u], lv = lab[v];
         if (lv >= 0) {
             unsigned long long inc = lv == 0 ? 1ULL : (1ULL << 32);
-            if (hu >= 0) atomicAdd(&s_cnt[hu], inc);
+            if (hu >= 0) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + hu) + (lv == 0 ? 0 : 1), 1u);   // native 32-bit half
             else atomicAdd(&cnt[u], inc);
         } else if (hu >= 0) {
             s_flag[hu] = 1;
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kEdgeThreads) k_count_init(const uint2* __rest
         }
         if (lu >= 0) {
             unsigned long long inc = lu == 0 ? 1ULL : (1ULL << 32);
-            if (hv >= 0) atomicAdd(&s_cnt[hv], inc);
+            if (hv >= 0) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + hv) + (lu == 0 ? 0 : 1), 1u);   // native 32-bit half
             else atomicAdd(&cnt[v], inc);
         } else if (hv >= 0) {
             s_flag[hv] = 1;
@@ -387,6 +387,14 @@ __device__ __forceinline__ void mark_changed_coarse(uint32_t* chgc, int shift, u
 #ifndef GREM_CD_MINB
 #define GREM_CD_MINB 4   // CTAs per SM the plain delta kernel's register budget allows (A/B build knob)
 #endif
+// a hub's label-code change (prev -> cur) on its two 32-bit count halves
+__device__ __forceinline__ void hub_delta_add(uint2* c, int cur, int prev) {
+    unsigned int* h = reinterpret_cast<unsigned int*>(c);
+    if (cur == 1) atomicAdd(h, 1u);
+    else if (cur == 2) atomicAdd(h + 1, 1u);
+    if (prev == 1) atomicAdd(h, 0xFFFFFFFFu);
+    else if (prev == 2) atomicAdd(h + 1, 0xFFFFFFFFu);
+}
 template <bool STAGED>
 __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_count_delta(const uint2* __restrict__ e, int64_t m,
                                                               const uint8_t* __restrict__ tl,
@@ -400,10 +408,13 @@ __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_cou
     pdl_wait();
     if (gate && *gate == 0) return;   // previous round changed nothing (converged)
     __shared__ __align__(8) uint32_t s_keys[kHubSlots];
-    __shared__ unsigned long long s_cnt[kHubSlots];
+    // per hub slot: {label-0, label-1} count deltas as two 32-bit halves
+    // (native shared atomics; a 64-bit shared atomicAdd is a CAS spin loop),
+    // merged as hi * 2^32 + (signed) lo -- the same 64-bit packed delta
+    __shared__ uint2 s_cnt[kHubSlots];
     __shared__ uint32_t s_chgc[kChgCoarseBits / 32];
     hub_load(s_keys, hub_keys);
-    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = 0ULL;
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_cnt[k] = make_uint2(0u, 0u);
     for (int k = threadIdx.x; k < kChgCoarseBits / 32; k += blockDim.x) s_chgc[k] = chgc[k];
     __syncthreads();
     int64_t lo, hi;
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_cou
                 int cur = t[j] & 0xF, prev = t[j] >> 4;
                 unsigned long long d = enc_label(cur) - enc_label(prev);
                 if (hb[j] >= 0) {
-                    atomicAdd(&s_cnt[hb[j]], d);
+                    hub_delta_add(s_cnt + hb[j], cur, prev);
                 } else {
                     int32_t pb = (int32_t)(q[j].y + __popc(q[j].x & ((1u << (B[j] & 31)) - 1u)));
                     atomicAdd(&cntc[pb], d);
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_cou
             unsigned long long d = enc_label(cur) - enc_label(prev);
             int hb = hub_find(s_keys, b);
             if (hb >= 0) {
-                atomicAdd(&s_cnt[hb], d);
+                hub_delta_add(s_cnt + hb, cur, prev);
             } else {
                 int32_t pb = (int32_t)word_rank(rankw, b);   // L2-resident succinct map
                 atomicAdd(&cntc[pb], d);
@@ -483,9 +494,11 @@ __global__ void __launch_bounds__(kEdgeThreads, STAGED ? 3 : GREM_CD_MINB) k_cou
     __syncthreads();
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
         uint32_t key = s_keys[k];
-        if (key != kHubEmpty && s_cnt[k]) {
+        uint2 hc = s_cnt[k];
+        unsigned long long dk = ((unsigned long long)hc.y << 32) + (unsigned long long)(long long)(int32_t)hc.x;
+        if (key != kHubEmpty && dk) {
             int32_t pk = (int32_t)word_rank(rankw, key);
-            atomicAdd(&cntc[pk], s_cnt[k]);
+            atomicAdd(&cntc[pk], dk);
             dirty[pk / kRTileC] = 1;
         }
     }
@@ -3257,6 +3270,10 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
                                                         unsigned long long* __restrict__ hub_cnt,
                                                         uint32_t* __restrict__ hub_flag) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // per hub slot {label-0 count, label-1 count} as two 32-bit halves: native
+    // 32-bit shared atomics (a 64-bit shared atomicAdd compiles to a CAS spin
+    // loop, which on the hot hub slots was a third of the kernel's shared
+    // wavefronts, ncu r02_final)
     unsigned long long* s_hcnt = reinterpret_cast<unsigned long long*>(smem_raw);
     uint32_t* s_keys = reinterpret_cast<uint32_t*>(s_hcnt + kHubSlots);
     uint32_t* s_hflag = s_keys + kHubSlots;
@@ -3300,13 +3317,13 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
                     int hv = hub_find(s_keys, v);
                     uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
                     if (hu >= 0) {
-                        if (cv) atomicAdd(&s_hcnt[hu], cv == 1 ? 1ULL : (1ULL << 32));
+                        if (cv) atomicAdd(reinterpret_cast<unsigned int*>(s_hcnt + hu) + (cv == 1 ? 0 : 1), 1u);
                         else s_hflag[hu] = 1u;
                     } else {
                         rec[2 * k] = (u << 2) | cv;
                     }
                     if (hv >= 0) {
-                        if (cu) atomicAdd(&s_hcnt[hv], cu == 1 ? 1ULL : (1ULL << 32));
+                        if (cu) atomicAdd(reinterpret_cast<unsigned int*>(s_hcnt + hv) + (cu == 1 ? 0 : 1), 1u);
                         else s_hflag[hv] = 1u;
                     } else {
                         rec[2 * k + 1] = (v << 2) | cu;
@@ -3459,6 +3476,14 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
         }
     }
     __syncthreads();
+    // counted nodes into the presence bits, one 32-node word per warp ballot
+    // (conflict-free: lane j reads node 32w + j; reading the counts of a
+    // thread's own 16 consecutive nodes below was a 32-way bank conflict)
+    for (int q = wid; q < kCmpSub / 32; q += kCmpT / 32) {
+        unsigned bal = __ballot_sync(0xffffffffu, s_cnt[q * 32 + lane] != 0ULL);
+        if (lane == 0 && bal) s_pres[q] |= bal;
+    }
+    __syncthreads();
     // this thread's 16 consecutive nodes: membership, old labels, new flags
     const int l0 = t * kCmpIPT;
     const int64_t gt = g0 + l0;
@@ -3476,7 +3501,7 @@ __global__ void __launch_bounds__(kCmpT) k_bin_compact(const uint32_t* __restric
     uint32_t pmask = 0, nmask = 0;
 #pragma unroll
     for (int j = 0; j < kCmpIPT; ++j) {
-        bool pres = (gt + j < n) && (((pw >> j) & 1u) || s_cnt[l0 + j] != 0ULL);
+        bool pres = (gt + j < n) && ((pw >> j) & 1u);
         if (pres) {
             pmask |= 1u << j;
             if (lab16[j] == -1) nmask |= 1u << j;

@@ -1681,6 +1681,28 @@ struct GreenParts {
     bool ok = false;
     CUgreenCtx dense = nullptr, sparse = nullptr;
 };
+// driver-API entry points through the runtime (the library does not link
+// libcuda, so it still loads where no driver is installed)
+struct GreenApi {
+    decltype(&::cuDeviceGet) deviceGet = nullptr;
+    decltype(&::cuDeviceGetDevResource) getDevResource = nullptr;
+    decltype(&::cuDevSmResourceSplitByCount) smSplit = nullptr;
+    decltype(&::cuDevResourceGenerateDesc) genDesc = nullptr;
+    decltype(&::cuGreenCtxCreate) ctxCreate = nullptr;
+    decltype(&::cuGreenCtxStreamCreate) streamCreate = nullptr;
+    bool load() {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPointByVersion(name, fn, CUDA_VERSION, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn;
+        };
+        return get("cuDeviceGet", (void**)&deviceGet) && get("cuDeviceGetDevResource", (void**)&getDevResource) &&
+               get("cuDevSmResourceSplitByCount", (void**)&smSplit) &&
+               get("cuDevResourceGenerateDesc", (void**)&genDesc) && get("cuGreenCtxCreate", (void**)&ctxCreate) &&
+               get("cuGreenCtxStreamCreate", (void**)&streamCreate);
+    }
+};
+GreenApi g_green_api;
 GreenParts* green_parts(int device) {
     static std::mutex mu;
     static GreenParts parts[16];
@@ -1695,14 +1717,15 @@ GreenParts* green_parts(int device) {
         CUdevResource res, grp[1], rest;
         unsigned nb = 1;
         CUdevResourceDesc dd, ds;
-        if (want > 0 && cuDeviceGet(&dev, device) == CUDA_SUCCESS &&
-            cuDeviceGetDevResource(dev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+        GreenApi& A = g_green_api;
+        if (want > 0 && A.load() && A.deviceGet(&dev, device) == CUDA_SUCCESS &&
+            A.getDevResource(dev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
             (int)res.sm.smCount > 2 * want &&
-            cuDevSmResourceSplitByCount(grp, &nb, &res, &rest, 0, (unsigned)want) == CUDA_SUCCESS && nb == 1 &&
-            cuDevResourceGenerateDesc(&ds, grp, 1) == CUDA_SUCCESS &&
-            cuDevResourceGenerateDesc(&dd, &rest, 1) == CUDA_SUCCESS &&
-            cuGreenCtxCreate(&g.sparse, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
-            cuGreenCtxCreate(&g.dense, dd, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS)
+            A.smSplit(grp, &nb, &res, &rest, 0, (unsigned)want) == CUDA_SUCCESS && nb == 1 &&
+            A.genDesc(&ds, grp, 1) == CUDA_SUCCESS &&
+            A.genDesc(&dd, &rest, 1) == CUDA_SUCCESS &&
+            A.ctxCreate(&g.sparse, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+            A.ctxCreate(&g.dense, dd, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS)
             g.ok = true;
         cudaGetLastError();
     }
@@ -1718,12 +1741,12 @@ void init_ctx(grem_ctx* c, int device, bool child = false) {
     bool high = (prio_mode == 1 && !child) || (prio_mode == 2 && child);
     GreenParts* gp = green_parts(device);
     CUstream cs = nullptr;
-    if (child && gp && cuGreenCtxStreamCreate(&cs, gp->sparse, CU_STREAM_NON_BLOCKING,
+    if (child && gp && g_green_api.streamCreate(&cs, gp->sparse, CU_STREAM_NON_BLOCKING,
                                               (prio_mode && high) ? hi : lo) == CUDA_SUCCESS)
         c->s = (cudaStream_t)cs;
     else
         CK(cudaStreamCreateWithPriority(&c->s, cudaStreamNonBlocking, (prio_mode && high) ? hi : lo));
-    if (!child && gp && cuGreenCtxStreamCreate(&cs, gp->dense, CU_STREAM_NON_BLOCKING,
+    if (!child && gp && g_green_api.streamCreate(&cs, gp->dense, CU_STREAM_NON_BLOCKING,
                                                prio_mode == 1 ? hi : lo) == CUDA_SUCCESS)
         c->s_dense = (cudaStream_t)cs;
     CK(cudaEventCreate(&c->ev0));
