@@ -186,6 +186,18 @@ int grem_node_stats_u32(grem_ctx* ctx, const uint32_t* edges, int64_t num_edges,
 int grem_node_stats_file(grem_ctx* ctx, const char* path, const int32_t* labels, int labels_on_device,
                          int64_t* k_out, int64_t* k0_out);
 
+/* expected_cuts / theory_curve (streamcut/theory.py:125-146): for every x in
+ * xs, cuts_out = sum over nodes with k >= 1 of (k - k0) p + k0 (1 - p),
+ * p = prob_correct(k, k0, x, multiplier) (theory.py:78-94; hypergeometric
+ * tail from log-gamma terms, theory.py:35-75).  k, k0: num_nodes int64 (host
+ * or device).  info_out (optional, 3 int64): first node with k >= 1, first
+ * such node whose k0 is not its majority side (-1 = none), sum of k (total
+ * endpoints).  Errors (FormatError, in the reference's order): "empty node
+ * stats" (num_nodes = 0 and nx > 0), the majority-side check, x outside
+ * (0, 1], multiplier < 1; nothing is checked when every k is 0. */
+int grem_theory_curve(grem_ctx* ctx, const int64_t* k, const int64_t* k0, int64_t num_nodes, int on_device,
+                      const double* xs, int64_t nx, double multiplier, double* cuts_out, int64_t* info_out);
+
 /* external_shuffle (streamcut/edgefile.py:248-327): a uniform random
  * permutation of the edge list, deterministic per seed (64-bit counter-hash
  * keys + one radix sort; the reference's numpy-PCG64 order is not

@@ -12,7 +12,7 @@ existing callers (CLI, tests) use the GPU path unchanged.
 
 from .config import ChunkPlan, CutReport, GremConfig, SeedConfig, default_capacity
 from .errors import CapacityError, DeviceError, FormatError, StreamcutError
-from .theory import compute_node_stats, node_stats_edges
+from .theory import compute_node_stats, curve_csv, expected_cuts, node_stats_edges, theory_curve
 from .shuffle import external_shuffle
 from .grem import bisect, bisect_edges, count_cuts, last_stats, partition, partition_edges, set_device
 
@@ -25,7 +25,7 @@ def install_into_streamcut(support: bool = False):
     the grem module globals (grem.py:300), so rebinding grem.* covers
     recursion as well.  ``support=True`` also swaps the label consumers this
     package provides (store.write_buckets / reorder_features,
-    theory.compute_node_stats, edgefile.external_shuffle), everywhere the
+    theory.compute_node_stats / expected_cuts / theory_curve, edgefile.external_shuffle), everywhere the
     reference binds them (package, module, CLI)."""
     import importlib
 
@@ -36,7 +36,8 @@ def install_into_streamcut(support: bool = False):
     swaps = {"bisect": bisect, "partition": partition, "count_cuts": count_cuts}
     mods = ["streamcut", "streamcut.grem", "streamcut.cli"]
     if support:
-        swaps.update(compute_node_stats=compute_node_stats, write_buckets=_store.write_buckets,
+        swaps.update(compute_node_stats=compute_node_stats, expected_cuts=expected_cuts, theory_curve=theory_curve,
+                     write_buckets=_store.write_buckets,
                      reorder_features=_store.reorder_features, external_shuffle=external_shuffle)
         mods += ["streamcut.theory", "streamcut.store", "streamcut.edgefile"]
     for name in mods:
@@ -54,5 +55,5 @@ __all__ = [
     "bisect", "partition", "count_cuts", "bisect_edges", "partition_edges", "set_device", "last_stats",
     "GremConfig", "SeedConfig", "ChunkPlan", "CutReport", "default_capacity",
     "StreamcutError", "FormatError", "CapacityError", "DeviceError", "install_into_streamcut",
-    "compute_node_stats", "node_stats_edges", "external_shuffle",
+    "compute_node_stats", "node_stats_edges", "expected_cuts", "theory_curve", "curve_csv", "external_shuffle",
 ]

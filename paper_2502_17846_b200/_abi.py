@@ -56,7 +56,7 @@ EXPORTS = [
     "grem_create", "grem_destroy", "grem_last_error", "grem_get_stats", "grem_set_profiling",
     "grem_get_phase_times", "grem_get_phase_bytes", "grem_mem_high_water", "grem_trim", "grem_bucket_edges",
     "grem_bisect_u32", "grem_partition_u32", "grem_partition_shard_u32", "grem_staged_edges", "grem_count_cuts_u32",
-    "grem_write_buckets_u32", "grem_write_buckets_file", "grem_reorder_records", "grem_node_stats_u32", "grem_shuffle_u32", "grem_shuffle_file", "grem_node_stats_file",
+    "grem_write_buckets_u32", "grem_write_buckets_file", "grem_reorder_records", "grem_node_stats_u32", "grem_shuffle_u32", "grem_shuffle_file", "grem_node_stats_file", "grem_theory_curve",
     "grem_bisect_file", "grem_partition_file", "grem_count_cuts_file", "grem_state_parts",
     "grem_device_alloc", "grem_device_free", "grem_memcpy_h2d", "grem_memcpy_d2h",
     "grem_gen_scale", "grem_gen_edges_host", "grem_gen_edges_device",
@@ -111,6 +111,7 @@ def _declare(L):
                                          P(c_i64)]
     L.grem_node_stats_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_int, c_vp, c_vp]
     L.grem_node_stats_file.argtypes = [c_vp, ctypes.c_char_p, c_vp, c_int, c_vp, c_vp]
+    L.grem_theory_curve.argtypes = [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_i64, ctypes.c_double, c_vp, c_vp]
     L.grem_write_buckets_file.argtypes = [c_vp, ctypes.c_char_p, c_vp, c_int, c_vp, c_int, c_vp, c_i64, P(c_i64)]
     L.grem_shuffle_u32.argtypes = [c_vp, c_vp, c_i64, c_i64, c_int, ctypes.c_uint64, c_vp, c_int]
     L.grem_shuffle_file.argtypes = [c_vp, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p]

@@ -2663,7 +2663,7 @@ __global__ void k_cut(const uint2* __restrict__ e, int64_t m, const int32_t* __r
 }
 __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long long* sizes, int64_t cap,
                        int* mx, int* neg) {
-    extern __shared__ unsigned long long sh[];
+    extern __shared__ unsigned int sh[];   // per-block counts: native 32-bit shared atomics (no CAS loop)
     int64_t nb = cap < 1024 ? cap : 1024;
     for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) sh[j] = 0;
     __syncthreads();
@@ -2694,10 +2694,10 @@ __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long
                 int l = lab[i];
                 if (l < 0) { anyneg = 1; continue; }
                 lm = l > lm ? l : lm;
-                if (l < nb) atomicAdd(&sh[l], 1ULL);
+                if (l < nb) atomicAdd(&sh[l], 1u);
             }
         }
-        if (lane < nb && mine) atomicAdd(&sh[lane], mine);
+        if (lane < nb && mine) atomicAdd(&sh[lane], (unsigned int)mine);
     } else {
         GRID_STRIDE(i, n) {
             int l = lab[i];
@@ -2706,7 +2706,7 @@ __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long
                 continue;
             }
             lm = l > lm ? l : lm;
-            if (l < nb) atomicAdd(&sh[l], 1ULL);
+            if (l < nb) atomicAdd(&sh[l], 1u);
             else if (l < cap) atomicAdd(&sizes[l], 1ULL);
         }
     }
@@ -2718,13 +2718,13 @@ __global__ void k_hist(const int32_t* __restrict__ lab, int64_t n, unsigned long
     if (anyneg) atomicOr(neg, 4);   // some node is unlabeled (allowed unless it is an endpoint)
     __syncthreads();
     for (int64_t j = threadIdx.x; j < nb; j += blockDim.x)
-        if (sh[j]) atomicAdd(&sizes[j], sh[j]);
+        if (sh[j]) atomicAdd(&sizes[j], (unsigned long long)sh[j]);
 }
 void launch_count_cuts(const uint2* e, int64_t m, const int32_t* lab, int64_t n, unsigned long long* d_cut,
                        unsigned long long* d_sizes, int64_t sizes_cap, int* d_max, int* d_neg, cudaStream_t s) {
     if (m > 0 && d_cut) k_cut<<<grid_for(m, 256, 16), 256, 0, s>>>(e, m, lab, d_cut, d_neg);
     int64_t nb = sizes_cap < 1024 ? sizes_cap : 1024;
-    k_hist<<<grid_for(n, 256, 4), 256, nb * sizeof(unsigned long long), s>>>(lab, n, d_sizes, sizes_cap, d_max,
+    k_hist<<<grid_for(n, 256, 4), 256, nb * sizeof(unsigned int), s>>>(lab, n, d_sizes, sizes_cap, d_max,
                                                                             d_neg);
 }
 
@@ -2784,9 +2784,10 @@ __global__ void __launch_bounds__(512) k_node_side_counts_hub(const uint2* __res
         }
         unsigned long long iu = 1ull << (32 * lv), iv = 1ull << (32 * lu);
         int hu = hub_find(s_keys, ed.x), hv = hub_find(s_keys, ed.y);
-        if (hu >= 0) atomicAdd(s_cnt + hu, iu);
+        // hub halves with native 32-bit shared atomics (a 64-bit one is a CAS loop)
+        if (hu >= 0) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + hu) + lv, 1u);
         else atomicAdd(cnt + ed.x, iu);
-        if (hv >= 0) atomicAdd(s_cnt + hv, iv);
+        if (hv >= 0) atomicAdd(reinterpret_cast<unsigned int*>(s_cnt + hv) + lu, 1u);
         else atomicAdd(cnt + ed.y, iv);
     }
     if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
@@ -3631,4 +3632,155 @@ int binned_shift(int64_t n) {
 }
 int64_t binned_tiles(int64_t n) { return (n + kCmpSub - 1) >> kSubShift; }
 
+// ============================================ expected-cut model (theory.py)
+// expected_cuts (theory.py:125-142): per node with k >= 1, p = prob_correct
+// (theory.py:78-94) = 1 - Pr(X <= t) for X ~ Hypergeom(k, k0, d), d = draws
+// (theory.py:67-75), t = ceil(d/2) - 1, the tail summed term by term as
+// exp(log C(k0, j) + log C(k - k0, d - j) - log C(k, d)) with log C from
+// log-gamma (theory.py:35-63), same association order.  Log-gamma values
+// come from a table lg[i] = lgamma(i), 0 <= i <= max k + 1.
+namespace {
+__device__ __forceinline__ double th_logc(const double* __restrict__ lg, int64_t n, int64_t r) {
+    return lg[n + 1] - lg[r + 1] - lg[n - r + 1];
+}
+__device__ __forceinline__ int64_t th_draws(int64_t k, double x_eff) {
+    int64_t d = (int64_t)rint(x_eff * (double)k);   // Python round(): half to even
+    return d < 1 ? 1 : (d > k ? k : d);
+}
+constexpr int kThBig = 1024;   // tail terms above which a node goes to the block kernel
+}  // namespace
+
+__global__ void k_lgamma_table(double* lg, int64_t count) {
+    GRID_STRIDE(i, count) lg[i] = lgamma((double)i);
+}
+
+// one thread per node: its expected cut endpoints into term[i]; nodes with a
+// long tail are queued (big_list) and summed by k_theory_big
+__global__ void k_theory_nodes(const int64_t* __restrict__ k, const int64_t* __restrict__ k0, int64_t n,
+                               const double* __restrict__ lg, double x_eff, double* __restrict__ term,
+                               int64_t* big_list, unsigned long long* big_count) {
+    GRID_STRIDE(i, n) {
+        int64_t ki = k[i], k0i = k0[i];
+        double v = 0.0;
+        if (ki >= 1) {
+            int64_t d = th_draws(ki, x_eff);
+            int64_t t = (d + 1) / 2 - 1;
+            int64_t lo = d - (ki - k0i) > 0 ? d - (ki - k0i) : 0;
+            int64_t hi = d < k0i ? d : k0i;
+            int64_t top = t < hi ? t : hi;
+            if (top - lo + 1 > kThBig) {
+                big_list[atomicAdd(big_count, 1ULL)] = i;
+                term[i] = 0.0;
+                continue;
+            }
+            double ld = th_logc(lg, ki, d), cdf = 0.0;
+            for (int64_t j = lo; j <= top; ++j) cdf += exp(th_logc(lg, k0i, j) + th_logc(lg, ki - k0i, d - j) - ld);
+            double p = 1.0 - cdf;
+            v = (double)(ki - k0i) * p + (double)k0i * (1.0 - p);
+        }
+        term[i] = v;
+    }
+}
+
+// one block per queued node: the tail terms in parallel, reduced in a fixed order
+__global__ void __launch_bounds__(256) k_theory_big(const int64_t* __restrict__ k, const int64_t* __restrict__ k0,
+                                                    const double* __restrict__ lg, double x_eff,
+                                                    const int64_t* __restrict__ big_list,
+                                                    const unsigned long long* big_count, double* __restrict__ term) {
+    __shared__ double sw[8];
+    for (unsigned long long b = blockIdx.x; b < *big_count; b += gridDim.x) {
+        int64_t i = big_list[b];
+        int64_t ki = k[i], k0i = k0[i];
+        int64_t d = th_draws(ki, x_eff);
+        int64_t t = (d + 1) / 2 - 1;
+        int64_t lo = d - (ki - k0i) > 0 ? d - (ki - k0i) : 0;
+        int64_t hi = d < k0i ? d : k0i;
+        int64_t top = t < hi ? t : hi;
+        double ld = th_logc(lg, ki, d), s = 0.0;
+        for (int64_t j = lo + threadIdx.x; j <= top; j += blockDim.x)
+            s += exp(th_logc(lg, k0i, j) + th_logc(lg, ki - k0i, d - j) - ld);
+        for (int off = 16; off; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+        if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double cdf = 0.0;
+            for (int w = 0; w < 8; ++w) cdf += sw[w];
+            double p = 1.0 - cdf;
+            term[i] = (double)(ki - k0i) * p + (double)k0i * (1.0 - p);
+        }
+        __syncthreads();
+    }
+}
+
+// deterministic sum: fixed per-block partials, then one block in block order
+__global__ void __launch_bounds__(256) k_sum_f64_partial(const double* __restrict__ v, int64_t n, double* part) {
+    __shared__ double sw[8];
+    double s = 0.0;
+    GRID_STRIDE(i, n) s += v[i];
+    for (int off = 16; off; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < 8; ++w) b += sw[w];
+        part[blockIdx.x] = b;
+    }
+}
+__global__ void k_sum_f64_final(const double* __restrict__ part, int np, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int b = 0; b < np; ++b) s += part[b];
+        *out = s;
+    }
+}
+
+int theory_sum_blocks() { return num_sms() * 4; }
+void launch_lgamma_table(double* lg, int64_t count, cudaStream_t s) {
+    k_lgamma_table<<<grid_for(count, 256), 256, 0, s>>>(lg, count);
+}
+void launch_expected_cuts(const int64_t* k, const int64_t* k0, int64_t n, const double* lg, double x_eff,
+                          double* term, int64_t* big_list, unsigned long long* big_count, double* part,
+                          double* out, cudaStream_t s) {
+    cudaMemsetAsync(big_count, 0, sizeof(unsigned long long), s);
+    k_theory_nodes<<<grid_for(n, 256), 256, 0, s>>>(k, k0, n, lg, x_eff, term, big_list, big_count);
+    k_theory_big<<<num_sms() * 8, 256, 0, s>>>(k, k0, lg, x_eff, big_list, big_count, term);
+    int nb = theory_sum_blocks();
+    k_sum_f64_partial<<<nb, 256, 0, s>>>(term, n, part);
+    k_sum_f64_final<<<1, 32, 0, s>>>(part, nb, out);
+}
+
+}  // namespace grem
+
+namespace grem {
+// validation and totals for expected_cuts: out[0] = first node with k >= 1,
+// out[1] = first such node whose k0 is not its majority side (theory.py:87-88),
+// out[2] = max k, out[3] = sum of k (total endpoints); indices as min, -1 = none
+__global__ void k_theory_check(const int64_t* __restrict__ k, const int64_t* __restrict__ k0, int64_t n,
+                               unsigned long long* out) {
+    unsigned long long first = ~0ULL, bad = ~0ULL, mx = 0, sum = 0;
+    GRID_STRIDE(i, n) {
+        int64_t ki = k[i], k0i = k0[i];
+        sum += (unsigned long long)ki;
+        if (ki >= 1) {
+            if ((unsigned long long)i < first) first = (unsigned long long)i;
+            if ((k0i < 0 || k0i > ki || 2 * k0i < ki) && (unsigned long long)i < bad) bad = (unsigned long long)i;
+            if ((unsigned long long)ki > mx) mx = (unsigned long long)ki;
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        first = min(first, __shfl_down_sync(0xffffffffu, first, off));
+        bad = min(bad, __shfl_down_sync(0xffffffffu, bad, off));
+        mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
+        sum += __shfl_down_sync(0xffffffffu, sum, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (first != ~0ULL) atomicMin(out + 0, first);
+        if (bad != ~0ULL) atomicMin(out + 1, bad);
+        if (mx) atomicMax(out + 2, mx);
+        if (sum) atomicAdd(out + 3, sum);
+    }
+}
+void launch_theory_check(const int64_t* k, const int64_t* k0, int64_t n, unsigned long long* out, cudaStream_t s) {
+    k_theory_check<<<grid_for(n, 256), 256, 0, s>>>(k, k0, n, out);
+}
 }  // namespace grem

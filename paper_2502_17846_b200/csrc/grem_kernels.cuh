@@ -316,6 +316,17 @@ void sort_pairs_u64_u32(const unsigned long long* kin, unsigned long long* kout,
 void sort_keys_u64(const unsigned long long* kin, unsigned long long* kout, int64_t n, void* temp,
                    size_t temp_bytes, cudaStream_t s);
 
+// expected-cut model (theory.py:125-146): lg = lgamma(i) table; term = n
+// doubles, big_list = n slots, part = theory_sum_blocks() doubles
+int theory_sum_blocks();
+// out[4] (pre-set to {~0, ~0, 0, 0}): first node with k >= 1, first with a
+// non-majority k0, max k, sum of k
+void launch_theory_check(const int64_t* k, const int64_t* k0, int64_t n, unsigned long long* out, cudaStream_t s);
+void launch_lgamma_table(double* lg, int64_t count, cudaStream_t s);
+void launch_expected_cuts(const int64_t* k, const int64_t* k0, int64_t n, const double* lg, double x_eff,
+                          double* term, int64_t* big_list, unsigned long long* big_count, double* part,
+                          double* out, cudaStream_t s);
+
 // synthetic generator (grem_gen.h)
 void launch_gen_edges(uint64_t n, uint32_t beta, uint64_t seed, double scale, uint64_t perm_mask,
                       uint32_t perm_bits, uint64_t e0, uint64_t count, uint32_t* out, cudaStream_t s);

@@ -224,6 +224,9 @@ struct grem_ctx {
     DBuf<unsigned long long> bk_counts{"bk_counts"};
     DBuf<unsigned long long> ns_cnt{"ns_cnt"};   // node stats (theory)
     DBuf<int64_t> ns_k{"ns_k"}, ns_k0{"ns_k0"};
+    DBuf<double> th_lg{"th_lg"}, th_term{"th_term"}, th_part{"th_part"};
+    DBuf<int64_t> th_big{"th_big"};
+    DBuf<unsigned long long> th_scal{"th_scal"};
     DBuf<uint32_t> ns_pack{"ns_pack"};
     DBuf<unsigned long long> sh_keys{"sh_keys"}, sh_vals{"sh_vals"};   // external shuffle
     DBuf<long long> bk_perm{"bk_perm"};
@@ -2287,6 +2290,7 @@ void ctx_trim_buffers(grem_ctx* c) {
     c->bk_keys_a.release(); c->bk_keys_b.release(); c->bk_order.release(); c->bk_out.release();
     c->bk_counts.release(); c->ns_cnt.release(); c->ns_k.release(); c->ns_k0.release(); c->ns_pack.release();
     c->sh_keys.release(); c->sh_vals.release();
+    c->th_lg.release(); c->th_term.release(); c->th_part.release(); c->th_big.release(); c->th_scal.release();
 }
 
 // =============================================================== C ABI
@@ -2703,6 +2707,65 @@ int grem_node_stats_file(grem_ctx* c, const char* path, const int32_t* labels, i
         GrpeHeader hd;
         const uint2* d = load_grpe(c, path, &hd);
         node_stats_dev(c, d, hd.m, hd.n, stage_labels(c, labels, hd.n, labels_on_device), k_out, k0_out);
+    });
+}
+
+int grem_theory_curve(grem_ctx* c, const int64_t* k, const int64_t* k0, int64_t n, int on_device, const double* xs,
+                      int64_t nx, double multiplier, double* cuts_out, int64_t* info_out) {
+    if (!c || (nx > 0 && (!xs || !cuts_out)) || n < 0) return GREM_E_FORMAT;
+    return guarded(c, [&] {
+        if (info_out) info_out[0] = info_out[1] = -1, info_out[2] = 0;
+        if (nx == 0) return;   // theory.py:145-146: nothing evaluated
+        if (n == 0) fail(GREM_E_FORMAT, "empty node stats");   // theory.py:131-132
+        if (!k || !k0) fail(GREM_E_FORMAT, "null node stats");
+        cudaStream_t s = c->s;
+        const int64_t* dk = k;
+        const int64_t* dk0 = k0;
+        if (!on_device) {
+            c->ns_k.ensure(n, s);
+            c->ns_k0.ensure(n, s);
+            CK(cudaMemcpyAsync(c->ns_k.p, k, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(c->ns_k0.p, k0, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+            dk = c->ns_k.p;
+            dk0 = c->ns_k0.p;
+        }
+        c->th_scal.ensure(8, s);
+        unsigned long long init[4] = {~0ULL, ~0ULL, 0ULL, 0ULL};
+        CK(cudaMemcpyAsync(c->th_scal.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        launch_theory_check(dk, dk0, n, c->th_scal.p, s);
+        c->kernels++;
+        unsigned long long chk[4];
+        CK(cudaMemcpyAsync(chk, c->th_scal.p, sizeof(chk), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        int64_t first = chk[0] == ~0ULL ? -1 : (int64_t)chk[0];
+        int64_t bad = chk[1] == ~0ULL ? -1 : (int64_t)chk[1];
+        if (info_out) info_out[0] = first, info_out[1] = bad, info_out[2] = (int64_t)chk[3];
+        if (first < 0) {   // every node has k = 0: nothing is evaluated, no domain check runs
+            for (int64_t q = 0; q < nx; ++q) cuts_out[q] = 0.0;
+            return;
+        }
+        // prob_correct's checks in its order at the first evaluated node (theory.py:85-92)
+        if (bad == first) fail(GREM_E_FORMAT, "k0 must be the majority side");
+        for (int64_t q = 0; q < nx; ++q)
+            if (!(xs[q] > 0.0 && xs[q] <= 1.0)) fail(GREM_E_FORMAT, "chunk fraction must be in (0, 1]");
+        if (multiplier < 1.0) fail(GREM_E_FORMAT, "multiplier must be >= 1");
+        if (bad >= 0) fail(GREM_E_FORMAT, "k0 must be the majority side");
+        int64_t maxk = (int64_t)chk[2];
+        c->th_lg.ensure(maxk + 2, s);
+        launch_lgamma_table(c->th_lg.p, maxk + 2, s);
+        c->th_term.ensure(n, s);
+        c->th_big.ensure(n, s);
+        c->th_part.ensure(theory_sum_blocks() + 1, s);
+        for (int64_t q = 0; q < nx; ++q) {
+            double x_eff = multiplier * xs[q] < 1.0 ? multiplier * xs[q] : 1.0;   // theory.py:73
+            launch_expected_cuts(dk, dk0, n, c->th_lg.p, x_eff, c->th_term.p, c->th_big.p, c->th_scal.p + 4,
+                                 c->th_part.p, c->th_part.p + theory_sum_blocks(), s);
+            c->kernels += 5;
+            CK(cudaMemcpyAsync(cuts_out + q, c->th_part.p + theory_sum_blocks(), sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+        }
+        c->kernels++;
+        CK(cudaStreamSynchronize(s));
     });
 }
 

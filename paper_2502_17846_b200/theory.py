@@ -6,10 +6,14 @@ node, ``k`` = neighbour endpoints excluding self-loops (duplicates count with
 multiplicity) and ``k0`` = those on the node's majority side of the bisection
 ``labels``.  It runs behind the C ABI (``grem_node_stats_u32``: two label
 gathers and two 64-bit REDs per edge, then k = c0 + c1, k0 = max) and returns
-the reference's ``NodeStats`` when it is importable.  The curve math on top
-(``expected_cuts``, ``theory_curve``: per-(k, k0) hypergeometric tails summed
-in node order) is host arithmetic over the returned arrays and stays the
-reference's.
+the reference's ``NodeStats`` when it is importable.
+
+``expected_cuts(stats, x, multiplier)`` / ``theory_curve(stats, xs,
+multiplier)`` (theory.py:125-146) run behind ``grem_theory_curve``: one
+thread per node sums its hypergeometric tail (long tails: one CTA per node)
+from a device log-gamma table, and the per-node expected cut endpoints are
+reduced in a fixed order.  The domain errors are the reference's, raised in
+the order its per-node loop would meet them.
 """
 
 from __future__ import annotations
@@ -47,6 +51,72 @@ except Exception:  # noqa: BLE001
         @property
         def total_endpoints(self) -> int:
             return int(self.k.sum())
+
+
+try:   # the reference's point type, so callers comparing results see the same class
+    from streamcut.theory import TheoryCurvePoint  # type: ignore
+except Exception:  # noqa: BLE001
+    from dataclasses import dataclass
+
+    @dataclass(frozen=True)
+    class TheoryCurvePoint:
+        """theory.py:29-32."""
+        x: float
+        expected_cuts: float
+        expected_cut_fraction: float
+
+
+def _curve(stats, xs, multiplier):
+    """expected cut endpoints for every x (GPU), with the reference's errors"""
+    xs = list(xs)
+    if not xs:
+        return [], 0
+    k = np.ascontiguousarray(np.asarray(stats.k, dtype=np.int64))
+    k0 = np.ascontiguousarray(np.asarray(stats.k0, dtype=np.int64))
+    xa = np.ascontiguousarray(np.asarray([float(x) for x in xs], dtype=np.float64))
+    out = np.zeros(len(xs), dtype=np.float64)
+    info = np.full(3, -1, dtype=np.int64)
+    rc = _abi.lib().grem_theory_curve(context(), k.ctypes.data, k0.ctypes.data, k.shape[0], 0, xa.ctypes.data,
+                                      len(xs), float(multiplier), out.ctypes.data, info.ctypes.data)
+    if rc == 1 and k.shape[0] > 0 and info[0] >= 0:   # a domain error: the reference's message and order
+        first, bad = int(info[0]), int(info[1])
+
+        def majority(i):
+            return FormatError(f"k0 must be the majority side: got k={int(k[i])}, k0={int(k0[i])}")
+        if bad == first:
+            raise majority(first)
+        if not 0 < xs[0] <= 1:
+            raise FormatError(f"chunk fraction must be in (0, 1], got {xs[0]}")
+        if multiplier < 1:
+            raise FormatError(f"multiplier must be >= 1, got {multiplier}")
+        if bad >= 0:
+            raise majority(bad)
+        for x in xs[1:]:
+            if not 0 < x <= 1:
+                raise FormatError(f"chunk fraction must be in (0, 1], got {x}")
+    _raise(rc)
+    return [float(v) for v in out], int(info[2])
+
+
+def expected_cuts(stats, x: float, multiplier: float = 1.0):
+    """theory.py:125-142: expected cut endpoints at chunk fraction x."""
+    (total,), endpoints = _curve(stats, [x], multiplier)
+    return TheoryCurvePoint(float(x), total, total / endpoints if endpoints else 0.0)
+
+
+def theory_curve(stats, xs, multiplier: float = 1.0):
+    """theory.py:145-146 (all points from one staging of the node stats)."""
+    xs = [float(x) for x in xs]
+    totals, endpoints = _curve(stats, xs, multiplier)
+    return [TheoryCurvePoint(x, t, t / endpoints if endpoints else 0.0) for x, t in zip(xs, totals)]
+
+
+def curve_csv(points, multiplier: float) -> str:
+    """theory.py:149-153."""
+    lines = ["x,expected_cuts,expected_cut_fraction,multiplier"]
+    for pt in points:
+        lines.append(f"{pt.x},{pt.expected_cuts},{pt.expected_cut_fraction},{multiplier}")
+    return "\n".join(lines) + "\n"
 
 
 def node_stats_edges(edges, num_nodes: int, labels, on_device_ptr: int | None = None,
