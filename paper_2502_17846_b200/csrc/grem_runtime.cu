@@ -180,6 +180,9 @@ struct grem_ctx {
     // copy_s, each checked and marked with an event; consumers wait only for
     // the pieces covering the edges they read
     cudaStream_t copy_s = nullptr;
+    // id checks of the staged pieces on their own stream: a check waiting for
+    // SMs behind a long round kernel must not hold back the next piece's DMA
+    cudaStream_t check_s = nullptr;
     struct IngestMark {
         int64_t end;
         cudaEvent_t ev;
@@ -1416,9 +1419,24 @@ void ingest_abort(grem_ctx* c) {
     }
     ingest_join(c);
     if (c->copy_s) cudaStreamSynchronize(c->copy_s);
+    if (c->check_s) cudaStreamSynchronize(c->check_s);
     for (auto& mk : c->ingest) cudaEventDestroy(mk.ev);
     c->ingest.clear();
     c->ingest_base = nullptr;
+}
+
+// the id check of a piece just queued on copy_s, on check_s; returns the
+// event consumers wait for (piece copied and checked)
+cudaEvent_t check_piece_async(grem_ctx* c, uint2* piece, int64_t cnt, uint32_t n) {
+    cudaEvent_t copied, ev;
+    CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CK(cudaEventRecord(copied, c->copy_s));
+    CK(cudaStreamWaitEvent(c->check_s, copied, 0));
+    cudaEventDestroy(copied);
+    launch_check_piece(piece, cnt, n, c->d_bad, c->check_s);
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, c->check_s));
+    return ev;
 }
 
 // copy stream + bad-id flag for an overlapped ingest into dst (ordered after
@@ -1429,6 +1447,7 @@ void ingest_begin(grem_ctx* c, const uint2* dst, int64_t m, int64_t n) {
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         static const bool low = getenv("GREM_COPY_PRIO_LOW") != nullptr;   // A/B switch
         CK(cudaStreamCreateWithPriority(&c->copy_s, cudaStreamNonBlocking, low ? lo : hi));
+        CK(cudaStreamCreateWithPriority(&c->check_s, cudaStreamNonBlocking, low ? lo : hi));
     }
     if (!c->d_bad) CK(cudaMalloc(&c->d_bad, sizeof(unsigned long long)));
     cudaEvent_t ready;
@@ -1463,11 +1482,7 @@ const uint2* stage_edges(grem_ctx* c, const uint32_t* edges, int64_t m, int64_t 
             for (int64_t off = 0; off < m; off += piece) {
                 int64_t cnt = m - off < piece ? m - off : piece;
                 CK(cudaMemcpyAsync(dst + off, edges + 2 * off, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->copy_s));
-                launch_check_piece(dst + off, cnt, (uint32_t)n, c->d_bad, c->copy_s);
-                cudaEvent_t ev;
-                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                CK(cudaEventRecord(ev, c->copy_s));
-                c->ingest.push_back({off + cnt, ev});
+                c->ingest.push_back({off + cnt, check_piece_async(c, dst + off, cnt, (uint32_t)n)});
             }
             return dst;
         } else if (pinned) {   // page-locked source: DMA straight into HBM
@@ -1593,10 +1608,7 @@ void ingest_reader(grem_ctx* c, std::string path, uint2* dst, int64_t m, uint32_
                 if (!o) fail(GREM_E_FORMAT, path + ": truncated payload");
             CK(cudaMemcpyAsync(dst + off, buf, bytes, cudaMemcpyHostToDevice, c->copy_s));
             CK(cudaEventRecord(c->ring_ev[slot], c->copy_s));
-            launch_check_piece(dst + off, cnt, n, c->d_bad, c->copy_s);
-            cudaEvent_t ev;
-            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            CK(cudaEventRecord(ev, c->copy_s));
+            cudaEvent_t ev = check_piece_async(c, dst + off, cnt, n);
             {
                 std::lock_guard<std::mutex> lk(c->ing_mu);
                 c->ingest.push_back({off + cnt, ev});
@@ -2350,6 +2362,7 @@ void grem_destroy(grem_ctx* c) {
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->s) cudaStreamDestroy(c->s);
     if (c->copy_s) cudaStreamDestroy(c->copy_s);
+    if (c->check_s) cudaStreamDestroy(c->check_s);
     if (c->d_bad) cudaFree(c->d_bad);
     delete c;
 }
