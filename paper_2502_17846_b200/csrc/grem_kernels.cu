@@ -293,6 +293,28 @@ __device__ __forceinline__ int hub_find(const uint32_t* s_keys, uint32_t u) {
     r = q.y == u ? (int)(2 * b2 + 1) : r;
     return r;
 }
+// One-bit-per-hash prefilter in front of the hub table (64 Kbit, one hash):
+// most endpoints are not hubs and leave after one 4-byte shared load instead
+// of the table's two 8-byte ones (the table probes were 39% of
+// k_bin_scatter's shared wavefronts, ncu r02i).  No false negatives.
+constexpr int kBloomWords = 2048;
+__device__ __forceinline__ uint32_t hub_bloom_bit(uint32_t u) { return (u * 0x2C1B3C6Du) >> 16; }
+__device__ __forceinline__ void hub_bloom_build(uint32_t* s_bloom, const uint32_t* s_keys) {
+    for (int k = threadIdx.x; k < kBloomWords; k += blockDim.x) s_bloom[k] = 0u;
+    __syncthreads();
+    for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) {
+        uint32_t key = s_keys[k];
+        if (key != kHubEmpty) {
+            uint32_t h = hub_bloom_bit(key);
+            atomicOr(&s_bloom[h >> 5], 1u << (h & 31));
+        }
+    }
+}
+__device__ __forceinline__ int hub_find_pf(const uint32_t* s_keys, const uint32_t* s_bloom, uint32_t u) {
+    uint32_t h = hub_bloom_bit(u);
+    if (!((s_bloom[h >> 5] >> (h & 31)) & 1u)) return -1;
+    return hub_find(s_keys, u);
+}
 __device__ __forceinline__ void hub_load(uint32_t* s_keys, const uint32_t* hub_keys) {
     for (int k = threadIdx.x; k < kHubSlots; k += blockDim.x) s_keys[k] = hub_keys ? hub_keys[k] : kHubEmpty;
 }
@@ -3259,9 +3281,32 @@ __global__ void __launch_bounds__(1024) k_bin_hist(const uint2* __restrict__ e, 
         hist[(int64_t)k * gridDim.x + blockIdx.x] = k < nbins ? (int32_t)s_hist[k] : 0;   // row nbins: total
 }
 
-constexpr int kScatIPT = 8;
+#ifndef GREM_SCAT_IPT
+#define GREM_SCAT_IPT 8
+#endif
+constexpr int kScatIPT = GREM_SCAT_IPT;
 constexpr int kScatBatch = kScatT * kScatIPT;   // edges per batch, <= 2 records each
-constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * (4 + 8) + (size_t)2 * kScatBatch * 4 + 64 * 4;
+// Shared-memory footprint (ncu r02i: hub probes 39% and carry-slot reads
+// 13.5% of the shared wavefronts).  GREM_SCAT_BLOOM=1 puts a one-bit
+// prefilter in front of the hub probes; GREM_CARRY_STRIDE=9 pads the per-bin
+// carry slots so the flush loop (thread t: bins 2t, 2t+1) leaves its 16-way
+// bank conflict.  Both need 8 KB of shared memory, and with 2048 bins either
+// one pushed the kernel (197 -> 205 KB) to the largest carve-out, halving the
+// L1 left for the label gathers: 91 -> 116 ms summed
+// (profiles/r02_ab_scatter_smem.txt).  With 1024 bins (GREM_MAX_BINS) the
+// kernel needs 160 KB, keeps the 164 KB carve-out with 92 KB of L1, and both
+// fit: step 570 -> 554 ms (profiles/r02_ab_scatter_bins.txt; the compact
+// reads each bin's records from twice as many tiles, 39 -> 49 ms summed).
+#ifndef GREM_SCAT_BLOOM
+#define GREM_SCAT_BLOOM 1
+#endif
+#ifndef GREM_CARRY_STRIDE
+#define GREM_CARRY_STRIDE 9
+#endif
+constexpr int kCarryStride = GREM_CARRY_STRIDE;
+constexpr size_t kScatSmem = (size_t)kHubSlots * (4 + 8 + 4) + (size_t)kMaxBins * 4 * 4 +
+                             (size_t)kMaxBins * 4 * kCarryStride + (size_t)2 * kScatBatch * 4 + 64 * 4 +
+                             (GREM_SCAT_BLOOM ? (size_t)kBloomWords * 4 : 0);
 
 __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2* __restrict__ e, int64_t m,
                                                         const uint32_t* __restrict__ lab2,
@@ -3283,10 +3328,18 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
     unsigned int* s_cur = s_start + kMaxBins;
     unsigned int* s_beg = s_cur + kMaxBins;       // first record slot of this CTA's region per bin
     uint32_t* s_carry = s_beg + kMaxBins;         // per bin: the open (incomplete) 32-byte sector
-    uint32_t* s_out = s_carry + 8 * kMaxBins;
+    uint32_t* s_out = s_carry + kCarryStride * kMaxBins;
     unsigned int* s_w = s_out + 2 * kScatBatch;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     hub_load(s_keys, hub_keys);
+#if GREM_SCAT_BLOOM
+    uint32_t* s_bloom = s_w + 64;
+    __syncthreads();
+    hub_bloom_build(s_bloom, s_keys);   // visible after the first batch's barrier
+#define SCAT_HUB_FIND(x) hub_find_pf(s_keys, s_bloom, (x))
+#else
+#define SCAT_HUB_FIND(x) hub_find(s_keys, (x))
+#endif
     for (int k = t; k < kHubSlots; k += kScatT) {
         s_hcnt[k] = 0ULL;
         s_hflag[k] = 0u;
@@ -3310,12 +3363,12 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
             rec[2 * k + 1] = 0xFFFFFFFFu;
             uint32_t u = ed[k].x, v = ed[k].y;
             if (u != kHubEmpty) {
-                int hu = hub_find(s_keys, u);
+                int hu = SCAT_HUB_FIND(u);
                 if (u == v) {   // self-loop: u is a chunk node, no count (model.py:53-55)
                     if (hu >= 0) s_hflag[hu] = 1u;
                     else rec[2 * k] = (u << 2) | 3u;
                 } else {
-                    int hv = hub_find(s_keys, v);
+                    int hv = SCAT_HUB_FIND(v);
                     uint32_t cu = lab2_code(lab2, u), cv = lab2_code(lab2, v);
                     if (hu >= 0) {
                         if (cv) atomicAdd(reinterpret_cast<unsigned int*>(s_hcnt + hu) + (cv == 1 ? 0 : 1), 1u);
@@ -3375,7 +3428,7 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
                 unsigned int cur = s_cur[k], sec = cur & ~7u;
                 if ((cur & 7u) && cur + v >= sec + 8) {
                     unsigned int lo = s_beg[k] > sec ? s_beg[k] : sec;
-                    for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[8 * k + (p & 7u)];
+                    for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[kCarryStride * k + (p & 7u)];
                 }
             }
         }
@@ -3386,7 +3439,7 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
             unsigned int bb = (r >> 2) >> shift;
             unsigned int p = s_cur[bb] + (k - s_start[bb]);
             if (p < ((s_cur[bb] + s_hist[bb]) & ~7u)) recs[p] = r;
-            else s_carry[8 * bb + (p & 7u)] = r;
+            else s_carry[kCarryStride * bb + (p & 7u)] = r;
         }
         __syncthreads();
         if (2 * t < nbins) s_cur[2 * t] += v0;
@@ -3397,7 +3450,7 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
         unsigned int cur = s_cur[k], sec = cur & ~7u;
         if (cur & 7u) {
             unsigned int lo = s_beg[k] > sec ? s_beg[k] : sec;
-            for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[8 * k + (p & 7u)];
+            for (unsigned int p = lo; p < cur; ++p) recs[p] = s_carry[kCarryStride * k + (p & 7u)];
         }
     }
     for (int k = t; k < kHubSlots; k += kScatT) {
@@ -3406,6 +3459,7 @@ __global__ void __launch_bounds__(kScatT, kScatPerSM) k_bin_scatter(const uint2*
         if (s_hflag[k]) hub_flag[k] = 1u;
     }
 }
+#undef SCAT_HUB_FIND
 
 constexpr int kCmpSub = 1 << kSubShift;              // nodes per tile
 constexpr int kCmpT = kCmpSub / 16;

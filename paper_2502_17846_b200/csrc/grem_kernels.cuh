@@ -88,7 +88,7 @@ constexpr int kRTileC = 4096;   // nodes per round tile (kRT * kRI in grem_kerne
 // <= kMaxBins bins); one CTA per 2^kSubShift-node tile then accumulates its
 // records in shared memory and writes the compact chunk state directly.
 #ifndef GREM_MAX_BINS
-#define GREM_MAX_BINS 2048
+#define GREM_MAX_BINS 1024   // k_bin_scatter's shared footprint, see GREM_SCAT_BLOOM in grem_kernels.cu
 #endif
 constexpr int kMaxBins = GREM_MAX_BINS;
 #ifndef GREM_SUB_SHIFT
