@@ -323,7 +323,7 @@ def main():
             "phases_note": "one extra step with the phase profiler on (CUDA events per launch group; sums of concurrent subtrees exceed the step)",
             "stats": {kk: st[kk] for kk in ("rounds", "visits", "bisections", "chunks")},
         }
-        print(json.dumps(out))
+        _emit(json.dumps(out))
     if dist:
         dist.destroy_process_group()
     return 0
@@ -447,9 +447,26 @@ def run_reference_arm(args):
            "config": bench_config(workload, k, args.gpus, args.gpus > 1 and not args.replicas),
            "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": kind, "sample": sample},
            "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    _emit(json.dumps(out))
     return 0
 
 
+# The JSON line is the only thing on stdout: native chatter written straight to
+# file descriptor 1 (e.g. NCCL's "NCCL version" banner at communicator init
+# under torchrun) is sent to stderr instead.
+_JSON_OUT = None
+
+
+def _emit(line: str) -> None:
+    (_JSON_OUT or sys.stdout).write(line + "\n")
+    (_JSON_OUT or sys.stdout).flush()
+
+
 if __name__ == "__main__":
+    try:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+    except OSError:
+        _JSON_OUT = None
     sys.exit(main())
