@@ -2888,7 +2888,10 @@ void launch_side_bits(const int8_t* lab, int64_t n, uint32_t* bits, uint32_t* wp
 // the edge goes to side 0, side 1 or is cut; order within a side stays the
 // file order through a tile-local ballot ranking plus a decoupled look-back
 // across tiles (dynamic tile ids, so waiting only ever targets started tiles).
-constexpr int kSplitT = 256;
+#ifndef GREM_SPLIT_T
+#define GREM_SPLIT_T 256
+#endif
+constexpr int kSplitT = GREM_SPLIT_T;   // threads (and 8x edges) per tile: fewer, larger tiles = fewer look-backs
 constexpr int kSplitI = 8;
 constexpr int kSplitTile = kSplitT * kSplitI;
 constexpr unsigned long long kLbAgg = 1ULL << 62, kLbInc = 2ULL << 62, kLbVal = (1ULL << 62) - 1;
@@ -2981,19 +2984,29 @@ __global__ void __launch_bounds__(kSplitT) k_split_edges(const uint2* __restrict
     // exclusive prefix over (k, warp) in edge order, per side; warps 0/1 own sides 0/1
     if (wid < 2) {
         int sd = wid;
-        constexpr int NE = kSplitI * NW;   // 64 entries
-        uint32_t v0 = s_c[sd][(2 * lane) / NW][(2 * lane) % NW];
-        uint32_t v1 = s_c[sd][(2 * lane + 1) / NW][(2 * lane + 1) % NW];
-        uint32_t pair = v0 + v1, incl = pair;
+        constexpr int NE = kSplitI * NW;   // (k, warp) entries in edge order
+        constexpr int PER = NE / 32;       // consecutive entries per lane
+        static_assert(NE % 32 == 0, "whole entries per lane");
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            int en = lane * PER + q;
+            v[q] = s_c[sd][en / NW][en % NW];
+            sum += v[q];
+        }
+        uint32_t incl = sum;
         for (int off = 1; off < 32; off <<= 1) {
             uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
             if (lane >= off) incl += o;
         }
-        uint32_t excl = incl - pair;
-        static_assert(NE == 64, "two entries per lane");
+        uint32_t excl = incl - sum;
         __syncwarp();
-        s_c[sd][(2 * lane) / NW][(2 * lane) % NW] = excl;
-        s_c[sd][(2 * lane + 1) / NW][(2 * lane + 1) % NW] = excl + v0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            int en = lane * PER + q;
+            s_c[sd][en / NW][en % NW] = excl;
+            excl += v[q];
+        }
         uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         unsigned long long* status = sd ? status1 : status0;
         unsigned long long prefix = 0;
