@@ -112,3 +112,37 @@ def test_gpu_shards_arxiv_k8():
     for world in (2, 4, 8):
         parts = _shards(e32, s.num_nodes, 8, cfg, world)
         assert np.array_equal(np.maximum.reduce(parts), full), world
+
+
+def _gather_worker(rank, world, port, m, q):
+    """the upload-slice + in-place all-gather of partition_distributed's host
+    path, on CPU tensors over gloo"""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2502_17846_b200.shard import upload_slice
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    host = torch.arange(2 * m, dtype=torch.int32).reshape(m, 2)
+    per, lo, hi = upload_slice(m, rank, world)
+    buf = torch.full((per * world, 2), -7, dtype=torch.int32)
+    buf[lo:hi] = host[lo:hi]
+    dist.all_gather_into_tensor(buf, buf[rank * per:(rank + 1) * per].clone())
+    q.put((rank, bool(torch.equal(buf[:m], host))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m", [1, 7, 1000])
+def test_gloo_upload_slices_reassemble_the_edge_list(m):
+    import multiprocessing as mp
+    world = 2 if m == 1 else 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29650 + m % 97
+    ps = [ctx.Process(target=_gather_worker, args=(r, world, port, m, q)) for r in range(world)]
+    for p_ in ps:
+        p_.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p_ in ps:
+        p_.join(timeout=60)
+    assert all(ok for _, ok in res), res
