@@ -300,7 +300,8 @@ def main():
                 "traffic_source": (traffic.get("step", {}) or {}).get("source"),
                 "algorithmic_bytes_per_step": path_bytes, "formula": "SURVEY.md 8(d): per level 8E+2E+34V, "
                 "+10E_l+8E_(l+1) per extraction, +10E final cut",
-                "kernels": rows[:3], "kernels_timed_in": f"{args.workload} level-0 bisection (k=2), CUDA events",
+                "kernels": rows[:3], "kernels_other": rows[3:],   # the remaining marked kernels (round-1 binning)
+                "kernels_timed_in": f"{args.workload} level-0 bisection (k=2), CUDA events",
                 "kernel_share_from": "kernel marks in the profiled k-way step (sum of kernel times across streams)"}
 
     cpu = None
