@@ -327,7 +327,10 @@ __device__ __forceinline__ void cta_range(int64_t m, int64_t& lo, int64_t& hi) {
 }
 
 constexpr int kEdgeThreads = 512;
-constexpr int kDeltaUnroll = 4;
+#ifndef GREM_DELTA_UNROLL
+#define GREM_DELTA_UNROLL 4
+#endif
+constexpr int kDeltaUnroll = GREM_DELTA_UNROLL;
 
 // round 1: every chunk neighbour read with its pre-sweep label (cnt_nbrs,
 // grem.py:82-97 / 138-145); nodes whose counts stay zero get a flag so the
